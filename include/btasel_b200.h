@@ -1,0 +1,131 @@
+/*
+ * btasel_b200 -- C ABI of the B200-native fused BT/BTA selected inversion (SI)
+ * and selected quadratic solution (SQ) solver.
+ *
+ * Drop-in boundary for the reference `btasel` package (arXiv 2601.04904,
+ * /root/reference/pkg/src/btasel).  The reference is pure Python/NumPy and has
+ * no FFI of its own; each entry point below replaces the Python function cited
+ * next to it, and the Python facade in paper_2601_04904_b200/ binds them with
+ * ctypes exactly like the reference functions are called.
+ *
+ * Conventions
+ *  - All matrix pointers are DEVICE pointers (CUDA global memory) unless the
+ *    function name says `_host`.
+ *  - complex128 is stored interleaved (re, im) as two IEEE doubles, blocks
+ *    row-major, block lists stacked contiguously: exactly the numpy layout of
+ *    a list of C-contiguous complex128 blocks and the BTA1 payload order
+ *    (fileio.py:37-49), so host <-> device is one memcpy per array.
+ *  - No exception crosses the ABI: every call returns a bsel_code_t and fills
+ *    the optional status struct (code, index, message).
+ *  - Calls are stream-ordered on the context's stream; they return after
+ *    enqueueing except where noted ("synchronizes").
+ */
+#ifndef BTASEL_B200_H
+#define BTASEL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSEL_ABI_VERSION 1
+
+typedef enum {
+  BSEL_OK = 0,
+  BSEL_ERR_SHAPE = 1,    /* -> ShapeMismatchError      (errors.py:8)      */
+  BSEL_ERR_SINGULAR = 2, /* -> SingularBlockError(index) (errors.py:12-24) */
+  BSEL_ERR_CUDA = 3,     /* -> RuntimeError                                 */
+  BSEL_ERR_ARG = 4,      /* -> ValueError                                   */
+  BSEL_ERR_INTERNAL = 5
+} bsel_code_t;
+
+typedef struct {
+  int32_t code;
+  int32_t reserved;
+  int64_t index; /* singular: global diagonal block index (n for the tip) or
+                    pivot row for bsel_block_inverse; -1 otherwise          */
+  char message[256];
+} bsel_status_t;
+
+/* BtaMatrix (matrix.py:35-72) as stacked device arrays.  a == 0: BT. */
+typedef struct {
+  int64_t n, b, a;
+  double* diag;      /* [n][b][b]                                  */
+  double* lower;     /* [n-1][b][b]  block (i+1, i)                */
+  double* upper;     /* [n-1][b][b]  block (i, i+1)                */
+  double* arrow_row; /* [n][a][b]    block (t, i)                  */
+  double* arrow_col; /* [n][b][a]    block (i, t)                  */
+  double* tip;       /* [a][a]                                     */
+} bsel_bta_t;
+
+/* RgfFactors (rgf.py:37-61) as device arrays. */
+typedef struct {
+  int64_t n, b, a;
+  int32_t fused; /* 1 = "siq", 0 = "si" */
+  int32_t reserved;
+  double* s_a;              /* [n][b][b]   inverted updated pivots          */
+  double* s_b;              /* [n-1][b][b] quadratic Schur blocks (fused)   */
+  double* b_diag_last;      /* [b][b]      (fused)                          */
+  double* tip_inv;          /* [a][a]      tip_schur_inv                    */
+  double* b_tip;            /* [a][a]      (fused)                          */
+  double* arrow_row_elim;   /* [n][a][b]   strips as seen at elimination    */
+  double* arrow_col_elim;   /* [n][b][a]                                    */
+  double* b_arrow_row_elim; /* [n][a][b]   (fused)                          */
+  double* b_arrow_col_elim; /* [n][b][a]   (fused)                          */
+} bsel_factors_t;
+
+typedef struct bsel_context bsel_context_t;
+
+/* ---- context ------------------------------------------------------------ */
+int bsel_abi_version(void);
+int bsel_context_create(int device, bsel_context_t** out, bsel_status_t* st);
+int bsel_context_destroy(bsel_context_t* ctx);
+/* Run subsequent calls on `cuda_stream` (cudaStream_t; NULL = legacy default). */
+int bsel_context_set_stream(bsel_context_t* ctx, void* cuda_stream);
+/* Synchronizes; reports deferred device errors (singular pivots). */
+int bsel_synchronize(bsel_context_t* ctx, bsel_status_t* st);
+/* Device time of the last forward / backward sweep in ms (synchronizes). */
+int bsel_last_timings(bsel_context_t* ctx, double* forward_ms, double* backward_ms);
+
+/* ---- kernels (kernels.py) ----------------------------------------------- */
+/* block_multiply_acc (kernels.py:106-154):
+ *   d = beta*c + alpha*op(a) @ op(b), op = identity or conjugate transpose.
+ *   op(a) is m x k, op(b) is k x n; c may be NULL (then beta is ignored);
+ *   d may alias c.  alpha/beta are complex (re, im).                        */
+int bsel_block_multiply_acc(bsel_context_t* ctx, double* d, int64_t ldd, const double* c, int64_t ldc,
+                            const double* a, int64_t lda, int trans_a, const double* b, int64_t ldb,
+                            int trans_b, int64_t m, int64_t n, int64_t k, double alpha_re, double alpha_im,
+                            double beta_re, double beta_im, bsel_status_t* st);
+/* block_inverse (kernels.py:220-236): out = a^-1 (n x n).  Exactly singular
+ * (partial pivoting meets a zero pivot) -> BSEL_ERR_SINGULAR, index = pivot
+ * row.  Synchronizes.                                                       */
+int bsel_block_inverse(bsel_context_t* ctx, const double* a, int64_t lda, double* out, int64_t ldo,
+                       int64_t n, bsel_status_t* st);
+
+/* ---- sequential solver (rgf.py) ----------------------------------------- */
+/* bt_forward / bta_forward (rgf.py:79, :207): a_work (and b_work, NULL for
+ * "si") are working copies mutated in place; factors are written to `f`
+ * (whose *_elim pointers must alias the working arrow strips or be copies
+ * filled afterwards by the caller).  Synchronizes; singular pivot ->
+ * BSEL_ERR_SINGULAR with the global block index (n for the tip).           */
+int bsel_bta_forward(bsel_context_t* ctx, const bsel_bta_t* a_work, const bsel_bta_t* b_work,
+                     const bsel_factors_t* f, bsel_status_t* st);
+/* bt_backward / bta_backward (rgf.py:127, :401): reads the factors and the
+ * original off-diagonal blocks of a (and b); writes x_a (and x_b).         */
+int bsel_bta_backward(bsel_context_t* ctx, const bsel_factors_t* f, const bsel_bta_t* a, const bsel_bta_t* b,
+                      const bsel_bta_t* x_a, const bsel_bta_t* x_b, int diagonal_only, bsel_status_t* st);
+/* Device workspace (bytes) needed by bsel_solve_selected. */
+int bsel_solve_workspace_size(int64_t n, int64_t b, int64_t a, int fused, size_t* bytes);
+/* solve_selected (rgf.py:497-531): non-destructive forward + backward.
+ * `b`, `x_b` NULL for "si".  workspace: >= bsel_solve_workspace_size bytes
+ * of device memory (NULL: the context allocates it).  Synchronizes.        */
+int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b, const bsel_bta_t* x_a,
+                        const bsel_bta_t* x_b, int diagonal_only, void* workspace, size_t workspace_bytes,
+                        bsel_status_t* st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BTASEL_B200_H */

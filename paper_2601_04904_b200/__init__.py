@@ -1,0 +1,44 @@
+"""B200-native fused BT/BTA selected inversion (SI) and selected quadratic
+solution (SQ): a drop-in for the hot path of `btasel` (arXiv 2601.04904).
+
+Public API mirrors btasel/__init__.py for the hot path:
+
+* containers / generators: BtaMatrix, SelectedSolution, generate_dd_bta,
+  hermitianize, to_dense, mask_to_pattern; DeviceBta (device fast path)
+* sequential solver: solve_selected, bt_forward, bt_backward, bta_forward,
+  bta_backward, RgfFactors
+* distributed solver: dist_solve, local_forward, assemble_reduced,
+  solve_reduced, local_backward, plan_partitions, Collectives
+* kernels: OpCounter, block_multiply_acc, mm, block_inverse
+* errors: the reference's exception hierarchy
+
+Every numerical call runs in libbtasel_b200.so (sm_100a); there is no CPU
+fallback.
+"""
+
+from .errors import (
+    BtaselError,
+    DenseGuardError,
+    NativeUnavailableError,
+    ProtocolError,
+    ShapeMismatchError,
+    SingularBlockError,
+    WorkerError,
+)
+from .matrix import BtaMatrix, SelectedSolution, generate_dd_bta, hermitianize, mask_to_pattern, to_dense
+from .partition import PartitionPlan, plan_partitions
+from .kernels import OpCounter, block_inverse, block_multiply_acc, mm
+from .device import DeviceBta, to_device, to_host
+from .rgf import RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, solve_selected
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BtaMatrix", "SelectedSolution", "RgfFactors", "OpCounter", "PartitionPlan", "DeviceBta",
+    "generate_dd_bta", "hermitianize", "to_dense", "mask_to_pattern", "to_device", "to_host",
+    "block_multiply_acc", "mm", "block_inverse",
+    "bt_forward", "bt_backward", "bta_forward", "bta_backward", "solve_selected",
+    "plan_partitions",
+    "BtaselError", "ShapeMismatchError", "SingularBlockError", "DenseGuardError", "ProtocolError",
+    "WorkerError", "NativeUnavailableError",
+]

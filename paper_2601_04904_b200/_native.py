@@ -1,0 +1,190 @@
+"""ctypes binding of the C ABI in include/btasel_b200.h (libbtasel_b200.so).
+
+This is the thin layer between the Python facade and the sm_100a library.
+It owns one ``bsel_context`` per CUDA device, maps ABI status codes to the
+reference's exceptions, and never falls back to a CPU implementation: a
+missing library or GPU raises NativeUnavailableError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import NativeUnavailableError, ShapeMismatchError, SingularBlockError
+
+LIB_NAME = "libbtasel_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+OK, ERR_SHAPE, ERR_SINGULAR, ERR_CUDA, ERR_ARG, ERR_INTERNAL = range(6)
+
+# Every symbol include/btasel_b200.h declares (checked by tests/test_abi_exports.py).
+EXPORTS = (
+    "bsel_abi_version",
+    "bsel_context_create",
+    "bsel_context_destroy",
+    "bsel_context_set_stream",
+    "bsel_synchronize",
+    "bsel_last_timings",
+    "bsel_block_multiply_acc",
+    "bsel_block_inverse",
+    "bsel_bta_forward",
+    "bsel_bta_backward",
+    "bsel_solve_workspace_size",
+    "bsel_solve_selected",
+)
+
+
+class Status(ctypes.Structure):
+    _fields_ = [
+        ("code", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("index", ctypes.c_int64),
+        ("message", ctypes.c_char * 256),
+    ]
+
+
+class Bta(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("b", ctypes.c_int64),
+        ("a", ctypes.c_int64),
+        ("diag", ctypes.c_void_p),
+        ("lower", ctypes.c_void_p),
+        ("upper", ctypes.c_void_p),
+        ("arrow_row", ctypes.c_void_p),
+        ("arrow_col", ctypes.c_void_p),
+        ("tip", ctypes.c_void_p),
+    ]
+
+
+class Factors(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("b", ctypes.c_int64),
+        ("a", ctypes.c_int64),
+        ("fused", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("s_a", ctypes.c_void_p),
+        ("s_b", ctypes.c_void_p),
+        ("b_diag_last", ctypes.c_void_p),
+        ("tip_inv", ctypes.c_void_p),
+        ("b_tip", ctypes.c_void_p),
+        ("arrow_row_elim", ctypes.c_void_p),
+        ("arrow_col_elim", ctypes.c_void_p),
+        ("b_arrow_row_elim", ctypes.c_void_p),
+        ("b_arrow_col_elim", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the C ABI.  Does not need a GPU."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise NativeUnavailableError(
+                f"{LIB_NAME} not found at {p}: run __graft_entry__.build() (make -C "
+                "paper_2601_04904_b200/csrc); there is no CPU fallback"
+            )
+        lib = ctypes.CDLL(p)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+        st = ctypes.POINTER(Status)
+        sig = {
+            "bsel_abi_version": ([], i32),
+            "bsel_context_create": ([i32, ctypes.POINTER(vp), st], i32),
+            "bsel_context_destroy": ([vp], i32),
+            "bsel_context_set_stream": ([vp, vp], i32),
+            "bsel_synchronize": ([vp, st], i32),
+            "bsel_last_timings": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], i32),
+            "bsel_block_multiply_acc": (
+                [vp, vp, i64, vp, i64, vp, i64, i32, vp, i64, i32, i64, i64, i64,
+                 ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, st], i32),
+            "bsel_block_inverse": ([vp, vp, i64, vp, i64, i64, st], i32),
+            "bsel_bta_forward": ([vp, ctypes.POINTER(Bta), ctypes.POINTER(Bta), ctypes.POINTER(Factors), st], i32),
+            "bsel_bta_backward": ([vp, ctypes.POINTER(Factors), ctypes.POINTER(Bta), ctypes.POINTER(Bta),
+                                   ctypes.POINTER(Bta), ctypes.POINTER(Bta), i32, st], i32),
+            "bsel_solve_workspace_size": ([i64, i64, i64, i32, ctypes.POINTER(ctypes.c_size_t)], i32),
+            "bsel_solve_selected": ([vp, ctypes.POINTER(Bta), ctypes.POINTER(Bta), ctypes.POINTER(Bta),
+                                     ctypes.POINTER(Bta), i32, vp, ctypes.c_size_t, st], i32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        if lib.bsel_abi_version() != 1:
+            raise NativeUnavailableError("ABI version mismatch")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def raise_for_status(code: int, st: Status) -> None:
+    if code == OK:
+        return
+    msg = st.message.decode(errors="replace")
+    if code == ERR_SINGULAR:
+        raise SingularBlockError(msg, index=int(st.index))
+    if code == ERR_SHAPE:
+        raise ShapeMismatchError(msg)
+    if code == ERR_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(f"btasel_b200 native error {code}: {msg}")
+
+
+class Context:
+    """One bsel_context per device; calls run on torch's current stream."""
+
+    _per_device: dict = {}
+
+    def __init__(self, device: int):
+        self.lib = load_library()
+        self.device = device
+        handle = ctypes.c_void_p()
+        st = Status()
+        raise_for_status(self.lib.bsel_context_create(device, ctypes.byref(handle), ctypes.byref(st)), st)
+        self.handle = handle
+
+    @classmethod
+    def get(cls, device: int | None = None) -> "Context":
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeUnavailableError("no CUDA device: the B200 solver has no CPU fallback")
+        if device is None:
+            device = torch.cuda.current_device()
+        ctx = cls._per_device.get(device)
+        if ctx is None:
+            with torch.cuda.device(device):
+                ctx = cls(device)
+            cls._per_device[device] = ctx
+        ctx.bind_stream()
+        return ctx
+
+    def bind_stream(self, stream=None) -> None:
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.lib.bsel_context_set_stream(self.handle, ctypes.c_void_p(s.cuda_stream))
+
+    def call(self, name: str, *args) -> None:
+        st = Status()
+        code = getattr(self.lib, name)(self.handle, *args, ctypes.byref(st))
+        raise_for_status(code, st)
+
+    def timings(self) -> tuple[float, float]:
+        f, b = ctypes.c_double(), ctypes.c_double()
+        self.lib.bsel_last_timings(self.handle, ctypes.byref(f), ctypes.byref(b))
+        return f.value, b.value
+
+    def workspace_bytes(self, n: int, b: int, a: int, fused: bool) -> int:
+        out = ctypes.c_size_t()
+        self.lib.bsel_solve_workspace_size(n, b, a, int(fused), ctypes.byref(out))
+        return out.value

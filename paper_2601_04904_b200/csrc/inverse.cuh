@@ -1,0 +1,40 @@
+// Complex128 block inverse for the RGF pivots (replaces block_inverse /
+// _lu_packed, pkg/src/btasel/kernels.py:169-236, and _invert_pivot,
+// pkg/src/btasel/rgf.py:64-71).
+//
+// Fast path: blocked Gauss-Jordan with kLeaf-wide panels.  Each panel's
+// diagonal leaf is inverted with partial pivoting inside one CTA (shared
+// memory, no physical row swaps); the panel is then applied to the whole
+// matrix with the grouped DMMA GEMM (zgemm.cuh).  This is exact block
+// Gauss-Jordan, stable for the (block) diagonally dominant pivots the RGF
+// produces.  Drop-in semantics of the reference (error iff LAPACK-style
+// partial pivoting meets an exactly zero pivot) are preserved by an exact
+// fallback: when a leaf meets an exactly zero pivot, a full-column
+// partial-pivoting Gauss-Jordan of the untouched input runs on device and
+// only it decides singularity.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bsel {
+
+constexpr int kLeaf = 32;
+
+// Workspace (complex elements) needed by launch_block_inverse for one n x n.
+int64_t block_inverse_workspace(int n);
+
+// Y = inv(X) for one n x n matrix (X untouched, Y must not alias X).
+//  work   : block_inverse_workspace(n) complex elements
+//  flag   : one device int, 0 on entry; 1 = leaf met a zero pivot (fallback ran),
+//           2 + row = exactly singular at pivot row `row`
+//  status : optional device u64; on exact singularity atomicMin(status, key)
+cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n,
+                                 double2* work, int* flag, unsigned long long* status,
+                                 unsigned long long key, cudaStream_t stream);
+
+// Batched small inverses (n <= kLeaf) in one launch: Y_b = inv(X_b).
+cudaError_t launch_leaf_inverse_batched(const double2* X, int64_t ldx, int64_t strideX, double2* Y,
+                                        int64_t ldy, int64_t strideY, int n, int batch, int* flags,
+                                        cudaStream_t stream);
+
+}  // namespace bsel

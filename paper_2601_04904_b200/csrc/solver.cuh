@@ -1,0 +1,108 @@
+// Device-side sequential RGF solver: forward Schur sweep, fused SI+SQ
+// backward sweep, arrowhead tip update (pkg/src/btasel/rgf.py) and the
+// distributed partition kernels (pkg/src/btasel/dist.py), expressed as
+// stream-ordered levels of grouped DMMA GEMMs plus block inverses.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "level.cuh"
+
+namespace bsel {
+
+// Stacked BT(A) matrix in device memory (see include/btasel_b200.h).
+struct BtaDev {
+  int64_t n = 0, b = 0, a = 0;
+  double2* diag = nullptr;       // [n][b][b]
+  double2* lower = nullptr;      // [n-1][b][b]   block (i+1, i)
+  double2* upper = nullptr;      // [n-1][b][b]   block (i, i+1)
+  double2* arrow_row = nullptr;  // [n][a][b]     block (t, i)
+  double2* arrow_col = nullptr;  // [n][b][a]     block (i, t)
+  double2* tip = nullptr;        // [a][a]
+  Mat D(int64_t i) const { return blk(diag, i, (int)b, (int)b); }
+  Mat L(int64_t i) const { return blk(lower, i, (int)b, (int)b); }
+  Mat U(int64_t i) const { return blk(upper, i, (int)b, (int)b); }
+  Mat AR(int64_t i) const { return blk(arrow_row, i, (int)a, (int)b); }
+  Mat AC(int64_t i) const { return blk(arrow_col, i, (int)b, (int)a); }
+  Mat T() const { return Mat{tip, a, (int)a, (int)a}; }
+};
+
+// RgfFactors (rgf.py:37-61) in device memory.
+struct FactorsDev {
+  int64_t n = 0, b = 0, a = 0;
+  bool fused = false;
+  double2* s_a = nullptr;             // [n][b][b]
+  double2* s_b = nullptr;             // [n-1][b][b]           (fused)
+  double2* b_diag_last = nullptr;     // [b][b]                (fused)
+  double2* tip_inv = nullptr;         // [a][a]                (a > 0)
+  double2* b_tip = nullptr;           // [a][a]                (fused, a > 0)
+  double2* arrow_row_elim = nullptr;  // [n][a][b]
+  double2* arrow_col_elim = nullptr;  // [n][b][a]
+  double2* b_arrow_row_elim = nullptr;
+  double2* b_arrow_col_elim = nullptr;
+  Mat SA(int64_t i) const { return blk(s_a, i, (int)b, (int)b); }
+  Mat SB(int64_t i) const { return blk(s_b, i, (int)b, (int)b); }
+  Mat ARe(int64_t i) const { return blk(arrow_row_elim, i, (int)a, (int)b); }
+  Mat ACe(int64_t i) const { return blk(arrow_col_elim, i, (int)b, (int)a); }
+  Mat BRe(int64_t i) const { return blk(b_arrow_row_elim, i, (int)a, (int)b); }
+  Mat BCe(int64_t i) const { return blk(b_arrow_col_elim, i, (int)b, (int)a); }
+};
+
+struct SingularInfo {
+  bool singular = false;
+  int64_t index = -1;
+};
+
+class Context {
+ public:
+  explicit Context(int device);
+  ~Context();
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  void set_stream(cudaStream_t s) { user_stream_ = s; }
+  cudaStream_t stream() const { return user_stream_; }
+  cudaStream_t aux() const { return aux_; }
+  int device() const { return device_; }
+
+  // Scratch: `count` temporaries of (r x c) complex, grow-only.
+  double2* scratch(int64_t elems);
+  // Temporary block slot k of size (r x c) inside the slot pool.
+  Mat tmp(int slot, int r, int c);
+  void reserve_slots(int nslots, int64_t slot_elems);
+  double2* inv_work(int64_t elems);
+
+  // Singularity bookkeeping (device side, checked at synchronize()).
+  void reset_status();
+  void invert(Mat X, Mat Y, uint64_t order, int64_t index, cudaStream_t s);
+  SingularInfo read_status();  // synchronizes the user stream
+
+  // Events for cross-stream ordering.
+  cudaEvent_t event(int i);
+  cudaEvent_t timer(int i);
+
+  float last_forward_ms = 0.f, last_backward_ms = 0.f;
+
+ private:
+  int device_;
+  cudaStream_t user_stream_ = nullptr;
+  cudaStream_t aux_ = nullptr;
+  double2* slots_ = nullptr;
+  int64_t slot_elems_ = 0;
+  int nslots_ = 0;
+  double2* inv_work_ = nullptr;
+  int64_t inv_work_elems_ = 0;
+  int* d_flag_ = nullptr;
+  unsigned long long* d_status_ = nullptr;
+  std::vector<cudaEvent_t> events_;
+  cudaEvent_t timers_[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+// rgf.py:79 bt_forward / rgf.py:207 bta_forward.  `A`, `B` are working
+// copies mutated in place (diag, arrow strips, tip); B may be null (SI).
+void bta_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev& F);
+// rgf.py:127 bt_backward / rgf.py:401 bta_backward.
+void bta_backward(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDev* B, const BtaDev& XA,
+                  const BtaDev* XB, bool diagonal_only);
+
+}  // namespace bsel

@@ -1,0 +1,328 @@
+// Grouped multi-term complex128 DMMA GEMM (see zgemm.cuh for the contract).
+//
+// Kernel anatomy (one CTA per output tile, tiles of all problems of a batch
+// flattened into one grid, heaviest problems first):
+//   * multi-stage cp.async pipeline (LDGSTS, zero-fill for ragged edges)
+//     staging op(A) as sA[m][k] and op(B) as sB[k][n] in padded,
+//     bank-conflict-free layouts; conjugate transposes are handled by the
+//     staging addresses (16-byte complex elements are the copy unit);
+//   * warp tiles of (BM/WM) x (BN/WN) complex held in registers as DMMA
+//     8x8 real accumulators (one complex value per thread per tile);
+//   * conjugation / term sign / the -B_im of the real embedding are sign-bit
+//     XORs on the ALU pipe, never FP64 multiplies;
+//   * epilogue fuses the +-addends (the reference's elementwise +/-).
+#include "zgemm.cuh"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace bsel {
+
+namespace {
+
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int BK = 8;                 // complex k per stage
+  static constexpr int THREADS = 32 * WM * WN;
+  static constexpr int WTM = BM / WM;          // warp tile rows (complex)
+  static constexpr int WTN = BN / WN;          // warp tile cols (complex)
+  static constexpr int FM = WTM / 8;           // DMMA row fragments per warp
+  static constexpr int FN = WTN / 4;           // DMMA col fragments per warp (4 complex cols)
+  static constexpr int SA_LD = BK + 2;         // 160 B rows: conflict-free A fragments
+  static constexpr int SB_LD = BN + 2;         // == 32 mod 128 B: conflict-free B fragments
+  static constexpr int SA_ELEMS = BM * SA_LD;
+  static constexpr int SB_ELEMS = BK * SB_LD;
+  static constexpr int A_PER_THREAD = BM * BK / THREADS;
+  static constexpr int B_PER_THREAD = BK * BN / THREADS;
+  static constexpr int SMEM = STAGES * (SA_ELEMS + SB_ELEMS) * 16;
+  static_assert(A_PER_THREAD * THREADS == BM * BK, "A tile split");
+  static_assert(B_PER_THREAD * THREADS == BK * BN, "B tile split");
+  static_assert(FM * 8 == WTM && FN * 4 == WTN, "warp tile");
+};
+
+using Cfg64 = Cfg<64, 64, 2, 4, 4, 2>;
+using Cfg32 = Cfg<32, 32, 2, 2, 4, 4>;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ double xor_sign(double x, unsigned mask) {
+  int hi = __double2hiint(x) ^ static_cast<int>(mask);
+  return __hiloint2double(hi, __double2loint(x));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Chunk iterator over the K-concatenation of the terms of one problem.
+struct ChunkIter {
+  int t;   // term index
+  int k0;  // complex k offset within the term
+};
+
+template <class C>
+__device__ __forceinline__ void load_chunk(const GemmProblem& P, const ChunkIter& it, int m0, int n0,
+                                           double2* sA, double2* sB, int tid) {
+  const GemmTerm& T = P.term[it.t];
+  const int K = T.K, M = P.M, N = P.N, k0 = it.k0;
+  const double2* A = T.A;
+  const double2* B = T.B;
+  const int64_t lda = T.lda, ldb = T.ldb;
+  if (T.opA == kOpN) {
+#pragma unroll
+    for (int j = 0; j < C::A_PER_THREAD; ++j) {
+      int e = tid + j * C::THREADS;
+      int row = e / C::BK, kc = e % C::BK;
+      bool ok = (m0 + row < M) && (k0 + kc < K);
+      const double2* src = ok ? A + (int64_t)(m0 + row) * lda + (k0 + kc) : A;
+      cp_async16(&sA[row * C::SA_LD + kc], src, ok);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::A_PER_THREAD; ++j) {
+      int e = tid + j * C::THREADS;
+      int kc = e / C::BM, row = e % C::BM;
+      bool ok = (m0 + row < M) && (k0 + kc < K);
+      const double2* src = ok ? A + (int64_t)(k0 + kc) * lda + (m0 + row) : A;
+      cp_async16(&sA[row * C::SA_LD + kc], src, ok);
+    }
+  }
+  if (T.opB == kOpN) {
+#pragma unroll
+    for (int j = 0; j < C::B_PER_THREAD; ++j) {
+      int e = tid + j * C::THREADS;
+      int kc = e / C::BN, col = e % C::BN;
+      bool ok = (n0 + col < N) && (k0 + kc < K);
+      const double2* src = ok ? B + (int64_t)(k0 + kc) * ldb + (n0 + col) : B;
+      cp_async16(&sB[kc * C::SB_LD + col], src, ok);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::B_PER_THREAD; ++j) {
+      int e = tid + j * C::THREADS;
+      int col = e / C::BK, kc = e % C::BK;
+      bool ok = (n0 + col < N) && (k0 + kc < K);
+      const double2* src = ok ? B + (int64_t)(n0 + col) * ldb + (k0 + kc) : B;
+      cp_async16(&sB[kc * C::SB_LD + col], src, ok);
+    }
+  }
+}
+
+__device__ __forceinline__ void advance(const GemmProblem& P, ChunkIter& it, int bk) {
+  it.k0 += bk;
+  if (it.k0 >= P.term[it.t].K) {
+    it.k0 = 0;
+    ++it.t;
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+    zgemm_grouped_kernel(const __grid_constant__ GemmBatch batch) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* sA_all = reinterpret_cast<double2*>(smem_raw);
+  double2* sB_all = sA_all + C::STAGES * C::SA_ELEMS;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm = warp / C::WN;
+  const int wn = warp % C::WN;
+
+  // Locate the problem / tile of this CTA.
+  const int bid = blockIdx.x;
+  int pi = 0;
+  while (pi + 1 < batch.nproblems && bid >= batch.p[pi + 1].tile_begin) ++pi;
+  const GemmProblem& P = batch.p[pi];
+  const int local = bid - P.tile_begin;
+  const int m0 = (local / P.tiles_n) * C::BM;
+  const int n0 = (local % P.tiles_n) * C::BN;
+
+  int nchunks = 0;
+  for (int t = 0; t < P.nterms; ++t) nchunks += (P.term[t].K + C::BK - 1) / C::BK;
+
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Skip empty-K terms at the front.
+  ChunkIter ld_it{0, 0};
+  while (ld_it.t < P.nterms && P.term[ld_it.t].K <= 0) ++ld_it.t;
+  ChunkIter cp_it = ld_it;
+
+  // Prologue: fill STAGES-1 stages.
+#pragma unroll
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    if (s < nchunks) {
+      load_chunk<C>(P, ld_it, m0, n0, sA_all + s * C::SA_ELEMS, sB_all + s * C::SB_ELEMS, tid);
+      advance(P, ld_it, C::BK);
+      while (ld_it.t < P.nterms && P.term[ld_it.t].K <= 0) ++ld_it.t;
+    }
+    cp_async_commit();
+  }
+
+  // Per-thread fragment coordinates (constant over the K loop).
+  const int a_row = wm * C::WTM + (lane >> 2);       // + im*8
+  const int a_kc = (lane & 3) >> 1;                  // + kk*2
+  const int a_part = lane & 1;
+  const int b_kc = (lane & 3) >> 1;                  // + kk*2
+  const int b_col = wn * C::WTN + ((lane >> 2) >> 1);  // + jn*4
+  const int b_r = lane & 1, b_s = (lane >> 2) & 1;
+  const int b_comp = b_r ^ b_s;
+
+  int cur_term = -1;
+  unsigned maskA = 0, maskB = 0;
+
+  for (int c = 0; c < nchunks; ++c) {
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nc = c + C::STAGES - 1;
+      if (nc < nchunks) {
+        const int st = nc % C::STAGES;
+        load_chunk<C>(P, ld_it, m0, n0, sA_all + st * C::SA_ELEMS, sB_all + st * C::SB_ELEMS, tid);
+        advance(P, ld_it, C::BK);
+        while (ld_it.t < P.nterms && P.term[ld_it.t].K <= 0) ++ld_it.t;
+      }
+      cp_async_commit();
+    }
+    if (cp_it.t != cur_term) {
+      cur_term = cp_it.t;
+      const GemmTerm& T = P.term[cur_term];
+      const unsigned SIGN = 0x80000000u;
+      maskA = (T.sign < 0 ? SIGN : 0u) ^ ((T.opA == kOpC && a_part) ? SIGN : 0u);
+      // Real embedding of op(B): rows (2k+r), cols (2n+s); value Re if r==s
+      // else Im; negative for (r,s)=(1,0) [op N] or (0,1) [op C: Im -> -Im].
+      if (T.opB == kOpN)
+        maskB = (b_r == 1 && b_s == 0) ? SIGN : 0u;
+      else
+        maskB = (b_r == 0 && b_s == 1) ? SIGN : 0u;
+    }
+    const int st = c % C::STAGES;
+    const double* sAd = reinterpret_cast<const double*>(sA_all + st * C::SA_ELEMS);
+    const double* sBd = reinterpret_cast<const double*>(sB_all + st * C::SB_ELEMS);
+#pragma unroll
+    for (int kk = 0; kk < C::BK / 2; ++kk) {
+      double af[C::FM], bf[C::FN];
+#pragma unroll
+      for (int im = 0; im < C::FM; ++im)
+        af[im] = xor_sign(sAd[((a_row + im * 8) * C::SA_LD + kk * 2 + a_kc) * 2 + a_part], maskA);
+#pragma unroll
+      for (int jn = 0; jn < C::FN; ++jn)
+        bf[jn] = xor_sign(sBd[((kk * 2 + b_kc) * C::SB_LD + b_col + jn * 4) * 2 + b_comp], maskB);
+#pragma unroll
+      for (int im = 0; im < C::FM; ++im)
+#pragma unroll
+        for (int jn = 0; jn < C::FN; ++jn) dmma(acc[im][jn], af[im], bf[jn]);
+    }
+    advance(P, cp_it, C::BK);
+    while (cp_it.t < P.nterms && P.term[cp_it.t].K <= 0) ++cp_it.t;
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: D = acc + sum of signed addends.
+  const int e_row = wm * C::WTM + (lane >> 2);
+  const int e_col = wn * C::WTN + (lane & 3);
+#pragma unroll
+  for (int im = 0; im < C::FM; ++im) {
+    const int m = m0 + e_row + im * 8;
+    if (m >= P.M) continue;
+#pragma unroll
+    for (int jn = 0; jn < C::FN; ++jn) {
+      const int n = n0 + e_col + jn * 4;
+      if (n >= P.N) continue;
+      double re = acc[im][jn][0], imv = acc[im][jn][1];
+      for (int a = 0; a < P.naddends; ++a) {
+        const GemmAddend& X = P.add[a];
+        double2 x = X.X[(int64_t)m * X.ldx + n];
+        if (X.sign > 0) {
+          re += x.x;
+          imv += x.y;
+        } else {
+          re -= x.x;
+          imv -= x.y;
+        }
+      }
+      P.D[(int64_t)m * P.ldd + n] = make_double2(re, imv);
+    }
+  }
+}
+
+template <class C>
+cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm_grouped_kernel<C>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int tiles = 0;
+  for (int i = 0; i < batch.nproblems; ++i) {
+    GemmProblem& P = batch.p[i];
+    P.tiles_n = (P.N + C::BN - 1) / C::BN;
+    P.tile_begin = tiles;
+    tiles += ((P.M + C::BM - 1) / C::BM) * P.tiles_n;
+  }
+  batch.total_tiles = tiles;
+  if (tiles == 0) return cudaSuccess;
+  zgemm_grouped_kernel<C><<<tiles, C::THREADS, C::SMEM, stream>>>(batch);
+  return cudaGetLastError();
+}
+
+int64_t problem_weight(const GemmProblem& P) {
+  int64_t k = 0;
+  for (int t = 0; t < P.nterms; ++t) k += P.term[t].K;
+  return k;
+}
+
+}  // namespace
+
+int device_sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cfg) {
+  // Drop empty problems; heaviest (longest K-concatenation) first so the
+  // long tiles start in the first wave.
+  int w = 0;
+  for (int i = 0; i < batch.nproblems; ++i)
+    if (batch.p[i].M > 0 && batch.p[i].N > 0) {
+      if (w != i) batch.p[w] = batch.p[i];
+      ++w;
+    }
+  batch.nproblems = w;
+  if (w == 0) return cudaSuccess;
+  std::stable_sort(batch.p, batch.p + w, [](const GemmProblem& x, const GemmProblem& y) {
+    return problem_weight(x) > problem_weight(y);
+  });
+  if (tile_cfg == kTileAuto) {
+    int64_t tiles64 = 0;
+    for (int i = 0; i < w; ++i)
+      tiles64 += (int64_t)((batch.p[i].M + 63) / 64) * ((batch.p[i].N + 63) / 64);
+    tile_cfg = (tiles64 >= 2 * device_sm_count()) ? kTile64 : kTile32;
+  }
+  if (tile_cfg == kTile64) return launch_cfg<Cfg64>(batch, stream);
+  return launch_cfg<Cfg32>(batch, stream);
+}
+
+}  // namespace bsel

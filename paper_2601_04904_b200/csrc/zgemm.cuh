@@ -1,0 +1,78 @@
+// Grouped multi-term complex128 GEMM on the FP64 tensor pipe (DMMA) for sm_100a.
+//
+// One launch evaluates up to kMaxProblems independent block products
+//
+//     D = sum_a  s_a * X_a  +  sum_t  s_t * op(A_t) @ op(B_t)      (s = +-1)
+//
+// with op in {N, C} (C = conjugate transpose, never materialised: the
+// transposition is folded into the shared-memory staging addresses and the
+// conjugation into a sign-bit XOR on the fragment registers).  This is the
+// B200 replacement for every `mm(...)` / `block_multiply_acc` call of the
+// reference (pkg/src/btasel/kernels.py:106-166) and for the elementwise
+// +/- combinations around them (e.g. rgf.py:113-118, rgf.py:258-280): the
+// K-concatenated terms share one accumulator tile, the addends are fused
+// into the epilogue.
+//
+// Complex arithmetic uses the real 2x2 embedding: an interleaved complex row
+// of length K is a real row of length 2K, and
+//     C_re = A_il . [B_re ; -B_im],   C_im = A_il . [B_im ; B_re]
+// so each mma.sync.m8n8k4.f64 computes an 8 x 4 (complex) tile over 2
+// complex k.  No flops are wasted (8 real flops per complex MAC).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bsel {
+
+enum : uint8_t { kOpN = 0, kOpC = 1 };
+
+constexpr int kMaxTerms = 6;
+constexpr int kMaxAddends = 3;
+constexpr int kMaxProblems = 16;
+
+struct GemmTerm {
+  const double2* A;   // op(A) is M x K
+  const double2* B;   // op(B) is K x N
+  int64_t lda;        // leading dimension of the STORED A (complex elements)
+  int64_t ldb;
+  int32_t K;
+  uint8_t opA, opB;
+  int8_t sign;        // +1 / -1
+  uint8_t pad_;
+};
+
+struct GemmAddend {
+  const double2* X;   // M x N
+  int64_t ldx;
+  int32_t sign;
+  int32_t pad_;
+};
+
+struct GemmProblem {
+  double2* D;         // M x N output (may alias an addend, never a term operand)
+  int64_t ldd;
+  int32_t M, N;
+  int32_t nterms, naddends;
+  int32_t tiles_n;    // filled by the launcher
+  int32_t tile_begin; // filled by the launcher
+  GemmAddend add[kMaxAddends];
+  GemmTerm term[kMaxTerms];
+};
+
+struct GemmBatch {
+  int32_t nproblems;
+  int32_t total_tiles;
+  GemmProblem p[kMaxProblems];
+};
+
+// Tile configurations (complex tile BM x BN).
+enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2 };
+
+// Launch one grouped batch on `stream`.  Problems with M==0 or N==0 are
+// dropped.  Returns cudaSuccess or the launch error.
+cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cfg = kTileAuto);
+
+// Number of SMs of the current device (cached).
+int device_sm_count();
+
+}  // namespace bsel

@@ -1,0 +1,93 @@
+"""Device-resident BT(A) matrices: stacked torch complex128 tensors.
+
+``DeviceBta`` is the zero-copy fast path of the boundary: its six tensors
+are exactly the arrays of ``bsel_bta_t`` (include/btasel_b200.h).  Host
+``BtaMatrix`` objects convert with one cudaMemcpy per block kind.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native
+from .errors import ShapeMismatchError
+from .matrix import KINDS, BtaMatrix
+
+__all__ = ["DeviceBta", "to_device", "to_host"]
+
+
+def _shapes(n, b, a):
+    return {"diag": (n, b, b), "lower": (n - 1, b, b), "upper": (n - 1, b, b),
+            "arrow_row": (n, a, b), "arrow_col": (n, b, a), "tip": (a, a)}
+
+
+class DeviceBta:
+    """Stacked device arrays of one BT(A) matrix (n, b, a)."""
+
+    def __init__(self, n, b, a, tensors: dict):
+        self.n, self.b, self.a = int(n), int(b), int(a)
+        shapes = _shapes(self.n, self.b, self.a)
+        for k, shp in shapes.items():
+            t = tensors[k]
+            if tuple(t.shape) != shp or t.dtype != torch.complex128 or not t.is_contiguous():
+                raise ShapeMismatchError(f"{k}: expected contiguous complex128 {shp}, got {tuple(t.shape)}")
+            setattr(self, k, t)
+
+    @property
+    def shape_params(self):
+        return (self.n, self.b, self.a)
+
+    @property
+    def device(self):
+        return self.diag.device
+
+    def tensors(self) -> dict:
+        return {k: getattr(self, k) for k in KINDS + ("tip",)}
+
+    @classmethod
+    def empty(cls, n, b, a, device=None, zero=True) -> "DeviceBta":
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        mk = torch.zeros if zero else torch.empty
+        return cls(n, b, a, {k: mk(s, dtype=torch.complex128, device=dev) for k, s in _shapes(n, b, a).items()})
+
+    def clone(self) -> "DeviceBta":
+        return DeviceBta(self.n, self.b, self.a, {k: t.clone() for k, t in self.tensors().items()})
+
+    def desc(self) -> _native.Bta:
+        d = _native.Bta()
+        d.n, d.b, d.a = self.n, self.b, self.a
+        for k, t in self.tensors().items():
+            setattr(d, k, t.data_ptr() if t.numel() else None)
+        return d
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * 16 for t in self.tensors().values())
+
+    def copy_from_host(self, m: BtaMatrix, non_blocking=True) -> "DeviceBta":
+        if m.shape_params != self.shape_params:
+            raise ShapeMismatchError("host/device shape mismatch")
+        for k, arr in m.stacked().items():
+            if arr.size:
+                getattr(self, k).copy_(torch.from_numpy(arr), non_blocking=non_blocking)
+        return self
+
+    def copy_to_host(self, m: BtaMatrix, non_blocking=False) -> BtaMatrix:
+        if m.shape_params != self.shape_params:
+            raise ShapeMismatchError("host/device shape mismatch")
+        for k, arr in m.stacked().items():
+            if arr.size:
+                torch.from_numpy(arr).copy_(getattr(self, k), non_blocking=non_blocking)
+        return m
+
+    def __repr__(self):
+        return f"DeviceBta(n={self.n}, b={self.b}, a={self.a}, device={self.device})"
+
+
+def to_device(m: BtaMatrix, device=None) -> DeviceBta:
+    return DeviceBta.empty(m.n, m.b, m.a, device, zero=False).copy_from_host(m, non_blocking=False)
+
+
+def to_host(d: DeviceBta, *, pinned=False) -> BtaMatrix:
+    out = BtaMatrix.zeros(d.n, d.b, d.a, pinned=pinned)
+    d.copy_to_host(out)
+    return out
