@@ -125,6 +125,18 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
                         const bsel_bta_t* x_b, int diagonal_only, void* workspace, size_t workspace_bytes,
                         bsel_status_t* st);
 
+/* ---- synthetic inputs (matrix.py) --------------------------------------- */
+/* generate_dd_bta (matrix.py:224-284) written straight into device arrays:
+ * bit-identical splitmix64 stream; the dominance shift sums |row| entries
+ * left to right (the host uses pairwise sums: last-bit differences on the
+ * shifted diagonal are possible).                                          */
+int bsel_generate_dd_bta(bsel_context_t* ctx, const bsel_bta_t* out, uint64_t seed, double dominance,
+                         bsel_status_t* st);
+/* hermitianize (matrix.py:337-354) in place: m <- (m + m^H)/2 on the pattern. */
+int bsel_hermitianize(bsel_context_t* ctx, const bsel_bta_t* m, bsel_status_t* st);
+/* Number of CUDA kernels this library has launched in this process.        */
+uint64_t bsel_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ from .errors import (
 from .matrix import BtaMatrix, SelectedSolution, generate_dd_bta, hermitianize, mask_to_pattern, to_dense
 from .partition import PartitionPlan, plan_partitions
 from .kernels import OpCounter, block_inverse, block_multiply_acc, mm
-from .device import DeviceBta, to_device, to_host
+from .device import DeviceBta, generate_dd_bta_device, hermitianize_device, kernel_launches, to_device, to_host
 from .rgf import RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, solve_selected
 
 __version__ = "0.1.0"

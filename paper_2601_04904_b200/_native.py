@@ -33,6 +33,9 @@ EXPORTS = (
     "bsel_bta_backward",
     "bsel_solve_workspace_size",
     "bsel_solve_selected",
+    "bsel_generate_dd_bta",
+    "bsel_hermitianize",
+    "bsel_kernel_launches",
 )
 
 
@@ -115,6 +118,9 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             "bsel_solve_selected": ([vp, ctypes.POINTER(Bta), ctypes.POINTER(Bta), ctypes.POINTER(Bta),
                                      ctypes.POINTER(Bta), i32, vp, ctypes.c_size_t, st], i32),
         }
+        sig["bsel_generate_dd_bta"] = ([vp, ctypes.POINTER(Bta), ctypes.c_uint64, ctypes.c_double, st], i32)
+        sig["bsel_hermitianize"] = ([vp, ctypes.POINTER(Bta), st], i32)
+        sig["bsel_kernel_launches"] = ([], ctypes.c_uint64)
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
             fn.argtypes = args

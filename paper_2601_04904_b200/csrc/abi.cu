@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/btasel_b200.h"
+#include "generate.cuh"
 #include "inverse.cuh"
 #include "solver.cuh"
 
@@ -411,5 +412,25 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
     cuda_check(cudaStreamSynchronize(s), "solve");
   });
 }
+
+int bsel_generate_dd_bta(bsel_context_t* ctx, const bsel_bta_t* out, uint64_t seed, double dominance,
+                         bsel_status_t* st) {
+  return guarded(st, [&] {
+    if (!ctx) throw ArgError("ctx is NULL");
+    check_shape(out, "out");
+    if (dominance < 1.0) throw ArgError("dominance must be >= 1");
+    cuda_check(generate_dd_bta_device(to_dev(*out), seed, dominance, ctx->impl->stream()), "generate");
+  });
+}
+
+int bsel_hermitianize(bsel_context_t* ctx, const bsel_bta_t* m, bsel_status_t* st) {
+  return guarded(st, [&] {
+    if (!ctx) throw ArgError("ctx is NULL");
+    check_shape(m, "m");
+    cuda_check(hermitianize_device(to_dev(*m), ctx->impl->stream()), "hermitianize");
+  });
+}
+
+uint64_t bsel_kernel_launches(void) { return launch_count(); }
 
 }  // extern "C"

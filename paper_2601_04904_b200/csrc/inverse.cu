@@ -234,6 +234,7 @@ cudaError_t launch_leaf_inverse_batched(const double2* X, int64_t ldx, int64_t s
   if (n > kLeaf) return cudaErrorInvalidValue;
   leaf_inverse_kernel<kLeaf, kLeafThreads>
       <<<batch, kLeafThreads, 0, stream>>>(X, ldx, strideX, Y, ldy, strideY, n, flags, 1);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -255,6 +256,7 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     // 1. leaf: W[J,J] = inv(R[J,J])
     leaf_inverse_kernel<kLeaf, kLeafThreads><<<1, kLeafThreads, 0, stream>>>(
         R + (int64_t)j0 * ldr + j0, ldr, 0, W + (int64_t)j0 * ldw + j0, ldw, 0, jb, flag, 0);
+    count_launch();
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (panels == 1) break;
     const double2* Dinv = W + (int64_t)j0 * ldw + j0;
@@ -324,6 +326,7 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     smem_set = smem;
   }
   exact_inverse_kernel<<<1, 1024, smem, stream>>>(X, ldx, Y, ldy, n, work, flag, status, key);
+  count_launch();
   return cudaGetLastError();
 }
 

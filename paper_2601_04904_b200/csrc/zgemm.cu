@@ -14,6 +14,7 @@
 #include "zgemm.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 
 namespace bsel {
@@ -279,6 +280,7 @@ cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
   batch.total_tiles = tiles;
   if (tiles == 0) return cudaSuccess;
   zgemm_grouped_kernel<C><<<tiles, C::THREADS, C::SMEM, stream>>>(batch);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -289,6 +291,12 @@ int64_t problem_weight(const GemmProblem& P) {
 }
 
 }  // namespace
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int device_sm_count() {
   static int sms = 0;

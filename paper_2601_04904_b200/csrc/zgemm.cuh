@@ -75,4 +75,8 @@ cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cf
 // Number of SMs of the current device (cached).
 int device_sm_count();
 
+// Process-wide count of kernels launched by this library (bench evidence).
+void count_launch(uint64_t k = 1);
+uint64_t launch_count();
+
 }  // namespace bsel

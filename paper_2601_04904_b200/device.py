@@ -13,7 +13,7 @@ from . import _native
 from .errors import ShapeMismatchError
 from .matrix import KINDS, BtaMatrix
 
-__all__ = ["DeviceBta", "to_device", "to_host"]
+__all__ = ["DeviceBta", "to_device", "to_host", "generate_dd_bta_device", "hermitianize_device", "kernel_launches"]
 
 
 def _shapes(n, b, a):
@@ -91,3 +91,36 @@ def to_host(d: DeviceBta, *, pinned=False) -> BtaMatrix:
     out = BtaMatrix.zeros(d.n, d.b, d.a, pinned=pinned)
     d.copy_to_host(out)
     return out
+
+
+def generate_dd_bta_device(n, b, a, seed, dominance=1.5, device=None) -> DeviceBta:
+    """generate_dd_bta (matrix.py:224-284) computed on the GPU: the same
+    splitmix64 stream bit for bit; the dominance shift's |row| sums are
+    accumulated sequentially (host: numpy pairwise), so shifted diagonal
+    entries may differ from the host generator in the last bit."""
+    import ctypes
+
+    if n < 1 or b < 1 or a < 0:
+        raise ValueError(f"invalid shape parameters (n={n}, b={b}, a={a})")
+    ctx = _native.Context.get(None if device is None else torch.device(device).index)
+    out = DeviceBta.empty(n, b, a, torch.device("cuda", ctx.device), zero=False)
+    d = out.desc()
+    ctx.bind_stream()
+    ctx.call("bsel_generate_dd_bta", ctypes.byref(d), int(seed) & 0xFFFFFFFFFFFFFFFF, float(dominance))
+    return out
+
+
+def hermitianize_device(m: DeviceBta) -> DeviceBta:
+    """In-place (m + m^H)/2 on the pattern (matrix.py:337-354); returns m."""
+    import ctypes
+
+    ctx = _native.Context.get(m.device.index)
+    d = m.desc()
+    ctx.bind_stream()
+    ctx.call("bsel_hermitianize", ctypes.byref(d))
+    return m
+
+
+def kernel_launches() -> int:
+    """Kernels launched by libbtasel_b200.so in this process."""
+    return int(_native.load_library().bsel_kernel_launches())
