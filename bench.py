@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark: ms per energy point of the fused BTA SI+SQ solve (BASELINE.json).
+
+Workload at N=1: BASELINE config 4 (the north-star shape, fits one B200):
+BTA n_blocks=1024, block=512, tip=256, complex128, bench-protocol synthetic
+inputs A = generate_dd_bta(seed 0), B = hermitianize(generate_dd_bta(seed 1))
+generated on the device (same splitmix64 stream as the reference generator).
+A "step" = one full SI+SQ solve of one energy point.  N>1 (torchrun): the
+same energy point partitioned across N GPUs with the paper's distributed
+scheme (strong scaling).
+
+Prints ONE JSON line (rank 0).  `value` is device-timed with inputs resident
+in HBM (inputs = 32 GiB >> 126 MB L2, so no flush is needed); `e2e` is the
+same metric through the public API with pinned host buffers (H2D of A, B and
+D2H of X_A, X_B inside the timed region).  `--impl reference` times the CPU
+reference path (the oracle port of btasel on the host cores) on a bounded
+sample and extrapolates to the full workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (n, b, a, config index in BASELINE.json)
+    "cfg4": (1024, 512, 256, 3),
+    "cfg3": (128, 512, 64, 2),
+    "cfg2": (64, 256, 0, 1),
+    "cfg5": (256, 1024, 256, 4),
+}
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+METRIC = "ms per energy point, fused BTA SI+SQ at 1/2/4/8 B200; % FP64 TC peak"
+
+
+def flops_seq(n, b, a, mode="siq"):
+    """Reference sequential op inventory (8 real flops per complex MAC, 8N^3
+    per inverse), summed from the per-step tables (kernels.record_sweep)."""
+    from paper_2601_04904_b200.kernels import OpCounter, record_sweep
+
+    c = OpCounter(b=b, a=a)
+    record_sweep(c, n, b, a, mode, "forward")
+    record_sweep(c, n, b, a, mode, "backward")
+    dim = {"b": b, "a": a}
+    total = 0.0
+    for label, cnt in c.gemm_by_shape.items():
+        m, k, nn = (dim[ch] if ch in dim else 0 for ch in label)
+        total += 8.0 * m * k * nn * cnt
+    total += 8.0 * n * b ** 3 + (8.0 * a ** 3 if a else 0.0)
+    return total
+
+
+def fp64_peak_tflops():
+    try:
+        with open(FP64_PEAK_FILE) as fh:
+            d = json.load(fh)
+        return max(d["dmma_m8n8k4_w8_tflops"], d["dmma_m8n8k4_w16_tflops"]), "measured DMMA mma.sync f64 loop (profiles/fp64_peak_r01.json)"
+    except Exception:  # pragma: no cover
+        return 37.2, "nominal 148 SM x 128 flop/clk x 1965 MHz"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(n_s, b, a, threads=None):
+    """Time the CPU reference path (oracle port of btasel, NumPy/SciPy on the
+    host BLAS) on an n_s-block sample of the workload.  Returns seconds."""
+    import oracle  # CPU baseline leg only
+
+    A = oracle.generate_dd_bta(n_s, b, a, seed=0)
+    B = oracle.hermitianize(oracle.generate_dd_bta(n_s, b, a, seed=1))
+    t0 = time.perf_counter()
+    oracle.solve_selected(A, B, "siq")
+    return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, n, b, a):
+    """--impl reference: CPU reference path on rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_s = args.cpu_sample_n
+    for _ in range(args.warmup):
+        cpu_sample(n_s, b, a)
+    times = [cpu_sample(n_s, b, a) for _ in range(args.steps)]
+    per = statistics.mean(times) / n_s * n * 1e3
+    sample = (f"oracle port of btasel solve_selected (NumPy/SciPy, OpenBLAS default threads) on "
+              f"n={n_s} of {n} blocks (b={b}, a={a}), extrapolated linearly in n (reference acceptance "
+              f"criterion 7)")
+    cores = host_cores()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": per, "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": args.workload, "n_blocks": n, "block": b, "tip": a, "mode": "siq"},
+        "cpu_baseline": {"value": per, "unit": "ms", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": per, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=None, help="override n_blocks (debug)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=8)
+    args = ap.parse_args()
+    n, b, a, cfg_idx = WORKLOADS[args.workload]
+    if args.n:
+        n = args.n
+    if args.impl == "reference":
+        return run_reference(args, n, b, a)
+
+    import torch
+
+    import paper_2601_04904_b200 as bs
+    from paper_2601_04904_b200 import _native
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        from paper_2601_04904_b200 import dist as bdist
+
+    # ---- inputs, generated on device --------------------------------------
+    t_gen = time.perf_counter()
+    A = bs.generate_dd_bta_device(n, b, a, seed=0, device=dev)
+    B = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=1, device=dev))
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+
+    if world == 1:
+        XA, XB = bs.DeviceBta.empty(n, b, a, dev, zero=False), bs.DeviceBta.empty(n, b, a, dev, zero=False)
+        ctx = _native.Context.get(local)
+        ws = torch.empty(ctx.workspace_bytes(n, b, a, True), dtype=torch.uint8, device=dev)
+
+        def step():
+            bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws)
+    else:
+        solver = bdist.DistSolver(A, B, "siq", world, rank, dev)
+
+        def step():
+            solver.solve()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region --------------------------------------
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = bs.kernel_launches()
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            step()
+        end.record()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    ms = start.elapsed_time(end) / args.steps
+    launches = (bs.kernel_launches() - launches0) // args.steps
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = clk.summary()
+
+    # ---- live per-kernel timing of the dominant kernel (one extra step) ----
+    prof = _native.Profile()
+    lib = _native.load_library()
+    lib.bsel_profile_begin()
+    step()
+    lib.bsel_profile_end(prof)
+    peak, peak_src = fp64_peak_tflops()
+    gemm_tflops = prof.gemm_flops / (prof.gemm_ms * 1e-3) / 1e12 if prof.gemm_ms > 0 else None
+    F = flops_seq(n, b, a)
+    achieved_step = F / (ms * 1e-3) / 1e12
+
+    # ---- end-to-end through the public API with pinned host buffers -------
+    e2e = None
+    if not args.no_e2e and world == 1:
+        hA = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
+        hB = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
+        A.copy_to_host(hA)
+        B.copy_to_host(hB)
+        del XA, XB
+        A = B = None
+        torch.cuda.empty_cache()
+        hXA = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
+        hXB = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
+        bs.solve_selected(hA, hB, "siq", out=(hXA, hXB), workspace=ws)  # warm allocator
+        torch.cuda.synchronize()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        for _ in range(args.steps):
+            bs.solve_selected(hA, hB, "siq", out=(hXA, hXB), workspace=ws)
+        e2.record()
+        torch.cuda.synchronize()
+        e2e_ms = s2.elapsed_time(e2) / args.steps
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": hA.nbytes + hB.nbytes,
+               "d2h_bytes_per_step": hXA.nbytes + hXB.nbytes}
+
+    # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
+    cpu = None
+    if not args.no_cpu and world == 1 and rank == 0:
+        n_s = args.cpu_sample_n
+        t_s = cpu_sample(n_s, b, a)
+        cpu = {"value": t_s / n_s * n * 1e3, "unit": "ms", "cores": host_cores(), "kind": "port",
+               "sample": f"oracle port (NumPy/SciPy, OpenBLAS default threads) solve_selected on n={n_s} of "
+                         f"{n} blocks (b={b}, a={a}) took {t_s:.2f} s; extrapolated linearly in n"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (device splitmix64 generator, bench protocol seeds 0/1)",
+            "config": {"workload": f"{args.workload}: BASELINE.json configs[{cfg_idx}]", "n_blocks": n, "block": b,
+                       "tip": a, "mode": "siq", "parallelism": f"partitions{world}" if world > 1 else "single",
+                       "l2": "inputs 32 GiB >> 126 MB L2 (no flush needed)" if args.workload == "cfg4" else "inputs > L2"},
+            "fp64_tflops_step": achieved_step,
+            "pct_fp64_peak_step": 100.0 * achieved_step / peak,
+            "flops_per_step": F,
+            "roofline": {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA)", "achieved": gemm_tflops,
+                         "peak": peak, "unit": "TFLOP/s", "frac": (gemm_tflops / peak) if gemm_tflops else None,
+                         "traffic": None, "peak_source": peak_src,
+                         "share_of_step": prof.gemm_ms / ms if ms else None,
+                         "inverse_ms_per_step": prof.inverse_ms, "gemm_launches_per_step": prof.gemm_launches},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "input_generation_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -137,6 +137,19 @@ int bsel_hermitianize(bsel_context_t* ctx, const bsel_bta_t* m, bsel_status_t* s
 /* Number of CUDA kernels this library has launched in this process.        */
 uint64_t bsel_kernel_launches(void);
 
+/* ---- instrumentation ------------------------------------------------------ */
+typedef struct {
+  int64_t gemm_launches; /* grouped DMMA GEMM launches (outside inverses)   */
+  double gemm_flops;     /* sum of 8*M*N*K over their products            */
+  double gemm_ms;        /* sum of their CUDA-event durations              */
+  int64_t inverse_calls; /* block inverses                                  */
+  double inverse_ms;     /* sum of their CUDA-event durations              */
+} bsel_profile_t;
+/* Bracket every launch with CUDA events on its stream until _end (which
+ * synchronizes the device and returns the totals).                        */
+int bsel_profile_begin(void);
+int bsel_profile_end(bsel_profile_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,8 @@ EXPORTS = (
     "bsel_generate_dd_bta",
     "bsel_hermitianize",
     "bsel_kernel_launches",
+    "bsel_profile_begin",
+    "bsel_profile_end",
 )
 
 
@@ -81,6 +83,16 @@ class Factors(ctypes.Structure):
     ]
 
 
+class Profile(ctypes.Structure):
+    _fields_ = [
+        ("gemm_launches", ctypes.c_int64),
+        ("gemm_flops", ctypes.c_double),
+        ("gemm_ms", ctypes.c_double),
+        ("inverse_calls", ctypes.c_int64),
+        ("inverse_ms", ctypes.c_double),
+    ]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -121,6 +133,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         sig["bsel_generate_dd_bta"] = ([vp, ctypes.POINTER(Bta), ctypes.c_uint64, ctypes.c_double, st], i32)
         sig["bsel_hermitianize"] = ([vp, ctypes.POINTER(Bta), st], i32)
         sig["bsel_kernel_launches"] = ([], ctypes.c_uint64)
+        sig["bsel_profile_begin"] = ([], i32)
+        sig["bsel_profile_end"] = ([ctypes.POINTER(Profile)], i32)
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
             fn.argtypes = args

@@ -433,4 +433,21 @@ int bsel_hermitianize(bsel_context_t* ctx, const bsel_bta_t* m, bsel_status_t* s
 
 uint64_t bsel_kernel_launches(void) { return launch_count(); }
 
+int bsel_profile_begin(void) {
+  profile_begin();
+  return BSEL_OK;
+}
+
+int bsel_profile_end(bsel_profile_t* out) {
+  ProfileTotals t = profile_end();
+  if (out) {
+    out->gemm_launches = t.gemm_launches;
+    out->gemm_flops = t.gemm_flops;
+    out->gemm_ms = t.gemm_ms;
+    out->inverse_calls = t.inverse_calls;
+    out->inverse_ms = t.inverse_ms;
+  }
+  return BSEL_OK;
+}
+
 }  // extern "C"

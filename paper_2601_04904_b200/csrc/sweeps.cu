@@ -77,8 +77,14 @@ void Context::invert(Mat X, Mat Y, uint64_t order, int64_t index, cudaStream_t s
   if (X.r != X.c || Y.r != X.r || Y.c != X.c) throw ShapeError("inverse needs square blocks");
   const unsigned long long key = (order << 32) | (uint64_t)(uint32_t)index;
   double2* work = inv_work(std::max<int64_t>(block_inverse_workspace(X.r), 1));
-  cuda_check(launch_block_inverse(X.p, X.ld, Y.p, Y.ld, X.r, work, d_flag_, d_status_, key, s),
-             "block inverse");
+  // Inner GEMM launches of the inverse are attributed to the inverse, not the GEMM kernel.
+  const bool prof = profiling();
+  int id = prof ? profile_open(s) : -1;
+  if (prof) profile_suspend(true);
+  cudaError_t e = launch_block_inverse(X.p, X.ld, Y.p, Y.ld, X.r, work, d_flag_, d_status_, key, s);
+  if (prof) profile_suspend(false);
+  profile_close(id, s, 1, 8.0 * X.r * (double)X.r * X.r);
+  cuda_check(e, "block inverse");
 }
 
 SingularInfo Context::read_status() {

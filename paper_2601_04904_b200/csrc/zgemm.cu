@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <vector>
 
 namespace bsel {
 
@@ -279,8 +280,17 @@ cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
   }
   batch.total_tiles = tiles;
   if (tiles == 0) return cudaSuccess;
+  int prof = -1;
+  double flops = 0.0;
+  if (profiling()) {
+    for (int i = 0; i < batch.nproblems; ++i)
+      for (int t = 0; t < batch.p[i].nterms; ++t)
+        flops += 8.0 * batch.p[i].M * (double)batch.p[i].N * batch.p[i].term[t].K;
+    prof = profile_open(stream);
+  }
   zgemm_grouped_kernel<C><<<tiles, C::THREADS, C::SMEM, stream>>>(batch);
   count_launch();
+  profile_close(prof, stream, 0, flops);
   return cudaGetLastError();
 }
 
@@ -294,6 +304,59 @@ int64_t problem_weight(const GemmProblem& P) {
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
+struct ProfRec {
+  cudaEvent_t t0, t1;
+  int kind;
+  double flops;
+};
+bool g_prof_on = false;
+bool g_prof_suspended = false;
+std::vector<ProfRec> g_prof;
+size_t g_prof_used = 0;
+}  // namespace
+
+void profile_begin() {
+  g_prof_on = true;
+  g_prof_used = 0;
+}
+bool profiling() { return g_prof_on && !g_prof_suspended; }
+void profile_suspend(bool on) { g_prof_suspended = on; }
+int profile_open(cudaStream_t s) {
+  if (!g_prof_on || g_prof_suspended) return -1;
+  if (g_prof_used == g_prof.size()) {
+    ProfRec r{};
+    cudaEventCreate(&r.t0);
+    cudaEventCreate(&r.t1);
+    g_prof.push_back(r);
+  }
+  const int id = (int)g_prof_used++;
+  cudaEventRecord(g_prof[id].t0, s);
+  return id;
+}
+void profile_close(int id, cudaStream_t s, int kind, double flops) {
+  if (id < 0) return;
+  g_prof[id].kind = kind;
+  g_prof[id].flops = flops;
+  cudaEventRecord(g_prof[id].t1, s);
+}
+ProfileTotals profile_end() {
+  ProfileTotals t{};
+  cudaDeviceSynchronize();
+  for (size_t i = 0; i < g_prof_used; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_prof[i].t0, g_prof[i].t1);
+    if (g_prof[i].kind == 0) {
+      ++t.gemm_launches;
+      t.gemm_flops += g_prof[i].flops;
+      t.gemm_ms += ms;
+    } else {
+      ++t.inverse_calls;
+      t.inverse_ms += ms;
+    }
+  }
+  g_prof_on = false;
+  g_prof_used = 0;
+  return t;
 }
 void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }

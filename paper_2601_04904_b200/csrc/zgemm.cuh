@@ -79,4 +79,21 @@ int device_sm_count();
 void count_launch(uint64_t k = 1);
 uint64_t launch_count();
 
+// Optional per-launch device timing (CUDA events on the launching stream),
+// used by bench.py to measure the dominant kernel live.  kind 0 = grouped
+// GEMM launch (flops = sum 8*M*N*K), kind 1 = one whole block inverse.
+struct ProfileTotals {
+  int64_t gemm_launches;
+  double gemm_flops;
+  double gemm_ms;
+  int64_t inverse_calls;
+  double inverse_ms;
+};
+void profile_begin();
+ProfileTotals profile_end();
+bool profiling();
+void profile_suspend(bool on);  // temporarily ignore GEMM launches (inside an inverse)
+int profile_open(cudaStream_t s);                          // returns record id (or -1)
+void profile_close(int id, cudaStream_t s, int kind, double flops);
+
 }  // namespace bsel

@@ -84,11 +84,12 @@ def _numpy_alloc(shape):
     return np.zeros(shape, dtype=COMPLEX)
 
 
-def pinned_alloc(shape):
+def pinned_alloc(shape, zero=True):
     """Page-locked host allocation (fast, async-capable H2D/D2H)."""
     import torch
 
-    t = torch.zeros(shape, dtype=torch.complex128, pin_memory=torch.cuda.is_available())
+    mk = torch.zeros if zero else torch.empty
+    t = mk(shape, dtype=torch.complex128, pin_memory=torch.cuda.is_available())
     return t.numpy()
 
 
@@ -180,8 +181,10 @@ class BtaMatrix:
         return sum(x.nbytes for x in self.stacked().values())
 
     @classmethod
-    def zeros(cls, n, b, a=0, *, pinned=False) -> "BtaMatrix":
-        alloc = pinned_alloc if pinned else _numpy_alloc
+    def zeros(cls, n, b, a=0, *, pinned=False, zero=True) -> "BtaMatrix":
+        """All-zero container; ``pinned`` = page-locked host memory (async
+        transfers); ``zero=False`` skips the fill (pinned only)."""
+        alloc = (lambda s: pinned_alloc(s, zero)) if pinned else _numpy_alloc
         m = cls.__new__(cls)
         m.n, m.b, m.a = int(n), int(b), int(a)
         m._diag, m._lower, m._upper = alloc((n, b, b)), alloc((n - 1, b, b)), alloc((n - 1, b, b))

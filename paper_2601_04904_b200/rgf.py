@@ -257,7 +257,8 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
     B = None
     if fused:
         B = DeviceBta.empty(n, bs, asz, device, zero=False).copy_from_host(b) if host else b
-    if out is not None:
+    host_out = None
+    if out is not None and isinstance(out[0], DeviceBta):
         XA, XB = out
         if diagonal_only:
             XA.lower.zero_()
@@ -266,8 +267,10 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
                 XB.lower.zero_()
                 XB.upper.zero_()
     else:
-        XA = DeviceBta.empty(n, bs, asz, device)
-        XB = DeviceBta.empty(n, bs, asz, device) if fused else None
+        # host outputs (optionally caller-provided, e.g. pinned BtaMatrix.zeros(pinned=True))
+        host_out = out
+        XA = DeviceBta.empty(n, bs, asz, device, zero=diagonal_only or out is None)
+        XB = DeviceBta.empty(n, bs, asz, device, zero=diagonal_only or out is None) if fused else None
     need = ctx.workspace_bytes(n, bs, asz, fused)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=device)
@@ -284,6 +287,13 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
         fwd_ms, bwd_ms = ctx.timings()
         timings["forward"] = fwd_ms / 1e3
         timings["backward"] = bwd_ms / 1e3
+    if host_out is not None:
+        hxa, hxb = host_out
+        XA.copy_to_host(hxa, non_blocking=True)
+        if fused:
+            XB.copy_to_host(hxb, non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()
+        return SelectedSolution(x_a=hxa, x_b=hxb if fused else None, mode=mode)
     if host:
         from .device import to_host
 
