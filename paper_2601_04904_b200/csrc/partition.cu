@@ -1,0 +1,235 @@
+// Partition kernels of the distributed scheme (dist.py:172-416, 542-744):
+// local elimination of one contiguous block range (first: downward into
+// hi-1, last: upward into lo, middle: downward with fill-in to lo) and the
+// seeded local back-substitution.  The collectives between the two phases
+// live in the host layer (NCCL through torch.distributed).
+#include "partition.cuh"
+#include "steps.cuh"
+
+namespace bsel {
+
+namespace {
+
+inline Mat cm(const double2* p, int r, int c) { return Mat{const_cast<double2*>(p), c, r, c}; }
+
+void copy_blocks(Context& ctx, double2* dst, const double2* src, int64_t elems) {
+  if (elems > 0)
+    cuda_check(cudaMemcpyAsync(dst, src, (size_t)elems * sizeof(double2), cudaMemcpyDeviceToDevice,
+                               ctx.stream()),
+               "partition copy");
+}
+
+}  // namespace
+
+void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev& WA, const BtaDev* WB,
+                   const LocalFactorsDev& F) {
+  const int64_t lo = F.lo, hi = F.hi, len = hi - lo, b = A.b, a = A.a;
+  const bool fused = B != nullptr;
+  if (len < 2 || lo < 0 || hi > A.n) throw ShapeError("invalid partition range");
+  if (WA.n != len || WA.b != b || WA.a != a) throw ShapeError("partition workspace shape");
+  const int mx = (int)std::max(a, b);
+  ctx.reserve_slots(40, (int64_t)mx * mx);
+  ctx.reset_status();
+  // Working copies of the partition (dist.py:194-202) and zeroed tip deltas.
+  auto stage = [&](const BtaDev& src, const BtaDev& w) {
+    copy_blocks(ctx, w.diag, src.diag + lo * b * b, len * b * b);
+    copy_blocks(ctx, w.arrow_row, src.arrow_row + lo * a * b, len * a * b);
+    copy_blocks(ctx, w.arrow_col, src.arrow_col + lo * b * a, len * b * a);
+    if (a > 0) cuda_check(cudaMemsetAsync(w.tip, 0, (size_t)(a * a) * sizeof(double2), ctx.stream()), "tip");
+  };
+  stage(A, WA);
+  if (fused) stage(*B, *WB);
+  cuda_check(cudaEventRecord(ctx.timer(0), ctx.stream()), "timer");
+  auto d = [&](const BtaDev& w, int64_t i) { return w.D(i - lo); };
+  auto ar = [&](const BtaDev& w, int64_t i) { return w.AR(i - lo); };
+  auto ac = [&](const BtaDev& w, int64_t i) { return w.AC(i - lo); };
+
+  if (F.kind == kMiddle) {
+    Level L(ctx.stream());
+    L.out(F.FR(1)).add(+1, A.U(lo));
+    L.out(F.FC(1)).add(+1, A.L(lo));
+    if (fused) {
+      L.out(F.BFR(1)).add(+1, B->U(lo));
+      L.out(F.BFC(1)).add(+1, B->L(lo));
+    }
+    L.flush();
+  }
+  streams_fork(ctx);
+  if (F.kind == kFirst || F.kind == kLast) {
+    const bool down = F.kind == kFirst;
+    for (int64_t s = 0; s < len - 1; ++s) {
+      const int64_t i = down ? lo + s : hi - 1 - s;
+      const int64_t j = down ? i + 1 : i - 1;
+      const int64_t e = down ? i : i - 1;  // index of the coupling pair
+      ring_wait(ctx, (int)s);
+      EndStep st;
+      st.Lk = down ? A.L(e) : A.U(e);
+      st.Uk = down ? A.U(e) : A.L(e);
+      st.ad_i = d(WA, i), st.ad_j = d(WA, j), st.ar_i = ar(WA, i), st.ar_j = ar(WA, j);
+      st.ac_i = ac(WA, i), st.ac_j = ac(WA, j), st.tipA = WA.T();
+      st.S = F.SA(i - lo);
+      if (fused) {
+        st.BL = down ? B->L(e) : B->U(e);
+        st.BU = down ? B->U(e) : B->L(e);
+        st.bd_i = d(*WB, i), st.bd_j = d(*WB, j), st.br_i = ar(*WB, i), st.br_j = ar(*WB, j);
+        st.bc_i = ac(*WB, i), st.bc_j = ac(*WB, j), st.tipB = WB->T();
+        st.sb = F.SB(i - lo);
+      }
+      end_step(ctx, st, fused, (uint64_t)s, i, (int)(s & 1));
+    }
+  } else {
+    for (int64_t i = lo + 1; i < hi - 1; ++i) {
+      const int64_t s = i - lo - 1;
+      ring_wait(ctx, (int)s);
+      MiddleStep st;
+      st.L = A.L(i), st.U = A.U(i);
+      st.ad_i = d(WA, i), st.ad_n = d(WA, i + 1), st.ad_lo = d(WA, lo);
+      st.ar_i = ar(WA, i), st.ar_n = ar(WA, i + 1), st.ar_lo = ar(WA, lo);
+      st.ac_i = ac(WA, i), st.ac_n = ac(WA, i + 1), st.ac_lo = ac(WA, lo), st.tipA = WA.T();
+      st.fill_r = F.FR(i - lo), st.fill_c = F.FC(i - lo);
+      st.nfill_r = F.FR(i - lo + 1), st.nfill_c = F.FC(i - lo + 1);
+      st.S = F.SA(i - lo);
+      if (fused) {
+        st.BL = B->L(i), st.BU = B->U(i);
+        st.bd_i = d(*WB, i), st.bd_n = d(*WB, i + 1), st.bd_lo = d(*WB, lo);
+        st.br_i = ar(*WB, i), st.br_n = ar(*WB, i + 1), st.br_lo = ar(*WB, lo);
+        st.bc_i = ac(*WB, i), st.bc_n = ac(*WB, i + 1), st.bc_lo = ac(*WB, lo), st.tipB = WB->T();
+        st.bfill_r = F.BFR(i - lo), st.bfill_c = F.BFC(i - lo);
+        st.nbfill_r = F.BFR(i - lo + 1), st.nbfill_c = F.BFC(i - lo + 1);
+        st.sb = F.SB(i - lo);
+      }
+      middle_step(ctx, st, fused, (uint64_t)s, i, (int)(s & 1));
+    }
+  }
+  streams_join(ctx);
+  cuda_check(cudaEventRecord(ctx.timer(1), ctx.stream()), "timer");
+}
+
+void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalFactorsDev& F, const BtaDev& WA,
+                    const BtaDev* WB, const BtaDev& XR, const BtaDev* ZR, int64_t k_top, int64_t k_bot,
+                    bool write_tip, const BtaDev& XA, const BtaDev* XB) {
+  const int64_t lo = F.lo, hi = F.hi, len = hi - lo, b = A.b, a = A.a;
+  const bool fused = F.fused;
+  if (fused && (!B || !WB || !ZR || !XB)) throw ShapeError("fused factors require the right-hand side");
+  const int mx = (int)std::max(a, b);
+  ctx.reserve_slots(40, (int64_t)mx * mx);
+  cudaStream_t s = ctx.stream();
+  cuda_check(cudaEventRecord(ctx.timer(2), s), "timer");
+  const Mat ytt = XR.T();
+  const Mat ztt = fused ? ZR->T() : Mat{};
+  Level L(s);
+  if (write_tip) {
+    L.out(XA.T()).add(+1, XR.T());
+    if (fused) L.out(XB->T()).add(+1, ZR->T());
+  }
+  auto seed = [&](int64_t k, int64_t g) {
+    L.out(XA.D(g)).add(+1, XR.D(k));
+    L.out(XA.AC(g)).add(+1, XR.AC(k));
+    L.out(XA.AR(g)).add(+1, XR.AR(k));
+    if (fused) {
+      L.out(XB->D(g)).add(+1, ZR->D(k));
+      L.out(XB->AC(g)).add(+1, ZR->AC(k));
+      L.out(XB->AR(g)).add(+1, ZR->AR(k));
+    }
+  };
+  auto separator = [&](int64_t k) {
+    L.out(XA.L(hi - 1)).add(+1, XR.L(k));
+    L.out(XA.U(hi - 1)).add(+1, XR.U(k));
+    if (fused) {
+      L.out(XB->L(hi - 1)).add(+1, ZR->L(k));
+      L.out(XB->U(hi - 1)).add(+1, ZR->U(k));
+    }
+  };
+  auto el = [&](const BtaDev& w, int64_t i, bool row) { return row ? w.AR(i - lo) : w.AC(i - lo); };
+
+  if (F.kind == kFirst || F.kind == kLast) {
+    const bool down = F.kind == kFirst;
+    if (down) {
+      seed(k_bot, hi - 1);
+      if (hi < A.n) separator(k_bot);
+    } else {
+      seed(k_top, lo);
+    }
+    L.flush();
+    for (int64_t t = 0; t < len - 1; ++t) {
+      const int64_t i = down ? hi - 2 - t : lo + 1 + t;
+      const int64_t p = down ? i + 1 : i - 1;  // previously solved neighbour
+      const int64_t e = down ? i : i - 1;
+      BackStep st;
+      st.k = 2;
+      st.g = F.SA(i - lo);
+      st.rs[0] = down ? A.U(e) : A.L(e), st.rs[1] = el(WA, i, false);
+      st.qs[0] = down ? A.L(e) : A.U(e), st.qs[1] = el(WA, i, true);
+      st.ya[0][0] = XA.D(p), st.ya[0][1] = XA.AC(p), st.ya[1][0] = XA.AR(p), st.ya[1][1] = ytt;
+      st.row[0] = down ? XA.U(e) : XA.L(e), st.row[1] = XA.AC(i);
+      st.col[0] = down ? XA.L(e) : XA.U(e), st.col[1] = XA.AR(i);
+      st.diag = XA.D(i);
+      if (fused) {
+        st.sc = F.SB(i - lo);
+        st.ss[0] = down ? B->U(e) : B->L(e), st.ss[1] = el(*WB, i, false);
+        st.ws[0] = down ? B->L(e) : B->U(e), st.ws[1] = el(*WB, i, true);
+        st.yb[0][0] = XB->D(p), st.yb[0][1] = XB->AC(p), st.yb[1][0] = XB->AR(p), st.yb[1][1] = ztt;
+        st.zrow[0] = down ? XB->U(e) : XB->L(e), st.zrow[1] = XB->AC(i);
+        st.zcol[0] = down ? XB->L(e) : XB->U(e), st.zcol[1] = XB->AR(i);
+        st.zdiag = XB->D(i);
+      }
+      back_step(ctx, s, st);
+    }
+  } else {
+    seed(k_top, lo);
+    seed(k_bot, hi - 1);
+    if (hi < A.n) separator(k_bot);
+    // X(lo, hi-1) / X(hi-1, lo) from the reduced system's fill coupling.
+    Mat yfr = XR.U(k_top), yfc = XR.L(k_top);
+    Mat zfr = fused ? ZR->U(k_top) : Mat{}, zfc = fused ? ZR->L(k_top) : Mat{};
+    if (len == 2) {
+      L.out(XA.U(lo)).add(+1, yfr);
+      L.out(XA.L(lo)).add(+1, yfc);
+      if (fused) {
+        L.out(XB->U(lo)).add(+1, zfr);
+        L.out(XB->L(lo)).add(+1, zfc);
+      }
+    }
+    L.flush();
+    for (int64_t i = hi - 2; i > lo; --i) {
+      const int q = (int)((hi - 2 - i) & 1);
+      const bool last_step = i == lo + 1;
+      BackStep st;
+      st.k = 3;
+      st.g = F.SA(i - lo);
+      st.rs[0] = F.FC(i - lo), st.rs[1] = A.U(i), st.rs[2] = el(WA, i, false);
+      st.qs[0] = F.FR(i - lo), st.qs[1] = A.L(i), st.qs[2] = el(WA, i, true);
+      const Mat y00 = XA.D(lo), y0t = XA.AC(lo), yt0 = XA.AR(lo);
+      st.ya[0][0] = y00, st.ya[0][1] = yfr, st.ya[0][2] = y0t;
+      st.ya[1][0] = yfc, st.ya[1][1] = XA.D(i + 1), st.ya[1][2] = XA.AC(i + 1);
+      st.ya[2][0] = yt0, st.ya[2][1] = XA.AR(i + 1), st.ya[2][2] = ytt;
+      // row[0] = X(i, lo), col[0] = X(lo, i): carried to the next step (ping-pong slots).
+      st.row[0] = last_step ? XA.L(lo) : ctx.tmp(2 * q + 1, (int)b, (int)b);
+      st.col[0] = last_step ? XA.U(lo) : ctx.tmp(2 * q, (int)b, (int)b);
+      st.row[1] = XA.U(i), st.row[2] = XA.AC(i);
+      st.col[1] = XA.L(i), st.col[2] = XA.AR(i);
+      st.diag = XA.D(i);
+      if (fused) {
+        st.sc = F.SB(i - lo);
+        st.ss[0] = F.BFC(i - lo), st.ss[1] = B->U(i), st.ss[2] = el(*WB, i, false);
+        st.ws[0] = F.BFR(i - lo), st.ws[1] = B->L(i), st.ws[2] = el(*WB, i, true);
+        const Mat z00 = XB->D(lo), z0t = XB->AC(lo), zt0 = XB->AR(lo);
+        st.yb[0][0] = z00, st.yb[0][1] = zfr, st.yb[0][2] = z0t;
+        st.yb[1][0] = zfc, st.yb[1][1] = XB->D(i + 1), st.yb[1][2] = XB->AC(i + 1);
+        st.yb[2][0] = zt0, st.yb[2][1] = XB->AR(i + 1), st.yb[2][2] = ztt;
+        st.zrow[0] = last_step ? XB->L(lo) : ctx.tmp(4 + 2 * q + 1, (int)b, (int)b);
+        st.zcol[0] = last_step ? XB->U(lo) : ctx.tmp(4 + 2 * q, (int)b, (int)b);
+        st.zrow[1] = XB->U(i), st.zrow[2] = XB->AC(i);
+        st.zcol[1] = XB->L(i), st.zcol[2] = XB->AR(i);
+        st.zdiag = XB->D(i);
+      }
+      back_step(ctx, s, st);
+      yfr = st.col[0], yfc = st.row[0];
+      if (fused) zfr = st.zcol[0], zfc = st.zrow[0];
+    }
+  }
+  L.flush();
+  cuda_check(cudaEventRecord(ctx.timer(3), s), "timer");
+}
+
+}  // namespace bsel

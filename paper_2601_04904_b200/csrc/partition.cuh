@@ -1,0 +1,45 @@
+// Partition kernels of the distributed scheme (dist.py:172-416, 542-744).
+#pragma once
+#include "solver.cuh"
+
+namespace bsel {
+
+enum PartKind : int { kFirst = 0, kMiddle = 1, kLast = 2 };
+
+// LocalFactors (dist.py:134-151) in device memory; block i of the partition
+// [lo, hi) is stored at index i - lo.  fill_* (middle only) hold the fill
+// couplings A'(lo, i) / A'(i, lo) as seen when block i is eliminated; index
+// len-1 receives the final coupling pair (the AllGather payload).
+struct LocalFactorsDev {
+  int64_t lo = 0, hi = 0, b = 0, a = 0;
+  int kind = kFirst;
+  bool fused = false;
+  double2* s_a = nullptr;         // [len][b][b]
+  double2* s_b = nullptr;         // [len][b][b]   (fused)
+  double2* fill_row = nullptr;    // [len][b][b]   (middle)
+  double2* fill_col = nullptr;    // [len][b][b]   (middle)
+  double2* b_fill_row = nullptr;  // [len][b][b]   (middle, fused)
+  double2* b_fill_col = nullptr;  // [len][b][b]   (middle, fused)
+  Mat SA(int64_t k) const { return blk(s_a, k, (int)b, (int)b); }
+  Mat SB(int64_t k) const { return blk(s_b, k, (int)b, (int)b); }
+  Mat FR(int64_t k) const { return blk(fill_row, k, (int)b, (int)b); }
+  Mat FC(int64_t k) const { return blk(fill_col, k, (int)b, (int)b); }
+  Mat BFR(int64_t k) const { return blk(b_fill_row, k, (int)b, (int)b); }
+  Mat BFC(int64_t k) const { return blk(b_fill_col, k, (int)b, (int)b); }
+};
+
+// dist.py:172-416.  A, B: full original matrices (read only).  WA/WB: the
+// partition's working copies (n = hi - lo blocks; diag / arrow strips; tip
+// receives this rank's tip contribution).  After the call WA/WB hold the
+// eliminated strips and the updated boundary blocks (the payload).
+void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev& WA, const BtaDev* WB,
+                   const LocalFactorsDev& F);
+
+// dist.py:542-744.  XR/ZR: reduced solution; k_top/k_bot: reduced indices of
+// this partition's boundaries; XA/XB: full-size outputs (only this rank's
+// pattern blocks are written; rank 0 also writes the tip).
+void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalFactorsDev& F, const BtaDev& WA,
+                    const BtaDev* WB, const BtaDev& XR, const BtaDev* ZR, int64_t k_top, int64_t k_bot,
+                    bool write_tip, const BtaDev& XA, const BtaDev* XB);
+
+}  // namespace bsel

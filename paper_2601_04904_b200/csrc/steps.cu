@@ -1,0 +1,214 @@
+// Generic elimination / back-substitution steps (see steps.cuh).
+//
+// Stream discipline of the fused forward steps: the A-side Schur chain
+// (pivot inverse, elimination factors, A updates) is issued on the main
+// stream, the quadratic B-side updates on the aux stream.  Temporaries of
+// step k live in ring half (k & 1); before the A side rewrites a ring half
+// it waits for the B side of step k-2 (ring_wait), so the B side may lag the
+// A chain by one full step and the pivot inverse of step k+1 overlaps the
+// B-side GEMM levels of step k.
+#include "steps.cuh"
+
+namespace bsel {
+
+namespace {
+constexpr int kRing = 8;        // slots per ring half
+constexpr int kBackBase = 16;   // first slot used by back_step
+Mat rt(Context& ctx, int parity, int k, int r, int c) { return ctx.tmp(parity * kRing + k, r, c); }
+}  // namespace
+
+void streams_fork(Context& ctx) {
+  cuda_check(cudaEventRecord(ctx.event(4), ctx.stream()), "fork");
+  cuda_check(cudaStreamWaitEvent(ctx.aux(), ctx.event(4), 0), "fork wait");
+}
+
+void streams_join(Context& ctx) {
+  cuda_check(cudaEventRecord(ctx.event(5), ctx.aux()), "join");
+  cuda_check(cudaStreamWaitEvent(ctx.stream(), ctx.event(5), 0), "join wait");
+}
+
+void ring_wait(Context& ctx, int step) {
+  if (step >= 2) cuda_check(cudaStreamWaitEvent(ctx.stream(), ctx.event(2 + (step & 1)), 0), "ring wait");
+}
+
+void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int parity) {
+  cudaStream_t sA = ctx.stream(), sB = ctx.aux();
+  const int b = st.ad_i.r, a = st.ar_i.r;
+  ctx.invert(st.ad_i, st.S, order, index, sA);
+  const Mat& S = st.S;
+  if (!fused) {
+    // rgf.py:283-288 / dist.py:252-257: right-hand temporaries.
+    Mat t1 = rt(ctx, parity, 0, b, b), t2 = rt(ctx, parity, 1, b, a);
+    Level L(sA);
+    L.out(t1).mm(+1, S, N, st.Uk, N);
+    L.out(t2).mm(+1, S, N, st.ac_i, N);
+    L.flush();
+    L.out(st.ad_j).add(+1, st.ad_j).mm(-1, st.Lk, N, t1, N);
+    L.out(st.ar_j).add(+1, st.ar_j).mm(-1, st.ar_i, N, t1, N);
+    L.out(st.ac_j).add(+1, st.ac_j).mm(-1, st.Lk, N, t2, N);
+    L.out(st.tipA).add(+1, st.tipA).mm(-1, st.ar_i, N, t2, N);
+    L.flush();
+    return;
+  }
+  Mat f = rt(ctx, parity, 0, b, b), g = rt(ctx, parity, 1, a, b), w = rt(ctx, parity, 2, b, b);
+  Mat p = rt(ctx, parity, 3, a, b), k = rt(ctx, parity, 4, b, a), v = rt(ctx, parity, 5, b, b);
+  {
+    Level L(sA);
+    L.out(f).mm(+1, st.Lk, N, S, N);
+    L.out(g).mm(+1, st.ar_i, N, S, N);
+    L.flush();
+    cuda_check(cudaEventRecord(ctx.event(parity), sA), "record A");
+    L.out(st.ad_j).add(+1, st.ad_j).mm(-1, f, N, st.Uk, N);
+    L.out(st.ar_j).add(+1, st.ar_j).mm(-1, g, N, st.Uk, N);
+    L.out(st.ac_j).add(+1, st.ac_j).mm(-1, f, N, st.ac_i, N);
+    L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
+    L.flush();
+  }
+  cuda_check(cudaStreamWaitEvent(sB, ctx.event(parity), 0), "wait A");
+  Level L(sB);
+  L.out(w).mm(+1, S, N, st.bd_i, N);
+  L.out(p).mm(+1, g, N, st.bd_i, N);
+  L.out(k).mm(+1, st.bd_i, N, g, H);
+  L.flush();
+  L.out(st.sb).mm(+1, w, N, S, H);
+  L.flush();
+  L.out(v).mm(+1, st.Lk, N, st.sb, N);
+  L.out(st.br_j).add(+1, st.br_j).mm(-1, g, N, st.BU, N).mm(+1, p, N, f, H).mm(-1, st.br_i, N, f, H);
+  L.out(st.bc_j).add(+1, st.bc_j).mm(-1, f, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, f, N, k, N);
+  L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
+  L.flush();
+  L.out(st.bd_j).add(+1, st.bd_j).mm(+1, v, N, st.Lk, H).mm(-1, st.BL, N, f, H).mm(-1, f, N, st.BU, N);
+  L.flush();
+  cuda_check(cudaEventRecord(ctx.event(2 + parity), sB), "record B");
+}
+
+void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int parity) {
+  cudaStream_t sA = ctx.stream(), sB = ctx.aux();
+  const int b = st.ad_i.r, a = st.ar_i.r;
+  ctx.invert(st.ad_i, st.S, order, index, sA);
+  const Mat& S = st.S;
+  Mat fn = rt(ctx, parity, 0, b, b), fr = rt(ctx, parity, 1, b, b), g = rt(ctx, parity, 2, a, b);
+  {
+    Level L(sA);
+    L.out(fn).mm(+1, st.L, N, S, N);
+    L.out(fr).mm(+1, st.fill_r, N, S, N);
+    L.out(g).mm(+1, st.ar_i, N, S, N);
+    L.flush();
+    if (fused) cuda_check(cudaEventRecord(ctx.event(parity), sA), "record A");
+    L.out(st.nfill_r).mm(-1, fr, N, st.U, N);
+    L.out(st.nfill_c).mm(-1, fn, N, st.fill_c, N);
+    L.out(st.ad_n).add(+1, st.ad_n).mm(-1, fn, N, st.U, N);
+    L.out(st.ad_lo).add(+1, st.ad_lo).mm(-1, fr, N, st.fill_c, N);
+    L.out(st.ar_n).add(+1, st.ar_n).mm(-1, g, N, st.U, N);
+    L.out(st.ar_lo).add(+1, st.ar_lo).mm(-1, g, N, st.fill_c, N);
+    L.out(st.ac_n).add(+1, st.ac_n).mm(-1, fn, N, st.ac_i, N);
+    L.out(st.ac_lo).add(+1, st.ac_lo).mm(-1, fr, N, st.ac_i, N);
+    L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
+    L.flush();
+  }
+  if (!fused) return;
+  cuda_check(cudaStreamWaitEvent(sB, ctx.event(parity), 0), "wait A");
+  Mat w = rt(ctx, parity, 3, b, b), v0 = rt(ctx, parity, 4, b, b), vn = rt(ctx, parity, 5, b, b);
+  Mat p = rt(ctx, parity, 6, a, b);
+  Level L(sB);
+  L.out(w).mm(+1, S, N, st.bd_i, N);
+  L.out(p).mm(+1, g, N, st.bd_i, N);
+  L.flush();
+  L.out(st.sb).mm(+1, w, N, S, H);
+  L.flush();
+  L.out(v0).mm(+1, st.fill_r, N, st.sb, N);
+  L.out(vn).mm(+1, st.L, N, st.sb, N);
+  L.out(st.br_n).add(+1, st.br_n).mm(-1, g, N, st.BU, N).mm(-1, st.br_i, N, fn, H).mm(+1, p, N, fn, H);
+  L.out(st.br_lo).add(+1, st.br_lo).mm(-1, g, N, st.bfill_c, N).mm(-1, st.br_i, N, fr, H).mm(+1, p, N, fr, H);
+  L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
+  L.flush();
+  L.out(st.bd_n).add(+1, st.bd_n).mm(-1, fn, N, st.BU, N).mm(-1, st.BL, N, fn, H).mm(+1, vn, N, st.L, H);
+  L.out(st.nbfill_c).mm(-1, fn, N, st.bfill_c, N).mm(-1, st.BL, N, fr, H).mm(+1, vn, N, st.fill_r, H);
+  L.out(st.nbfill_r).mm(-1, fr, N, st.BU, N).mm(-1, st.bfill_r, N, fn, H).mm(+1, v0, N, st.L, H);
+  L.out(st.bd_lo).add(+1, st.bd_lo).mm(-1, fr, N, st.bfill_c, N).mm(-1, st.bfill_r, N, fr, H)
+      .mm(+1, v0, N, st.fill_r, H);
+  L.out(st.bc_n).add(+1, st.bc_n).mm(-1, fn, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, vn, N, st.ar_i, H);
+  L.out(st.bc_lo).add(+1, st.bc_lo).mm(-1, fr, N, st.bc_i, N).mm(-1, st.bfill_r, N, g, H)
+      .mm(+1, v0, N, st.ar_i, H);
+  L.flush();
+  cuda_check(cudaEventRecord(ctx.event(2 + parity), sB), "record B");
+}
+
+void back_step(Context& ctx, cudaStream_t s, const BackStep& st) {
+  const int k = st.k;
+  const bool fused = st.sc.p != nullptr;
+  const int b = st.g.r;
+  int slot = kBackBase;
+  auto T = [&](int r, int c) { return ctx.tmp(slot++, r, c); };
+  // trailing block sizes d_l: rs_l is (b x d_l)
+  Mat RA[3], CA[3], RZ[3], CZ[3], e[3], f[3];
+  Level L(s);
+  // L1: everything that only needs inputs.
+  for (int j = 0; j < k; ++j) {
+    const int dj = st.rs[j].c;
+    RA[j] = T(b, dj);
+    CA[j] = T(dj, b);
+    L.out(RA[j]);
+    for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, st.ya[l][j], N);
+    L.out(CA[j]);
+    for (int l = 0; l < k; ++l) L.mm(+1, st.ya[j][l], N, st.qs[l], N);
+    if (fused) {
+      RZ[j] = T(b, dj);
+      CZ[j] = T(dj, b);
+      L.out(RZ[j]);
+      for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, st.yb[l][j], N);
+      L.out(CZ[j]);
+      for (int l = 0; l < k; ++l) L.mm(+1, st.yb[j][l], N, st.rs[l], H);
+      e[j] = T(b, dj);
+      f[j] = T(dj, b);
+      L.out(e[j]).mm(+1, st.g, N, st.ss[j], N).mm(-1, st.sc, N, st.qs[j], H);
+      L.out(f[j]).mm(+1, st.ws[j], N, st.g, H).mm(-1, st.qs[j], N, st.sc, N);
+    }
+  }
+  L.flush();
+  // L2: row/column blocks of X_A and X_B, and the quadratic coupling.
+  Mat quad = T(b, b);
+  for (int j = 0; j < k; ++j) {
+    L.out(st.row[j]).mm(-1, st.g, N, RA[j], N);
+    L.out(st.col[j]).mm(-1, CA[j], N, st.g, N);
+    if (fused) {
+      L.out(st.zrow[j]);
+      for (int l = 0; l < k; ++l) L.mm(+1, e[l], N, st.ya[j][l], H);
+      L.mm(-1, st.g, N, RZ[j], N);
+      L.out(st.zcol[j]);
+      for (int l = 0; l < k; ++l) L.mm(+1, st.ya[j][l], N, f[l], N);
+      L.mm(-1, CZ[j], N, st.g, H);
+    }
+  }
+  if (fused) {
+    L.out(quad);
+    for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, CZ[l], N);
+  }
+  L.flush();
+  // L3
+  Mat phi = T(b, b), acc1 = T(b, b), acc2 = T(b, b), gq = T(b, b);
+  L.out(phi);
+  for (int l = 0; l < k; ++l) L.mm(-1, st.row[l], N, st.qs[l], N);
+  if (fused) {
+    L.out(acc1);
+    for (int l = 0; l < k; ++l) L.mm(+1, st.ss[l], N, st.row[l], H);
+    L.out(acc2);
+    for (int l = 0; l < k; ++l) L.mm(+1, st.row[l], N, st.ws[l], N);
+    L.out(gq).mm(+1, st.g, N, quad, N);
+  }
+  L.flush();
+  // L4: diagonal blocks.
+  L.out(st.diag).add(+1, st.g).mm(+1, phi, N, st.g, N);
+  if (fused) {
+    L.out(st.zdiag)
+        .add(+1, st.sc)
+        .mm(+1, phi, N, st.sc, N)
+        .mm(+1, st.sc, N, phi, H)
+        .mm(+1, st.g, N, acc1, N)
+        .mm(+1, acc2, N, st.g, H)
+        .mm(+1, gq, N, st.g, H);
+  }
+  L.flush();
+}
+
+}  // namespace bsel

@@ -1,0 +1,54 @@
+// Generic elimination / back-substitution steps shared by the sequential BTA
+// sweep (rgf.py:237-288, 322-398) and the partition kernels of the
+// distributed scheme (dist.py:211-397, 595-742).
+#pragma once
+#include "solver.cuh"
+
+namespace bsel {
+
+// One downward/upward elimination step of block i into its neighbour j
+// (rgf.py:246-288; dist.py:216-257 first, 265-306 last).
+//   Lk = A(j,i), Uk = A(i,j), BL = B(j,i), BU = B(i,j).
+// Updates ad_j, ar_j, ac_j, tipA (and the B-side counterparts); writes S
+// (and sb).  The A-side chain runs on ctx.stream(), the B side on ctx.aux().
+struct EndStep {
+  Mat Lk, Uk, BL, BU;
+  Mat ad_i, ad_j, ar_i, ar_j, ac_i, ac_j, tipA;
+  Mat bd_i, bd_j, br_i, br_j, bc_i, bc_j, tipB;
+  Mat S, sb;
+};
+void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int parity);
+
+// One interior step of a middle partition with fill-in to its top boundary
+// lo (dist.py:315-396).  fill_* are the couplings before the step, nfill_*
+// receive the updated ones.
+struct MiddleStep {
+  Mat L, U, BL, BU;              // A(i+1,i), A(i,i+1), B(i+1,i), B(i,i+1)
+  Mat ad_i, ad_n, ad_lo, ar_i, ar_n, ar_lo, ac_i, ac_n, ac_lo, tipA;
+  Mat bd_i, bd_n, bd_lo, br_i, br_n, br_lo, bc_i, bc_n, bc_lo, tipB;
+  Mat fill_r, fill_c, bfill_r, bfill_c;
+  Mat nfill_r, nfill_c, nbfill_r, nbfill_c;
+  Mat S, sb;
+};
+void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int parity);
+
+// Wait for the B side of the step that last used ring slot `parity` (call
+// before reusing it) and join both streams at the end of a sweep.
+void ring_wait(Context& ctx, int step);
+void streams_fork(Context& ctx);
+void streams_join(Context& ctx);
+
+// Generic Takahashi back-substitution step with k <= 3 trailing couplings
+// (rgf.py:322-398).  sc.p == nullptr -> selected inversion only.
+struct BackStep {
+  int k = 0;
+  Mat g, sc;
+  Mat rs[3], qs[3], ss[3], ws[3];
+  Mat ya[3][3], yb[3][3];
+  // outputs
+  Mat row[3], col[3], diag;
+  Mat zrow[3], zcol[3], zdiag;
+};
+void back_step(Context& ctx, cudaStream_t s, const BackStep& st);
+
+}  // namespace bsel
