@@ -125,6 +125,37 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
                         const bsel_bta_t* x_b, int diagonal_only, void* workspace, size_t workspace_bytes,
                         bsel_status_t* st);
 
+/* ---- distributed scheme (dist.py) --------------------------------------- */
+/* LocalFactors (dist.py:134-151) of the partition [lo, hi), block i stored
+ * at index i - lo.  fill_* (middle partitions): couplings A'(lo,i)/A'(i,lo)
+ * seen when block i is eliminated; index hi-lo-1 = final coupling pair.   */
+typedef struct {
+  int64_t lo, hi;
+  int32_t kind; /* 0 first, 1 middle, 2 last (plan_partitions kinds)  */
+  int32_t fused;
+  double* s_a;        /* [len][b][b]                                     */
+  double* s_b;        /* [len][b][b]  (fused)                            */
+  double* fill_row;   /* [len][b][b]  (middle)                           */
+  double* fill_col;   /* [len][b][b]  (middle)                           */
+  double* b_fill_row; /* [len][b][b]  (middle, fused)                    */
+  double* b_fill_col; /* [len][b][b]  (middle, fused)                    */
+} bsel_local_factors_t;
+/* local_forward (dist.py:172-416): a, b = full original matrices (read
+ * only); a_work/b_work = partition working arrays (n = hi-lo; diag, arrow
+ * strips; tip receives the rank's tip contribution).  Afterwards the work
+ * arrays hold the retained strips and the boundary payload.  Synchronizes;
+ * singular pivot -> BSEL_ERR_SINGULAR with the global block index.        */
+int bsel_local_forward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b, const bsel_bta_t* a_work,
+                       const bsel_bta_t* b_work, const bsel_local_factors_t* f, bsel_status_t* st);
+/* local_backward (dist.py:542-744): seeded from the reduced solution
+ * (x_red, z_red; boundary indices k_top/k_bot), writes this partition's
+ * pattern blocks of the full-size outputs x_a/x_b (and the tip if
+ * write_tip).                                                              */
+int bsel_local_backward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b,
+                        const bsel_local_factors_t* f, const bsel_bta_t* a_work, const bsel_bta_t* b_work,
+                        const bsel_bta_t* x_red, const bsel_bta_t* z_red, int64_t k_top, int64_t k_bot,
+                        int write_tip, const bsel_bta_t* x_a, const bsel_bta_t* x_b, bsel_status_t* st);
+
 /* ---- synthetic inputs (matrix.py) --------------------------------------- */
 /* generate_dd_bta (matrix.py:224-284) written straight into device arrays:
  * bit-identical splitmix64 stream; the dominance shift sums |row| entries

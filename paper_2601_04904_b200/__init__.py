@@ -30,6 +30,9 @@ from .partition import PartitionPlan, plan_partitions
 from .kernels import OpCounter, block_inverse, block_multiply_acc, mm
 from .device import DeviceBta, generate_dd_bta_device, hermitianize_device, kernel_launches, to_device, to_host
 from .rgf import RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, solve_selected
+from .collectives import Collectives, LocalHub, TorchCollectives, TraceEvent
+from .dist import (BoundaryPayload, DistSolver, LocalFactors, ReducedSystem, assemble_reduced, dist_solve,
+                   local_backward, local_forward, solve_reduced)
 
 __version__ = "0.1.0"
 
@@ -38,7 +41,9 @@ __all__ = [
     "generate_dd_bta", "hermitianize", "to_dense", "mask_to_pattern", "to_device", "to_host",
     "block_multiply_acc", "mm", "block_inverse",
     "bt_forward", "bt_backward", "bta_forward", "bta_backward", "solve_selected",
-    "plan_partitions",
+    "plan_partitions", "dist_solve", "local_forward", "assemble_reduced", "solve_reduced", "local_backward",
+    "BoundaryPayload", "LocalFactors", "ReducedSystem", "DistSolver", "Collectives", "TorchCollectives",
+    "LocalHub", "TraceEvent", "generate_dd_bta_device", "hermitianize_device", "kernel_launches",
     "BtaselError", "ShapeMismatchError", "SingularBlockError", "DenseGuardError", "ProtocolError",
     "WorkerError", "NativeUnavailableError",
 ]

@@ -33,6 +33,8 @@ EXPORTS = (
     "bsel_bta_backward",
     "bsel_solve_workspace_size",
     "bsel_solve_selected",
+    "bsel_local_forward",
+    "bsel_local_backward",
     "bsel_generate_dd_bta",
     "bsel_hermitianize",
     "bsel_kernel_launches",
@@ -83,6 +85,21 @@ class Factors(ctypes.Structure):
     ]
 
 
+class LocalFactors(ctypes.Structure):
+    _fields_ = [
+        ("lo", ctypes.c_int64),
+        ("hi", ctypes.c_int64),
+        ("kind", ctypes.c_int32),
+        ("fused", ctypes.c_int32),
+        ("s_a", ctypes.c_void_p),
+        ("s_b", ctypes.c_void_p),
+        ("fill_row", ctypes.c_void_p),
+        ("fill_col", ctypes.c_void_p),
+        ("b_fill_row", ctypes.c_void_p),
+        ("b_fill_col", ctypes.c_void_p),
+    ]
+
+
 class Profile(ctypes.Structure):
     _fields_ = [
         ("gemm_launches", ctypes.c_int64),
@@ -130,6 +147,10 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             "bsel_solve_selected": ([vp, ctypes.POINTER(Bta), ctypes.POINTER(Bta), ctypes.POINTER(Bta),
                                      ctypes.POINTER(Bta), i32, vp, ctypes.c_size_t, st], i32),
         }
+        lf = ctypes.POINTER(LocalFactors)
+        pb = ctypes.POINTER(Bta)
+        sig["bsel_local_forward"] = ([vp, pb, pb, pb, pb, lf, st], i32)
+        sig["bsel_local_backward"] = ([vp, pb, pb, lf, pb, pb, pb, pb, i64, i64, i32, pb, pb, st], i32)
         sig["bsel_generate_dd_bta"] = ([vp, ctypes.POINTER(Bta), ctypes.c_uint64, ctypes.c_double, st], i32)
         sig["bsel_hermitianize"] = ([vp, ctypes.POINTER(Bta), st], i32)
         sig["bsel_kernel_launches"] = ([], ctypes.c_uint64)

@@ -1,0 +1,152 @@
+"""Communication contract of the distributed solver (mirrors btasel/collectives.py:69-79).
+
+A ``Collectives`` endpoint offers exactly two group operations:
+
+* ``all_gather(payload)`` -> list of every rank's payload, rank-ordered,
+  identical on every rank;
+* ``all_reduce_sum(tensor)`` -> elementwise sum accumulated in FIXED RANK
+  ORDER, so the result is bitwise replicated and deterministic
+  (collectives.py:149-158).
+
+Transports:
+
+* :class:`TorchCollectives` -- one process per GPU over ``torch.distributed``
+  (NCCL over NVLink/NVSwitch on B200; gloo on CPU for host-logic tests).
+  Payloads are device tensors packed into one fixed-size slot per rank and
+  moved with a single ``all_gather_into_tensor``.  ``all_reduce_sum`` is an
+  ``all_gather`` of the (tiny, 2*a*a) tip contributions followed by a
+  rank-ordered local sum: same bytes on the wire as an allreduce tree at this
+  size, and bitwise-identical, order-fixed results on every rank.
+* :class:`LocalHub` -- all partitions in one process on one GPU (the
+  ``transport=None`` default of ``dist_solve``); rounds are recorded, data
+  never leaves the device.
+
+Both record a trace of rounds (``TraceEvent``) for communication-contract
+checks (reference tests/test_dist.py:87-133).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from .errors import ProtocolError
+
+__all__ = ["TraceEvent", "Collectives", "TorchCollectives", "LocalHub"]
+
+
+@dataclass
+class TraceEvent:
+    """One collective round (collectives.py:52-58)."""
+
+    kind: str  # "all_gather" | "all_reduce"
+    round_id: int
+    payloads: list
+
+
+def _summary(obj):
+    if hasattr(obj, "summary"):
+        return obj.summary()
+    if isinstance(obj, torch.Tensor):
+        return {"nbytes": obj.numel() * obj.element_size(), "elements": obj.numel()}
+    return {"nbytes": None}
+
+
+class Collectives:
+    """Abstract endpoint (collectives.py:69-79)."""
+
+    rank: int
+    world_size: int
+
+    def all_gather(self, payload) -> list:
+        raise NotImplementedError
+
+    def all_reduce_sum(self, array: torch.Tensor) -> torch.Tensor:
+        raise NotImplementedError
+
+
+class TorchCollectives(Collectives):
+    """torch.distributed transport; the process group must be initialised."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise ProtocolError("torch.distributed is not initialised")
+        self._dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world_size = dist.get_world_size(group)
+        self.trace: list[TraceEvent] = []
+        self._round = 0
+
+    def _record(self, kind, payloads):
+        self.trace.append(TraceEvent(kind=kind, round_id=self._round, payloads=payloads))
+        self._round += 1
+
+    def gather_tensor(self, flat: torch.Tensor) -> torch.Tensor:
+        """all_gather of equal-size flat tensors -> [world, numel]."""
+        out = torch.empty((self.world_size,) + tuple(flat.shape), dtype=flat.dtype, device=flat.device)
+        try:
+            self._dist.all_gather_into_tensor(out, flat.contiguous(), group=self.group)
+        except (RuntimeError, NotImplementedError):  # backends without the fused op (older gloo)
+            self._dist.all_gather(list(out.unbind(0)), flat.contiguous(), group=self.group)
+        return out
+
+    def all_gather(self, payload) -> list:
+        """Payloads exposing pack()/unpack() travel as one fixed-size slot per
+        rank; anything else must be a tensor of identical shape on all ranks."""
+        if hasattr(payload, "pack"):
+            flat = payload.pack()
+            allp = self.gather_tensor(flat)
+            out = [payload.unpack(allp[r], rank=r) for r in range(self.world_size)]
+        else:
+            allp = self.gather_tensor(payload)
+            out = [allp[r] for r in range(self.world_size)]
+        self._record("all_gather", [_summary(p) for p in out])
+        return out
+
+    def all_reduce_sum(self, array: torch.Tensor) -> torch.Tensor:
+        allp = self.gather_tensor(torch.view_as_real(array) if array.is_complex() else array)
+        if array.is_complex():
+            allp = torch.view_as_complex(allp)
+        total = allp[0].clone()
+        for r in range(1, self.world_size):
+            total += allp[r]
+        self._record("all_reduce", [{"nbytes": array.numel() * array.element_size(),
+                                     "elements": array.numel()}] * self.world_size)
+        return total
+
+
+class LocalHub:
+    """In-process stand-in for P ranks on one device (ThreadHub analogue,
+    collectives.py:87-133): the driver hands it the list of per-rank
+    contributions; rounds are recorded like a real transport."""
+
+    def __init__(self, world_size: int):
+        if world_size < 1:
+            raise ValueError("world_size must be positive")
+        self.world_size = world_size
+        self.trace: list[TraceEvent] = []
+        self._round = 0
+
+    def _record(self, kind, payloads):
+        self.trace.append(TraceEvent(kind=kind, round_id=self._round, payloads=payloads))
+        self._round += 1
+
+    def all_gather_all(self, payloads: list) -> list:
+        if len(payloads) != self.world_size:
+            raise ProtocolError(f"expected {self.world_size} payloads, got {len(payloads)}")
+        self._record("all_gather", [_summary(p) for p in payloads])
+        return list(payloads)
+
+    def all_reduce_all(self, arrays: list) -> torch.Tensor:
+        total = arrays[0].clone()
+        for part in arrays[1:]:
+            if part.shape != total.shape:
+                raise ProtocolError(f"all_reduce shape mismatch: {tuple(part.shape)} vs {tuple(total.shape)}")
+            total += part
+        self._record("all_reduce", [{"nbytes": x.numel() * x.element_size(), "elements": x.numel()}
+                                    for x in arrays])
+        return total

@@ -8,6 +8,7 @@
 #include "../../include/btasel_b200.h"
 #include "generate.cuh"
 #include "inverse.cuh"
+#include "partition.cuh"
 #include "solver.cuh"
 
 struct bsel_context {
@@ -410,6 +411,67 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
     // Original off-diagonals are read in place (never modified by the sweep).
     bta_backward(cx, F, A, fused ? &B : nullptr, XA, fused ? &XB : nullptr, diagonal_only != 0);
     cuda_check(cudaStreamSynchronize(s), "solve");
+  });
+}
+
+static LocalFactorsDev to_dev(const bsel_local_factors_t& f, int64_t b, int64_t a) {
+  LocalFactorsDev d;
+  d.lo = f.lo;
+  d.hi = f.hi;
+  d.b = b;
+  d.a = a;
+  d.kind = f.kind;
+  d.fused = f.fused != 0;
+  d.s_a = dp(f.s_a);
+  d.s_b = dp(f.s_b);
+  d.fill_row = dp(f.fill_row);
+  d.fill_col = dp(f.fill_col);
+  d.b_fill_row = dp(f.b_fill_row);
+  d.b_fill_col = dp(f.b_fill_col);
+  return d;
+}
+
+int bsel_local_forward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b, const bsel_bta_t* a_work,
+                       const bsel_bta_t* b_work, const bsel_local_factors_t* f, bsel_status_t* st) {
+  return guarded(st, [&] {
+    if (!ctx || !f) throw ArgError("NULL argument");
+    check_shape(a, "a");
+    check_shape(a_work, "a_work");
+    if (f->kind < 0 || f->kind > 2) throw ArgError("invalid partition kind");
+    if ((f->fused != 0) != (b != nullptr) || (b != nullptr) != (b_work != nullptr))
+      throw ArgError("factors mode disagrees with right-hand side");
+    if (b) check_same(a, b);
+    BtaDev A = to_dev(*a), WA = to_dev(*a_work), B, WB;
+    if (b) {
+      B = to_dev(*b);
+      WB = to_dev(*b_work);
+    }
+    local_forward(*ctx->impl, A, b ? &B : nullptr, WA, b ? &WB : nullptr, to_dev(*f, a->b, a->a));
+    raise_if_singular(*ctx->impl, a->n);
+  });
+}
+
+int bsel_local_backward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b,
+                        const bsel_local_factors_t* f, const bsel_bta_t* a_work, const bsel_bta_t* b_work,
+                        const bsel_bta_t* x_red, const bsel_bta_t* z_red, int64_t k_top, int64_t k_bot,
+                        int write_tip, const bsel_bta_t* x_a, const bsel_bta_t* x_b, bsel_status_t* st) {
+  return guarded(st, [&] {
+    if (!ctx || !f) throw ArgError("NULL argument");
+    check_shape(a, "a");
+    check_shape(x_a, "x_a");
+    check_shape(x_red, "x_red");
+    const bool fused = f->fused != 0;
+    if (fused && (!b || !b_work || !z_red || !x_b)) throw ShapeError("fused factors require the right-hand side");
+    BtaDev A = to_dev(*a), WA = to_dev(*a_work), XR = to_dev(*x_red), XA = to_dev(*x_a), B, WB, ZR, XB;
+    if (fused) {
+      B = to_dev(*b);
+      WB = to_dev(*b_work);
+      ZR = to_dev(*z_red);
+      XB = to_dev(*x_b);
+    }
+    local_backward(*ctx->impl, A, fused ? &B : nullptr, to_dev(*f, a->b, a->a), WA, fused ? &WB : nullptr, XR,
+                   fused ? &ZR : nullptr, k_top, k_bot, write_tip != 0, XA, fused ? &XB : nullptr);
+    cuda_check(cudaGetLastError(), "local backward");
   });
 }
 

@@ -12,6 +12,7 @@
 
 #include "inverse.cuh"
 #include "solver.cuh"
+#include "steps.cuh"
 
 namespace bsel {
 
@@ -162,87 +163,30 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
   }
 }
 
-// rgf.py:207-319, BTA (a > 0).
+// rgf.py:207-319, BTA (a > 0): n-1 elimination steps (steps.cu end_step),
+// then the last block is eliminated into the tip and the tip is inverted.
 void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev& F) {
   const int n = (int)A.n, b = (int)A.b, a = (int)A.a;
   cudaStream_t sA = ctx.stream(), sB = ctx.aux();
   const bool fused = B != nullptr;
   const int mx = std::max(a, b);
-  ctx.reserve_slots(16, (int64_t)mx * mx);
+  ctx.reserve_slots(40, (int64_t)mx * mx);
   for (int i = 0; i < n - 1; ++i) {
-    Mat S = F.SA(i);
-    ctx.invert(A.D(i), S, i, i, sA);
-    if (!fused) {
-      // rgf.py:281-288: right-hand temporaries.
-      Mat t1 = ctx.tmp(0, b, b), t2 = ctx.tmp(1, b, a);
-      Level L(sA);
-      L.out(t1).mm(+1, S, N, A.U(i), N);
-      L.out(t2).mm(+1, S, N, A.AC(i), N);
-      L.flush();
-      L.out(A.D(i + 1)).add(+1, A.D(i + 1)).mm(-1, A.L(i), N, t1, N);
-      L.out(A.AR(i + 1)).add(+1, A.AR(i + 1)).mm(-1, A.AR(i), N, t1, N);
-      L.out(A.AC(i + 1)).add(+1, A.AC(i + 1)).mm(-1, A.L(i), N, t2, N);
-      L.out(A.T()).add(+1, A.T()).mm(-1, A.AR(i), N, t2, N);
-      L.flush();
-      continue;
+    ring_wait(ctx, i);
+    EndStep st;
+    st.Lk = A.L(i), st.Uk = A.U(i);
+    st.ad_i = A.D(i), st.ad_j = A.D(i + 1), st.ar_i = A.AR(i), st.ar_j = A.AR(i + 1);
+    st.ac_i = A.AC(i), st.ac_j = A.AC(i + 1), st.tipA = A.T();
+    st.S = F.SA(i);
+    if (fused) {
+      st.BL = B->L(i), st.BU = B->U(i);
+      st.bd_i = B->D(i), st.bd_j = B->D(i + 1), st.br_i = B->AR(i), st.br_j = B->AR(i + 1);
+      st.bc_i = B->AC(i), st.bc_j = B->AC(i + 1), st.tipB = B->T();
+      st.sb = F.SB(i);
     }
-    // rgf.py:246-280, fused.
-    const int r = (i & 1) * 8;
-    Mat f = ctx.tmp(r + 0, b, b), g = ctx.tmp(r + 1, a, b), w = ctx.tmp(r + 2, b, b);
-    Mat p = ctx.tmp(r + 3, a, b), k = ctx.tmp(r + 4, b, a), v = ctx.tmp(r + 5, b, b);
-    Mat sb = F.SB(i);
-    if (i >= 2) cuda_check(cudaStreamWaitEvent(sA, ctx.event(2 + (i & 1)), 0), "wait B");
-    {
-      Level L(sA);
-      L.out(f).mm(+1, A.L(i), N, S, N);
-      L.out(g).mm(+1, A.AR(i), N, S, N);
-      L.flush();
-    }
-    cuda_check(cudaEventRecord(ctx.event(i & 1), sA), "record A");
-    {
-      Level L(sA);
-      L.out(A.D(i + 1)).add(+1, A.D(i + 1)).mm(-1, f, N, A.U(i), N);
-      L.out(A.AR(i + 1)).add(+1, A.AR(i + 1)).mm(-1, g, N, A.U(i), N);
-      L.out(A.AC(i + 1)).add(+1, A.AC(i + 1)).mm(-1, f, N, A.AC(i), N);
-      L.out(A.T()).add(+1, A.T()).mm(-1, g, N, A.AC(i), N);
-      L.flush();
-    }
-    cuda_check(cudaStreamWaitEvent(sB, ctx.event(i & 1), 0), "wait A");
-    {
-      Level L(sB);
-      L.out(w).mm(+1, S, N, B->D(i), N);
-      L.out(p).mm(+1, g, N, B->D(i), N);
-      L.out(k).mm(+1, B->D(i), N, g, H);
-      L.flush();
-      L.out(sb).mm(+1, w, N, S, H);
-      L.flush();
-      L.out(v).mm(+1, A.L(i), N, sb, N);
-      L.out(B->AR(i + 1))
-          .add(+1, B->AR(i + 1))
-          .mm(-1, g, N, B->U(i), N)
-          .mm(+1, p, N, f, H)
-          .mm(-1, B->AR(i), N, f, H);
-      L.out(B->AC(i + 1))
-          .add(+1, B->AC(i + 1))
-          .mm(-1, f, N, B->AC(i), N)
-          .mm(-1, B->L(i), N, g, H)
-          .mm(+1, f, N, k, N);
-      L.out(B->T())
-          .add(+1, B->T())
-          .mm(-1, g, N, B->AC(i), N)
-          .mm(-1, B->AR(i), N, g, H)
-          .mm(+1, p, N, g, H);
-      L.flush();
-      L.out(B->D(i + 1))
-          .add(+1, B->D(i + 1))
-          .mm(+1, v, N, A.L(i), H)
-          .mm(-1, B->L(i), N, f, H)
-          .mm(-1, f, N, B->U(i), N);
-      L.flush();
-    }
-    cuda_check(cudaEventRecord(ctx.event(2 + (i & 1)), sB), "record B");
+    end_step(ctx, st, fused, i, i, i & 1);
   }
-  // Epilogue (rgf.py:290-318): eliminate block n-1 into the tip, invert it.
+  // Epilogue (rgf.py:290-318).
   const int i = n - 1;
   Mat S = F.SA(i);
   ctx.invert(A.D(i), S, i, i, sA);
@@ -256,7 +200,7 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
   } else {
     const int r = (i & 1) * 8;
     Mat g = ctx.tmp(r + 1, a, b), p = ctx.tmp(r + 3, a, b);
-    if (i >= 2) cuda_check(cudaStreamWaitEvent(sA, ctx.event(2 + (i & 1)), 0), "wait B");
+    ring_wait(ctx, i);
     Level L(sA);
     L.out(g).mm(+1, A.AR(i), N, S, N);
     L.flush();
@@ -346,14 +290,15 @@ void bt_backward(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDe
   }
 }
 
-// rgf.py:322-398 (_backstep, k = 1 and k = 2) driven by rgf.py:401-489.
+// rgf.py:401-489: generic _backstep (steps.cu back_step) with k = 1 at the
+// last block (tip coupling only) and k = 2 elsewhere (next block, tip).
 void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDev* B,
                         const BtaDev& XA, const BtaDev* XB, bool diag_only) {
   const int n = (int)A.n, b = (int)A.b, a = (int)A.a;
   cudaStream_t s = ctx.stream();
   const bool fused = B != nullptr;
   const int mx = std::max(a, b);
-  ctx.reserve_slots(24, (int64_t)mx * mx);
+  ctx.reserve_slots(40, (int64_t)mx * mx);
   Mat Xtt = cm(F.tip_inv, a, a);
   Mat Ztt;
   Level L(s);
@@ -366,124 +311,43 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
     Ztt = XB->T();
   }
   L.flush();
-
-  // ---- i = n-1: one trailing coupling (the tip) ----
-  {
-    const int i = n - 1;
-    Mat g = F.SA(i), ACe = F.ACe(i), ARe = F.ARe(i);
-    Mat RA = ctx.tmp(0, b, a), CA = ctx.tmp(1, a, b), phi = ctx.tmp(2, b, b);
-    L.out(RA).mm(+1, ACe, N, Xtt, N);
-    L.out(CA).mm(+1, Xtt, N, ARe, N);
-    Mat RZ = ctx.tmp(3, b, a), CZ = ctx.tmp(4, a, b), sct = ctx.tmp(5, b, b), sc = ctx.tmp(6, b, b);
-    Mat quad = ctx.tmp(7, b, b), e0 = ctx.tmp(8, b, a), f0 = ctx.tmp(9, a, b);
-    Mat acc1 = ctx.tmp(10, b, b), acc2 = ctx.tmp(11, b, b), gq = ctx.tmp(12, b, b);
-    if (fused) {
-      L.out(RZ).mm(+1, ACe, N, Ztt, N);
-      L.out(CZ).mm(+1, Ztt, N, ACe, H);
-      L.out(sct).mm(+1, g, N, cm(F.b_diag_last, b, b), N);
+  for (int i = n - 1; i >= 0; --i) {
+    BackStep st;
+    st.g = F.SA(i);
+    if (i == n - 1) {
+      st.k = 1;
+      st.rs[0] = F.ACe(i), st.qs[0] = F.ARe(i), st.ya[0][0] = Xtt;
+      st.row[0] = XA.AC(i), st.col[0] = XA.AR(i);
+      if (fused) {
+        Mat sct = ctx.tmp(1, b, b), sc = ctx.tmp(2, b, b);
+        L.out(sct).mm(+1, st.g, N, cm(F.b_diag_last, b, b), N);
+        L.flush();
+        L.out(sc).mm(+1, sct, N, st.g, H);
+        L.flush();
+        st.sc = sc;
+        st.ss[0] = F.BCe(i), st.ws[0] = F.BRe(i), st.yb[0][0] = Ztt;
+        st.zrow[0] = XB->AC(i), st.zcol[0] = XB->AR(i);
+      }
+    } else {
+      st.k = 2;
+      st.rs[0] = A.U(i), st.rs[1] = F.ACe(i);
+      st.qs[0] = A.L(i), st.qs[1] = F.ARe(i);
+      st.ya[0][0] = XA.D(i + 1), st.ya[0][1] = XA.AC(i + 1), st.ya[1][0] = XA.AR(i + 1), st.ya[1][1] = Xtt;
+      st.row[0] = diag_only ? ctx.tmp(3, b, b) : XA.U(i), st.row[1] = XA.AC(i);
+      st.col[0] = diag_only ? ctx.tmp(4, b, b) : XA.L(i), st.col[1] = XA.AR(i);
+      if (fused) {
+        st.sc = F.SB(i);
+        st.ss[0] = B->U(i), st.ss[1] = F.BCe(i);
+        st.ws[0] = B->L(i), st.ws[1] = F.BRe(i);
+        st.yb[0][0] = XB->D(i + 1), st.yb[0][1] = XB->AC(i + 1), st.yb[1][0] = XB->AR(i + 1);
+        st.yb[1][1] = Ztt;
+        st.zrow[0] = diag_only ? ctx.tmp(5, b, b) : XB->U(i), st.zrow[1] = XB->AC(i);
+        st.zcol[0] = diag_only ? ctx.tmp(6, b, b) : XB->L(i), st.zcol[1] = XB->AR(i);
+      }
     }
-    L.flush();
-    Mat xrow = XA.AC(i), xcol = XA.AR(i);
-    L.out(xrow).mm(-1, g, N, RA, N);
-    L.out(xcol).mm(-1, CA, N, g, N);
-    if (fused) {
-      L.out(sc).mm(+1, sct, N, g, H);
-      L.out(quad).mm(+1, ACe, N, CZ, N);
-    }
-    L.flush();
-    L.out(phi).mm(-1, xrow, N, ARe, N);
-    if (fused) {
-      Mat BCe = F.BCe(i), BRe = F.BRe(i);
-      L.out(e0).mm(+1, g, N, BCe, N).mm(-1, sc, N, ARe, H);
-      L.out(f0).mm(+1, BRe, N, g, H).mm(-1, ARe, N, sc, N);
-      L.out(acc1).mm(+1, BCe, N, xrow, H);
-      L.out(acc2).mm(+1, xrow, N, BRe, N);
-      L.out(gq).mm(+1, g, N, quad, N);
-    }
-    L.flush();
-    L.out(XA.D(i)).add(+1, g).mm(+1, phi, N, g, N);
-    if (fused) {
-      L.out(XB->AC(i)).mm(+1, e0, N, Xtt, H).mm(-1, g, N, RZ, N);
-      L.out(XB->AR(i)).mm(+1, Xtt, N, f0, N).mm(-1, CZ, N, g, H);
-      L.out(XB->D(i))
-          .add(+1, sc)
-          .mm(+1, phi, N, sc, N)
-          .mm(+1, sc, N, phi, H)
-          .mm(+1, g, N, acc1, N)
-          .mm(+1, acc2, N, g, H)
-          .mm(+1, gq, N, g, H);
-    }
-    L.flush();
-  }
-
-  // ---- i = n-2 .. 0: two trailing couplings (next diagonal block, tip) ----
-  for (int i = n - 2; i >= 0; --i) {
-    Mat g = F.SA(i), U = A.U(i), Lo = A.L(i), ACe = F.ACe(i), ARe = F.ARe(i);
-    Mat Ydd = XA.D(i + 1), Ydt = XA.AC(i + 1), Ytd = XA.AR(i + 1), Ytt = Xtt;
-    Mat RA0 = ctx.tmp(0, b, b), RA1 = ctx.tmp(1, b, a), CA0 = ctx.tmp(2, b, b), CA1 = ctx.tmp(3, a, b);
-    L.out(RA0).mm(+1, U, N, Ydd, N).mm(+1, ACe, N, Ytd, N);
-    L.out(RA1).mm(+1, U, N, Ydt, N).mm(+1, ACe, N, Ytt, N);
-    L.out(CA0).mm(+1, Ydd, N, Lo, N).mm(+1, Ydt, N, ARe, N);
-    L.out(CA1).mm(+1, Ytd, N, Lo, N).mm(+1, Ytt, N, ARe, N);
-    Mat RZ0 = ctx.tmp(4, b, b), RZ1 = ctx.tmp(5, b, a), CZ0 = ctx.tmp(6, b, b), CZ1 = ctx.tmp(7, a, b);
-    Mat e0 = ctx.tmp(8, b, b), e1 = ctx.tmp(9, b, a), f0 = ctx.tmp(10, b, b), f1 = ctx.tmp(11, a, b);
-    Mat Zdd, Zdt, Ztd, sc, BU, BL, BCe, BRe;
-    if (fused) {
-      Zdd = XB->D(i + 1);
-      Zdt = XB->AC(i + 1);
-      Ztd = XB->AR(i + 1);
-      sc = F.SB(i);
-      BU = B->U(i);
-      BL = B->L(i);
-      BCe = F.BCe(i);
-      BRe = F.BRe(i);
-      L.out(RZ0).mm(+1, U, N, Zdd, N).mm(+1, ACe, N, Ztd, N);
-      L.out(RZ1).mm(+1, U, N, Zdt, N).mm(+1, ACe, N, Ztt, N);
-      L.out(CZ0).mm(+1, Zdd, N, U, H).mm(+1, Zdt, N, ACe, H);
-      L.out(CZ1).mm(+1, Ztd, N, U, H).mm(+1, Ztt, N, ACe, H);
-      L.out(e0).mm(+1, g, N, BU, N).mm(-1, sc, N, Lo, H);
-      L.out(e1).mm(+1, g, N, BCe, N).mm(-1, sc, N, ARe, H);
-      L.out(f0).mm(+1, BL, N, g, H).mm(-1, Lo, N, sc, N);
-      L.out(f1).mm(+1, BRe, N, g, H).mm(-1, ARe, N, sc, N);
-    }
-    L.flush();
-    Mat xr0 = diag_only ? ctx.tmp(12, b, b) : XA.U(i);
-    Mat xc0 = diag_only ? ctx.tmp(13, b, b) : XA.L(i);
-    Mat xr1 = XA.AC(i), xc1 = XA.AR(i);
-    L.out(xr0).mm(-1, g, N, RA0, N);
-    L.out(xr1).mm(-1, g, N, RA1, N);
-    L.out(xc0).mm(-1, CA0, N, g, N);
-    L.out(xc1).mm(-1, CA1, N, g, N);
-    Mat quad = ctx.tmp(14, b, b);
-    if (fused) {
-      Mat zr0 = diag_only ? ctx.tmp(15, b, b) : XB->U(i);
-      Mat zc0 = diag_only ? ctx.tmp(16, b, b) : XB->L(i);
-      L.out(zr0).mm(+1, e0, N, Ydd, H).mm(+1, e1, N, Ydt, H).mm(-1, g, N, RZ0, N);
-      L.out(XB->AC(i)).mm(+1, e0, N, Ytd, H).mm(+1, e1, N, Ytt, H).mm(-1, g, N, RZ1, N);
-      L.out(zc0).mm(+1, Ydd, N, f0, N).mm(+1, Ydt, N, f1, N).mm(-1, CZ0, N, g, H);
-      L.out(XB->AR(i)).mm(+1, Ytd, N, f0, N).mm(+1, Ytt, N, f1, N).mm(-1, CZ1, N, g, H);
-      L.out(quad).mm(+1, U, N, CZ0, N).mm(+1, ACe, N, CZ1, N);
-    }
-    L.flush();
-    Mat phi = ctx.tmp(17, b, b), acc1 = ctx.tmp(18, b, b), acc2 = ctx.tmp(19, b, b), gq = ctx.tmp(20, b, b);
-    L.out(phi).mm(-1, xr0, N, Lo, N).mm(-1, xr1, N, ARe, N);
-    if (fused) {
-      L.out(acc1).mm(+1, BU, N, xr0, H).mm(+1, BCe, N, xr1, H);
-      L.out(acc2).mm(+1, xr0, N, BL, N).mm(+1, xr1, N, BRe, N);
-      L.out(gq).mm(+1, g, N, quad, N);
-    }
-    L.flush();
-    L.out(XA.D(i)).add(+1, g).mm(+1, phi, N, g, N);
-    if (fused) {
-      L.out(XB->D(i))
-          .add(+1, sc)
-          .mm(+1, phi, N, sc, N)
-          .mm(+1, sc, N, phi, H)
-          .mm(+1, g, N, acc1, N)
-          .mm(+1, acc2, N, g, H)
-          .mm(+1, gq, N, g, H);
-    }
-    L.flush();
+    st.diag = XA.D(i);
+    if (fused) st.zdiag = XB->D(i);
+    back_step(ctx, s, st);
   }
 }
 
@@ -496,14 +360,12 @@ void bta_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDe
   cudaStream_t s = ctx.stream();
   ctx.reset_status();
   cuda_check(cudaEventRecord(ctx.timer(0), s), "timer");
-  cuda_check(cudaEventRecord(ctx.event(4), s), "fork");
-  cuda_check(cudaStreamWaitEvent(ctx.aux(), ctx.event(4), 0), "fork wait");
+  streams_fork(ctx);
   if (A.a == 0)
     bt_forward(ctx, A, B, F);
   else
     bta_forward_arrow(ctx, A, B, F);
-  cuda_check(cudaEventRecord(ctx.event(5), ctx.aux()), "join");
-  cuda_check(cudaStreamWaitEvent(s, ctx.event(5), 0), "join wait");
+  streams_join(ctx);
   cuda_check(cudaEventRecord(ctx.timer(1), s), "timer");
 }
 

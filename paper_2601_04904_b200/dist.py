@@ -1,0 +1,554 @@
+"""Distributed selected inversion / quadratic solution (drop-in for btasel/dist.py).
+
+The paper's scheme: contiguous partitions of diagonal
+blocks (partition.py), each eliminated locally on its own GPU by the sm_100a
+partition kernels (csrc/partition.cu: first = downward, last = upward,
+middle = downward with fill-in to its top boundary); ONE all_gather of the
+fixed-layout boundary payload plus (a > 0) ONE rank-ordered all_reduce of the
+tip contributions; every rank assembles and solves the small reduced BTA
+system (2P-2 diagonal blocks + tip) redundantly; then each partition
+back-substitutes locally, seeded from the reduced solution.  Outputs stay
+sharded on the devices unless gathered.
+
+Transports: ``TorchCollectives`` (one process per GPU, NCCL over NVLink) or
+the in-process ``LocalHub`` (all partitions on one GPU, the default).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native
+from .collectives import Collectives, LocalHub, TorchCollectives
+from .device import DeviceBta, to_device, to_host
+from .errors import ProtocolError, ShapeMismatchError, WorkerError
+from .kernels import OpCounter, record_sweep
+from .matrix import BtaMatrix, SelectedSolution
+from .partition import PartitionPlan, plan_partitions
+from .rgf import solve_selected
+
+__all__ = ["BoundaryPayload", "LocalFactors", "ReducedSystem", "local_forward", "assemble_reduced",
+           "solve_reduced", "local_backward", "dist_solve", "DistSolver", "record_partition"]
+
+_KIND_CODES = {"first": 0, "middle": 1, "last": 2}
+_KIND_NAMES = {v: k for k, v in _KIND_CODES.items()}
+_FIELDS = ("diag", "coupling", "arrow_row", "arrow_col", "b_diag", "b_coupling", "b_arrow_row", "b_arrow_col")
+
+# Logical per-step product inventory of the partition sweeps (dist.py:211-397,
+# 595-742), checked against the reference OpCounter in tests.
+_PART_TABLE = {
+    ("si", "end", "forward"): {"bbb": 2, "bba": 2, "abb": 1, "aba": 1},
+    ("siq", "end", "forward"): {"bbb": 8, "abb": 5, "bba": 5, "aba": 4},
+    ("si", "middle", "forward"): {"bbb": 6, "abb": 3, "bba": 2, "aba": 1},
+    ("siq", "middle", "forward"): {"bbb": 22, "abb": 10, "bba": 8, "aba": 4},
+    ("si", "end", "backward"): {"bbb": 6, "bab": 3, "bba": 2, "baa": 1, "abb": 2, "aab": 1},
+    ("siq", "end", "backward"): {"bbb": 26, "bab": 11, "bba": 7, "baa": 3, "abb": 8, "aab": 4},
+    ("si", "middle", "backward"): {"bbb": 15, "bab": 5, "bba": 3, "baa": 1, "abb": 3, "aab": 1},
+    ("siq", "middle", "backward"): {"bbb": 59, "bab": 18, "bba": 10, "baa": 3, "abb": 12, "aab": 4},
+}
+
+
+def record_partition(counter, kind, length, b, a, mode, phase):
+    """Add the reference's logical counts of one partition sweep."""
+    if counter is None:
+        return
+    role = "middle" if kind == "middle" else "end"
+    steps = length - 2 if role == "middle" else length - 1
+    if steps <= 0:
+        return
+    dims = {"b": b, "a": a}
+    for label, cnt in _PART_TABLE[(mode, role, phase)].items():
+        if "a" in label and a == 0:
+            continue
+        counter.gemm_by_shape["".join(counter._classify(dims[ch]) for ch in label)] += cnt * steps
+    if phase == "forward":
+        counter.lu_count += steps
+        counter.inv_count += steps
+        counter.trsm_count += 2 * steps
+
+
+# ---------------------------------------------------------------------------
+# Containers
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class BoundaryPayload:
+    """One rank's AllGather contribution (dist.py:73-131), device tensors.
+
+    ``pack``/``unpack`` use one fixed-size slot (the middle-partition
+    inventory) so the exchange is a single equal-size all_gather.
+    """
+
+    rank: int
+    kind: str
+    b: int
+    a: int
+    fused: bool
+    diag: list = field(default_factory=list)
+    coupling: list = field(default_factory=list)
+    arrow_row: list = field(default_factory=list)
+    arrow_col: list = field(default_factory=list)
+    b_diag: list = field(default_factory=list)
+    b_coupling: list = field(default_factory=list)
+    b_arrow_row: list = field(default_factory=list)
+    b_arrow_col: list = field(default_factory=list)
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for f in _FIELDS for t in getattr(self, f))
+
+    def summary(self) -> dict:
+        blocks = {f: [tuple(t.shape) for t in getattr(self, f)] for f in _FIELDS if getattr(self, f)}
+        return {"rank": self.rank, "kind": self.kind, "nbytes": self.nbytes(), "blocks": blocks}
+
+    def _layout(self):
+        b, a = self.b, self.a
+        shapes = {"diag": (b, b), "coupling": (b, b), "arrow_row": (a, b), "arrow_col": (b, a)}
+        sides = ("",) + (("b_",) if self.fused else ())
+        return [(s + f, shapes[f]) for s in sides for f in ("diag", "coupling", "arrow_row", "arrow_col")]
+
+    def slot_elems(self) -> int:
+        return 4 + sum(2 * 2 * r * c for _, (r, c) in self._layout())  # 2 blocks per field
+
+    def pack(self) -> torch.Tensor:
+        dev = self.diag[0].device
+        out = torch.zeros(self.slot_elems(), dtype=torch.float64, device=dev)
+        out[0], out[1], out[2], out[3] = float(self.rank), float(_KIND_CODES[self.kind]), len(self.diag), 0.0
+        off = 4
+        for name, (r, c) in self._layout():
+            for t in getattr(self, name):
+                out[off:off + 2 * r * c] = torch.view_as_real(t.contiguous()).reshape(-1)
+                off += 2 * r * c
+            off += 2 * r * c * (2 - len(getattr(self, name)))
+        return out
+
+    def unpack(self, flat: torch.Tensor, rank: int) -> "BoundaryPayload":
+        hdr = flat[:4].tolist()
+        kind = _KIND_NAMES.get(int(hdr[1]))
+        if kind is None or int(hdr[0]) != rank:
+            raise ProtocolError(f"payload {rank} carries rank {int(hdr[0])} kind code {int(hdr[1])}")
+        nbnd = int(hdr[2])
+        p = BoundaryPayload(rank=rank, kind=kind, b=self.b, a=self.a, fused=self.fused)
+        off = 4
+        for name, (r, c) in self._layout():
+            count = nbnd if not name.endswith("coupling") else (2 if kind == "middle" else 0)
+            lst = []
+            for j in range(2):
+                if j < count:
+                    lst.append(torch.view_as_complex(flat[off:off + 2 * r * c].view(r, c, 2)))
+                off += 2 * r * c
+            setattr(p, name, lst)
+        return p
+
+
+@dataclass
+class LocalFactors:
+    """Per-rank retained elimination data (dist.py:134-151), device tensors."""
+
+    kind: str
+    lo: int
+    hi: int
+    mode: str
+    tensors: dict = field(default_factory=dict)
+    work_a: object = None
+    work_b: object = None
+
+    def desc(self) -> _native.LocalFactors:
+        f = _native.LocalFactors()
+        f.lo, f.hi, f.kind, f.fused = self.lo, self.hi, _KIND_CODES[self.kind], int(self.mode == "siq")
+        for k in ("s_a", "s_b", "fill_row", "fill_col", "b_fill_row", "b_fill_col"):
+            t = self.tensors.get(k)
+            setattr(f, k, t.data_ptr() if (t is not None and t.numel()) else None)
+        return f
+
+
+@dataclass
+class ReducedSystem:
+    """The boundary-coupling system, replicated on every rank (dist.py:154-169)."""
+
+    matrix_a: DeviceBta
+    matrix_b: DeviceBta | None
+    provenance: list
+    index: dict
+
+
+class _Strips:
+    """Partition working arrays: diag / arrow strips (+ tip contribution)."""
+
+    def __init__(self, length, b, a, device):
+        c128 = dict(dtype=torch.complex128, device=device)
+        self.n, self.b, self.a = length, b, a
+        self.diag = torch.empty((length, b, b), **c128)
+        self.arrow_row = torch.empty((length, a, b), **c128)
+        self.arrow_col = torch.empty((length, b, a), **c128)
+        self.tip = torch.zeros((a, a), **c128)
+
+    def desc(self) -> _native.Bta:
+        d = _native.Bta()
+        d.n, d.b, d.a = self.n, self.b, self.a
+        for k in ("diag", "arrow_row", "arrow_col", "tip"):
+            t = getattr(self, k)
+            setattr(d, k, t.data_ptr() if t.numel() else None)
+        return d
+
+
+# ---------------------------------------------------------------------------
+# Phases
+# ---------------------------------------------------------------------------
+
+
+def _as_device(m, device=None):
+    if m is None or isinstance(m, DeviceBta):
+        return m
+    return to_device(m, device)
+
+
+def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | None = None, *, _factors=None):
+    """Eliminate one partition's interior blocks on the GPU (dist.py:172-416).
+
+    Returns ``(payload, tip_delta, factors)``; inputs are never mutated.
+    """
+    A = _as_device(a)
+    B = _as_device(b, A.device) if b is not None else None
+    lo, hi = plan.ranges[rank]
+    kind = plan.kinds[rank]
+    fused = B is not None
+    n, bs, asz = A.shape_params
+    length = hi - lo
+    dev = A.device
+    fac = _factors
+    if fac is None:
+        c128 = dict(dtype=torch.complex128, device=dev)
+        t = {"s_a": torch.empty((length, bs, bs), **c128)}
+        if fused:
+            t["s_b"] = torch.empty((length, bs, bs), **c128)
+        if kind == "middle":
+            t["fill_row"] = torch.empty((length, bs, bs), **c128)
+            t["fill_col"] = torch.empty((length, bs, bs), **c128)
+            if fused:
+                t["b_fill_row"] = torch.empty((length, bs, bs), **c128)
+                t["b_fill_col"] = torch.empty((length, bs, bs), **c128)
+        fac = LocalFactors(kind=kind, lo=lo, hi=hi, mode="siq" if fused else "si", tensors=t,
+                           work_a=_Strips(length, bs, asz, dev), work_b=_Strips(length, bs, asz, dev) if fused else None)
+    WA, WB = fac.work_a, fac.work_b
+    ctx = _native.Context.get(dev.index)
+    ad, wad, fd = A.desc(), WA.desc(), fac.desc()
+    bd = B.desc() if fused else None
+    wbd = WB.desc() if fused else None
+    ctx.bind_stream()
+    ctx.call("bsel_local_forward", ctypes.byref(ad), ctypes.byref(bd) if fused else None, ctypes.byref(wad),
+             ctypes.byref(wbd) if fused else None, ctypes.byref(fd))
+    record_partition(counter, kind, length, bs, asz, fac.mode, "forward")
+    bnd = {"first": [hi - 1], "last": [lo], "middle": [lo, hi - 1]}[kind]
+    pay = BoundaryPayload(rank=rank, kind=kind, b=bs, a=asz, fused=fused)
+    pay.diag = [WA.diag[g - lo] for g in bnd]
+    pay.arrow_row = [WA.arrow_row[g - lo] for g in bnd]
+    pay.arrow_col = [WA.arrow_col[g - lo] for g in bnd]
+    if kind == "middle":
+        pay.coupling = [fac.tensors["fill_row"][length - 1], fac.tensors["fill_col"][length - 1]]
+    if fused:
+        pay.b_diag = [WB.diag[g - lo] for g in bnd]
+        pay.b_arrow_row = [WB.arrow_row[g - lo] for g in bnd]
+        pay.b_arrow_col = [WB.arrow_col[g - lo] for g in bnd]
+        if kind == "middle":
+            pay.b_coupling = [fac.tensors["b_fill_row"][length - 1], fac.tensors["b_fill_col"][length - 1]]
+    tip_delta = torch.stack([WA.tip, WB.tip]) if fused else WA.tip.unsqueeze(0)
+    return pay, tip_delta, fac
+
+
+def _assemble(gathered, a, b, plan: PartitionPlan, tip_sum) -> ReducedSystem:
+    """Reduced system from all payloads (dist.py:440-504)."""
+    fused = b is not None
+    if len(gathered) != plan.num_parts:
+        raise ProtocolError(f"expected {plan.num_parts} payloads, got {len(gathered)}")
+    prov, d, r, c, bd, br, bc = [], [], [], [], [], [], []
+    for p, pay in enumerate(gathered):
+        if pay.rank != p or pay.kind != plan.kinds[p]:
+            raise ProtocolError(f"payload {p} carries rank {pay.rank} kind {pay.kind!r}")
+        expected = 2 if pay.kind == "middle" else 1
+        if len(pay.diag) != expected or (fused and len(pay.b_diag) != expected):
+            raise ProtocolError(f"payload {p} has malformed boundary blocks")
+        if pay.kind == "middle" and (len(pay.coupling) != 2 or (fused and len(pay.b_coupling) != 2)):
+            raise ProtocolError(f"payload {p} lacks its fill-in coupling pair")
+        sides = {"first": ("bottom",), "last": ("top",), "middle": ("top", "bottom")}[pay.kind]
+        for j, side in enumerate(sides):
+            prov.append((p, side))
+            d.append(pay.diag[j])
+            r.append(pay.arrow_row[j])
+            c.append(pay.arrow_col[j])
+            if fused:
+                bd.append(pay.b_diag[j])
+                br.append(pay.b_arrow_row[j])
+                bc.append(pay.b_arrow_col[j])
+    nr = len(d)
+    up, lw, bup, blw = [], [], [], []
+    for k in range(nr - 1):
+        p1, p2 = prov[k][0], prov[k + 1][0]
+        if p1 == p2:
+            up.append(gathered[p1].coupling[0])
+            lw.append(gathered[p1].coupling[1])
+            if fused:
+                bup.append(gathered[p1].b_coupling[0])
+                blw.append(gathered[p1].b_coupling[1])
+        else:  # original separator owned by the upper-side rank
+            g = plan.ranges[p1][1] - 1
+            up.append(a.upper[g])
+            lw.append(a.lower[g])
+            if fused:
+                bup.append(b.upper[g])
+                blw.append(b.lower[g])
+    asz, bs = a.a, a.b
+    dev = d[0].device
+
+    def stack(lst, shape):
+        if lst:
+            return torch.stack([x.to(dev) for x in lst]).contiguous()
+        return torch.empty((0,) + shape, dtype=torch.complex128, device=dev)
+
+    tip = (a.tip.to(dev) + tip_sum[0]) if asz else torch.empty((0, 0), dtype=torch.complex128, device=dev)
+    ra = DeviceBta(nr, bs, asz, {"diag": stack(d, (bs, bs)), "lower": stack(lw, (bs, bs)),
+                                 "upper": stack(up, (bs, bs)), "arrow_row": stack(r, (asz, bs)),
+                                 "arrow_col": stack(c, (bs, asz)), "tip": tip.contiguous()})
+    rb = None
+    if fused:
+        btip = (b.tip.to(dev) + tip_sum[1]) if asz else torch.empty((0, 0), dtype=torch.complex128, device=dev)
+        rb = DeviceBta(nr, bs, asz, {"diag": stack(bd, (bs, bs)), "lower": stack(blw, (bs, bs)),
+                                     "upper": stack(bup, (bs, bs)), "arrow_row": stack(br, (asz, bs)),
+                                     "arrow_col": stack(bc, (bs, asz)), "tip": btip.contiguous()})
+    return ReducedSystem(matrix_a=ra, matrix_b=rb, provenance=prov, index={key: k for k, key in enumerate(prov)})
+
+
+def assemble_reduced(coll: Collectives, a, b, plan: PartitionPlan, payload: BoundaryPayload,
+                     tip_delta) -> ReducedSystem:
+    """Exchange boundary data and build the replicated reduced system
+    (dist.py:419-504): one all_gather, plus one all_reduce when a > 0."""
+    gathered = coll.all_gather(payload)
+    tip_sum = coll.all_reduce_sum(tip_delta) if a.a > 0 else None
+    return _assemble(gathered, a, b, plan, tip_sum)
+
+
+def solve_reduced(reduced: ReducedSystem, mode: str, counter=None, recursive_parts=None):
+    """Solve the replicated reduced system (dist.py:507-523) on the GPU."""
+    if recursive_parts and reduced.matrix_a.n >= 2 * recursive_parts:
+        return dist_solve(reduced.matrix_a, reduced.matrix_b, num_parts=recursive_parts, mode=mode)
+    return solve_selected(reduced.matrix_a, reduced.matrix_b if mode == "siq" else None, mode, counter=counter)
+
+
+def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, reduced: ReducedSystem,
+                   red_sol: SelectedSolution, counter=None, *, out=None):
+    """Back-substitute one partition seeded with the reduced solution
+    (dist.py:542-744).  Writes this rank's pattern blocks (and, on rank 0,
+    the tip) into ``out`` = (x_a, x_b) full-size DeviceBta (allocated zeroed
+    if None) and returns it."""
+    A = _as_device(a)
+    B = _as_device(b, A.device) if b is not None else None
+    lo, hi = plan.ranges[rank]
+    fused = factors.mode == "siq"
+    if fused and B is None:
+        raise ProtocolError("fused factors require the right-hand side")
+    if red_sol.x_a.shape_params != reduced.matrix_a.shape_params:
+        raise ProtocolError("reduced solution shape disagrees with reduced system")
+    n, bs, asz = A.shape_params
+    if out is None:
+        out = (DeviceBta.empty(n, bs, asz, A.device), DeviceBta.empty(n, bs, asz, A.device) if fused else None)
+    XA, XB = out
+    kind = plan.kinds[rank]
+    k_top = reduced.index.get((rank, "top"), -1)
+    k_bot = reduced.index.get((rank, "bottom"), -1)
+    ctx = _native.Context.get(A.device.index)
+    ad, fd, wad = A.desc(), factors.desc(), factors.work_a.desc()
+    xrd, xad = red_sol.x_a.desc(), XA.desc()
+    bd = B.desc() if fused else None
+    wbd = factors.work_b.desc() if fused else None
+    zrd = red_sol.x_b.desc() if fused else None
+    xbd = XB.desc() if fused else None
+    ref = lambda x: ctypes.byref(x) if x is not None else None  # noqa: E731
+    ctx.bind_stream()
+    ctx.call("bsel_local_backward", ref(ad), ref(bd), ref(fd), ref(wad), ref(wbd), ref(xrd), ref(zrd),
+             k_top, k_bot, int(rank == 0), ref(xad), ref(xbd))
+    record_partition(counter, kind, hi - lo, bs, asz, factors.mode, "backward")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Facade
+# ---------------------------------------------------------------------------
+
+
+class _PhaseTimer:
+    def __init__(self, names):
+        self.ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in names}
+
+    def start(self, k):
+        self.ev[k][0].record()
+
+    def stop(self, k):
+        self.ev[k][1].record()
+
+    def seconds(self):
+        torch.cuda.synchronize()
+        return {k: s.elapsed_time(e) / 1e3 for k, (s, e) in self.ev.items()}
+
+
+def _reduced_counts(reduced, mode):
+    c = OpCounter(b=reduced.matrix_a.b, a=reduced.matrix_a.a)
+    record_sweep(c, reduced.matrix_a.n, reduced.matrix_a.b, reduced.matrix_a.a, mode, "forward")
+    record_sweep(c, reduced.matrix_a.n, reduced.matrix_a.b, reduced.matrix_a.a, mode, "backward")
+    return c
+
+
+def dist_solve(a, b=None, num_parts=2, mode=None, transport=None, *, counter=None, timings=None,
+               rank_counters=None, recursive_parts=None, gather=True):
+    """Distributed selected solve (dist.py:804-896).
+
+    ``transport=None`` (or a LocalHub): every partition runs on the current
+    GPU in this process and the full solution is returned.  A
+    ``TorchCollectives`` endpoint makes this process one rank of a
+    one-process-per-GPU job: with ``gather`` rank 0 returns the merged
+    solution and other ranks None; without, every rank returns its sharded
+    (zero-elsewhere) device solution.  ``num_parts=1`` delegates to
+    ``solve_selected``.
+    """
+    if mode is None:
+        mode = "si" if b is None else "siq"
+    if mode == "siq" and b is None:
+        raise ValueError("mode 'siq' requires a right-hand side")
+    if mode == "si":
+        b = None
+    if num_parts == 1:
+        return solve_selected(a, b, mode, counter=counter, timings=timings)
+    host = not isinstance(a, DeviceBta)
+    plan = plan_partitions(a.n, num_parts, mode)
+    if isinstance(transport, TorchCollectives):
+        if transport.world_size != num_parts:
+            raise ProtocolError(f"transport world size {transport.world_size} != num_parts {num_parts}")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        A = _as_device(a, dev)
+        B = _as_device(b, dev) if b is not None else None
+        rank = transport.rank
+        tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
+        cnt = OpCounter(b=A.b, a=A.a)
+        try:
+            tm.start("forward")
+            pay, delta, fac = local_forward(A, B, plan, rank, cnt)
+            tm.stop("forward")
+        except Exception as exc:  # rank attribution (dist.py:875-885)
+            raise WorkerError(rank, exc) from exc
+        tm.start("communication")
+        reduced = assemble_reduced(transport, A, B, plan, pay, delta)
+        tm.stop("communication")
+        tm.start("reduced")
+        red_sol = solve_reduced(reduced, mode, None, recursive_parts)
+        tm.stop("reduced")
+        tm.start("backward")
+        XA, XB = local_backward(A, B, plan, rank, fac, reduced, red_sol, cnt)
+        tm.stop("backward")
+        if timings is not None:
+            timings.update(tm.seconds())
+        if counter is not None:
+            counter.merge(cnt)
+            if rank == 0:
+                counter.merge(_reduced_counts(reduced, mode))
+        if rank_counters is not None:
+            rank_counters.append(cnt)
+        if not gather:
+            return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
+        import torch.distributed as tdist
+
+        # pattern blocks are owned by exactly one rank (zeros elsewhere):
+        # a sum-reduce to rank 0 is an exact merge.
+        for m in (XA, XB) if XB is not None else (XA,):
+            for t in m.tensors().values():
+                if t.numel():
+                    tdist.reduce(torch.view_as_real(t), dst=0, group=transport.group)
+        if rank != 0:
+            return None
+        if host:
+            return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if XB is not None else None, mode=mode)
+        return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
+
+    hub = transport if transport is not None else LocalHub(num_parts)
+    if hub.world_size != num_parts:
+        raise ProtocolError(f"transport world size {hub.world_size} != num_parts {num_parts}")
+    dev = a.device if isinstance(a, DeviceBta) else torch.device("cuda", torch.cuda.current_device())
+    A = _as_device(a, dev)
+    B = _as_device(b, dev) if b is not None else None
+    tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
+    counters = [OpCounter(b=A.b, a=A.a) for _ in range(num_parts)]
+    results, errors = [], []
+    tm.start("forward")
+    for rank in range(num_parts):
+        try:
+            results.append(local_forward(A, B, plan, rank, counters[rank]))
+        except Exception as exc:  # noqa: BLE001 - rank attribution
+            errors.append((rank, exc))
+            results.append(None)
+    tm.stop("forward")
+    if errors:
+        primary = [e for e in errors if not isinstance(e[1], ProtocolError)]
+        rank, exc = min(primary or errors, key=lambda e: e[0])
+        raise WorkerError(rank, exc) from exc
+    tm.start("communication")
+    gathered = hub.all_gather_all([r[0] for r in results])
+    tip_sum = hub.all_reduce_all([r[1] for r in results]) if A.a > 0 else None
+    reduced = _assemble(gathered, A, B, plan, tip_sum)
+    tm.stop("communication")
+    tm.start("reduced")
+    red_sol = solve_reduced(reduced, mode, None, recursive_parts)
+    tm.stop("reduced")
+    tm.start("backward")
+    out = (DeviceBta.empty(A.n, A.b, A.a, dev), DeviceBta.empty(A.n, A.b, A.a, dev) if B is not None else None)
+    for rank in range(num_parts):
+        local_backward(A, B, plan, rank, results[rank][2], reduced, red_sol, counters[rank], out=out)
+    tm.stop("backward")
+    if timings is not None:
+        timings.update(tm.seconds())
+    if counter is not None:
+        for c in counters:
+            counter.merge(c)
+        counter.merge(_reduced_counts(reduced, mode))
+    if rank_counters is not None:
+        rank_counters.extend(counters)
+    XA, XB = out
+    if host:
+        return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if XB is not None else None, mode=mode)
+    return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
+
+
+class DistSolver:
+    """Repeated distributed solves of one energy point on this rank with all
+    device buffers preallocated (the bench / multi-GPU production path)."""
+
+    def __init__(self, A: DeviceBta, B: DeviceBta | None, mode: str, world: int, rank: int, device,
+                 transport: TorchCollectives | None = None):
+        self.A, self.B, self.mode = A, B if mode == "siq" else None, mode
+        self.plan = plan_partitions(A.n, world, mode)
+        self.rank = rank
+        self.coll = transport or TorchCollectives()
+        self.out = (DeviceBta.empty(A.n, A.b, A.a, device),
+                    DeviceBta.empty(A.n, A.b, A.a, device) if self.B is not None else None)
+        self._fac = None
+        self.timings = {}
+
+    def solve(self):
+        tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
+        tm.start("forward")
+        pay, delta, self._fac = local_forward(self.A, self.B, self.plan, self.rank, _factors=self._fac)
+        tm.stop("forward")
+        tm.start("communication")
+        reduced = assemble_reduced(self.coll, self.A, self.B, self.plan, pay, delta)
+        tm.stop("communication")
+        tm.start("reduced")
+        red_sol = solve_reduced(reduced, self.mode)
+        tm.stop("reduced")
+        tm.start("backward")
+        local_backward(self.A, self.B, self.plan, self.rank, self._fac, reduced, red_sol, out=self.out)
+        tm.stop("backward")
+        self._tm = tm
+        return self.out
+
+    def phase_seconds(self):
+        return self._tm.seconds()

@@ -1,0 +1,160 @@
+"""CPU (gloo, world_size 2 and 3) tests of the distributed host logic:
+payload packing, the single all_gather, the rank-ordered all_reduce and the
+reduced-system assembly, against the oracle's restatement of dist.py."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from conftest import manifest
+
+import oracle
+from oracle.dist import assemble as oracle_assemble
+from oracle.dist import local_forward as oracle_local_forward
+from oracle.seq import _Mul
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _t(x):
+    return torch.from_numpy(np.ascontiguousarray(x))
+
+
+def _device_bta(m):
+    from paper_2601_04904_b200 import DeviceBta
+    st = lambda blocks, shp: torch.from_numpy(np.ascontiguousarray(np.stack(blocks) if len(blocks) else np.zeros((0,) + shp, np.complex128)))  # noqa: E731
+    return DeviceBta(m.n, m.b, m.a, {"diag": st(m.diag, (m.b, m.b)), "lower": st(m.lower, (m.b, m.b)),
+                                     "upper": st(m.upper, (m.b, m.b)), "arrow_row": st(m.arrow_row, (m.a, m.b)),
+                                     "arrow_col": st(m.arrow_col, (m.b, m.a)), "tip": _t(m.tip)})
+
+
+def _payload(pay, rank, b, a, fused):
+    from paper_2601_04904_b200.dist import BoundaryPayload
+    p = BoundaryPayload(rank=rank, kind=pay["kind"], b=b, a=a, fused=fused)
+    p.diag = [_t(x) for x in pay["diag"]]
+    p.arrow_row = [_t(x) for x in pay["arrow_row"]]
+    p.arrow_col = [_t(x) for x in pay["arrow_col"]]
+    p.coupling = [_t(x) for x in (pay["coupling"] or [])]
+    if fused:
+        p.b_diag = [_t(x) for x in pay["b_diag"]]
+        p.b_arrow_row = [_t(x) for x in pay["b_arrow_row"]]
+        p.b_arrow_col = [_t(x) for x in pay["b_arrow_col"]]
+        p.b_coupling = [_t(x) for x in (pay["b_coupling"] or [])]
+    return p
+
+
+def _worker(rank, world, port, n, b, a, mode, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2601_04904_b200 import TorchCollectives, plan_partitions
+    from paper_2601_04904_b200.dist import assemble_reduced
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _body(rank, world, n, b, a, mode, q)
+    except Exception:  # report instead of hanging the peer's queue.get
+        import traceback
+        q.put((rank, traceback.format_exc(), None, None, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _body(rank, world, n, b, a, mode, q):
+    from paper_2601_04904_b200 import TorchCollectives, plan_partitions
+    from paper_2601_04904_b200.dist import assemble_reduced
+    if True:
+        A = oracle.generate_dd_bta(n, b, a, seed=3)
+        B = oracle.hermitianize(oracle.generate_dd_bta(n, b, a, seed=4)) if mode == "siq" else None
+        ranges, kinds = oracle.plan_partitions(n, world, mode)
+        pay, delta, _ = oracle_local_forward(A, B, ranges, kinds, rank, _Mul(b, a))
+        coll = TorchCollectives()
+        plan = plan_partitions(n, world, mode)
+        red = assemble_reduced(coll, _device_bta(A), _device_bta(B) if B is not None else None, plan,
+                               _payload(pay, rank, b, a, B is not None), _t(delta))
+        # oracle reference assembly from all ranks' payloads
+        outs = [oracle_local_forward(A, B, ranges, kinds, r, _Mul(b, a)) for r in range(world)]
+        tot = outs[0][1].copy()
+        for o in outs[1:]:
+            tot = tot + o[1]
+        RA, RB, index = oracle_assemble(A, B, ranges, [o[0] for o in outs], tot)
+        err = 0.0
+        pairs = [(red.matrix_a, RA)] + ([(red.matrix_b, RB)] if B is not None else [])
+        for got, ref in pairs:
+            for kind in ("diag", "lower", "upper", "arrow_row", "arrow_col"):
+                for g, r in zip(getattr(got, kind), getattr(ref, kind)):
+                    err = max(err, float(np.max(np.abs(g.numpy() - r))) if r.size else 0.0)
+            if a:
+                err = max(err, float(np.max(np.abs(got.tip.numpy() - ref.tip))))
+        q.put((rank, err, [e.kind for e in coll.trace], red.index == index,
+               [p.get("nbytes") for p in coll.trace[0].payloads], red.matrix_a.tip.numpy().tobytes()))
+
+
+@pytest.mark.parametrize("world,n,b,a,mode", [(2, 8, 3, 2, "siq"), (3, 12, 3, 2, "siq"), (3, 12, 4, 0, "si"),
+                                              (3, 12, 4, 2, "si")])
+def test_gloo_exchange_and_assembly(world, n, b, a, mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, a, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=240) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, kinds, same_index, nbytes, tip in res:
+        assert not isinstance(err, str), err
+        assert err == 0.0, (rank, err)   # same blocks, same rank-ordered sum: bitwise
+        assert kinds == (["all_gather", "all_reduce"] if a else ["all_gather"])
+        assert same_index
+    assert len({r[5] for r in res}) == 1  # replicated bitwise
+    if mode == "si" and world == 3:
+        assert res[0][4][1] == 16 * (4 * b * b + 4 * a * b)  # middle payload bytes (test_dist.py:115-120)
+
+
+def test_payload_pack_roundtrip():
+    from paper_2601_04904_b200.dist import BoundaryPayload
+    rng = np.random.default_rng(0)
+    c = lambda *s: torch.from_numpy(rng.standard_normal(s) + 1j * rng.standard_normal(s))  # noqa: E731
+    p = BoundaryPayload(rank=1, kind="middle", b=3, a=2, fused=True,
+                        diag=[c(3, 3), c(3, 3)], coupling=[c(3, 3), c(3, 3)], arrow_row=[c(2, 3), c(2, 3)],
+                        arrow_col=[c(3, 2), c(3, 2)], b_diag=[c(3, 3), c(3, 3)], b_coupling=[c(3, 3), c(3, 3)],
+                        b_arrow_row=[c(2, 3), c(2, 3)], b_arrow_col=[c(3, 2), c(3, 2)])
+    q = p.unpack(p.pack(), rank=1)
+    for f in ("diag", "coupling", "arrow_row", "arrow_col", "b_diag", "b_coupling", "b_arrow_row", "b_arrow_col"):
+        for x, y in zip(getattr(p, f), getattr(q, f)):
+            assert torch.equal(x, y)
+    e = BoundaryPayload(rank=0, kind="first", b=3, a=2, fused=False, diag=[c(3, 3)], arrow_row=[c(2, 3)],
+                        arrow_col=[c(3, 2)])
+    assert e.pack().numel() == p.pack().numel() // 2 + 2 or e.pack().numel() > 0
+    r = e.unpack(e.pack(), rank=0)
+    assert r.kind == "first" and r.coupling == [] and len(r.diag) == 1
+    with pytest.raises(Exception):
+        e.unpack(e.pack(), rank=1)
+
+
+@pytest.mark.parametrize("name", sorted(k for k, v in manifest()["cases"].items() if v["kind"] == "dist"))
+def test_partition_counts_match_reference(name):
+    from paper_2601_04904_b200 import OpCounter, plan_partitions
+    from paper_2601_04904_b200.dist import record_partition
+    from paper_2601_04904_b200.kernels import record_sweep
+    meta = manifest()["cases"][name]
+    n, b, a, mode, parts = meta["n"], meta["b"], meta["a"], meta["mode"], meta["parts"]
+    plan = plan_partitions(n, parts, mode)
+    c = OpCounter(b=b, a=a)
+    for r in range(parts):
+        lo, hi = plan.ranges[r]
+        record_partition(c, plan.kinds[r], hi - lo, b, a, mode, "forward")
+        record_partition(c, plan.kinds[r], hi - lo, b, a, mode, "backward")
+    nr = 2 * parts - 2
+    record_sweep(c, nr, b, a, mode, "forward")
+    record_sweep(c, nr, b, a, mode, "backward")
+    assert c.as_dict() == meta["counts"]

@@ -283,3 +283,19 @@ def test_timings_and_device_path():
     assert isinstance(sol.x_a, bs.DeviceBta)
     host = bs.solve_selected(A, B)
     assert max_block_rel_err(bs.to_host(sol.x_b), host.x_b) == 0.0
+
+
+def test_device_generator_matches_host_generator():
+    for n, b, a, seed in ((5, 16, 4, 0), (3, 33, 0, 7), (4, 8, 12, 123)):
+        d = bs.to_host(bs.generate_dd_bta_device(n, b, a, seed=seed))
+        h = bs.generate_dd_bta(n, b, a, seed=seed)
+        for (k, i, x), (_, _, y) in zip(d.pattern_blocks(), h.pattern_blocks()):
+            if k in ("diag", "tip"):
+                off = ~np.eye(x.shape[0], dtype=bool)
+                np.testing.assert_array_equal(x[off], y[off])
+                np.testing.assert_allclose(np.diagonal(x), np.diagonal(y), rtol=4e-16, atol=0)
+            else:
+                np.testing.assert_array_equal(x, y)
+        hd = bs.to_host(bs.hermitianize_device(bs.to_device(h)))
+        hh = bs.hermitianize(h)
+        assert hd.equals_exact(hh)
