@@ -25,35 +25,30 @@ __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y
 // n steps the storage S satisfies inv(A)[r][piv[k]] = S[piv[r]][k].
 // Pivot choice: max |re|+|im| among unused rows (LAPACK izamax), lowest
 // index on ties.  Two barriers per elimination step.
+template <int NB>
+struct LeafSmem {
+  double2 a[NB][NB + 1];
+  double2 fcol[NB];
+  double2 prow[NB];
+  int piv[NB];
+  int used[NB];
+};
+
+// Gauss-Jordan with partial pivoting on L.a (n <= NB) by the whole CTA.
+// Returns true (on every thread) if an exactly zero pivot was met.
 template <int NB, int THREADS>
-__global__ void __launch_bounds__(THREADS)
-    leaf_inverse_kernel(const double2* __restrict__ X, int64_t ldx, int64_t sx, double2* __restrict__ Y,
-                        int64_t ldy, int64_t sy, int n, int* flags, int64_t flag_stride) {
-  __shared__ double2 a[NB][NB + 1];
-  __shared__ double2 fcol[NB];
-  __shared__ double2 prow[NB];
-  __shared__ int piv[NB];
-  __shared__ int used[NB];
+__device__ bool gj_leaf(LeafSmem<NB>& L, int n) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  X += blockIdx.x * sx;
-  Y += blockIdx.x * sy;
-  int* flag = flags + blockIdx.x * flag_stride;
-
-  for (int e = tid; e < NB * NB; e += THREADS) {
-    int i = e / NB, j = e % NB;
-    if (i < n && j < n) a[i][j] = X[(int64_t)i * ldx + j];
-  }
-  for (int i = tid; i < NB; i += THREADS) used[i] = 0;
+  for (int i = tid; i < NB; i += THREADS) L.used[i] = 0;
   __syncthreads();
-
   bool any_zero = false;
   for (int k = 0; k < n; ++k) {
     if (warp == 0) {
       double best = -1.0;
       int bi = NB;
       for (int i = lane; i < n; i += 32) {
-        if (!used[i]) {
-          double v = cabs1(a[i][k]);
+        if (!L.used[i]) {
+          double v = cabs1(L.a[i][k]);
           if (v > best) {
             best = v;
             bi = i;
@@ -72,37 +67,58 @@ __global__ void __launch_bounds__(THREADS)
       const bool zero = !(best > 0.0);
       int p = bi;
       if (p >= n) p = k;  // only reachable for NaN columns
-      double2 inv = zero ? make_double2(1.0, 0.0) : crecip(a[p][k]);
-      for (int i = lane; i < n; i += 32) fcol[i] = (i == p) ? make_double2(0.0, 0.0) : a[i][k];
-      for (int j = lane; j < n; j += 32) prow[j] = (j == k) ? inv : cmul(a[p][j], inv);
+      double2 inv = zero ? make_double2(1.0, 0.0) : crecip(L.a[p][k]);
+      for (int i = lane; i < n; i += 32) L.fcol[i] = (i == p) ? make_double2(0.0, 0.0) : L.a[i][k];
+      for (int j = lane; j < n; j += 32) L.prow[j] = (j == k) ? inv : cmul(L.a[p][j], inv);
       if (lane == 0) {
-        piv[k] = p;
-        used[p] = 1;
+        L.piv[k] = p;
+        L.used[p] = 1;
       }
       any_zero |= zero;
     }
     __syncthreads();
-    const int p = piv[k];
+    const int p = L.piv[k];
     for (int e = tid; e < NB * NB; e += THREADS) {
       int i = e / NB, j = e % NB;
       if (i >= n || j >= n) continue;
-      double2 pr = prow[j];
+      double2 pr = L.prow[j];
       if (i == p) {
-        a[i][j] = pr;
+        L.a[i][j] = pr;
       } else {
-        double2 f = fcol[i];
-        double2 v = (j == k) ? make_double2(0.0, 0.0) : a[i][j];
+        double2 f = L.fcol[i];
+        double2 v = (j == k) ? make_double2(0.0, 0.0) : L.a[i][j];
         v.x -= f.x * pr.x - f.y * pr.y;
         v.y -= f.x * pr.y + f.y * pr.x;
-        a[i][j] = v;
+        L.a[i][j] = v;
       }
     }
     __syncthreads();
   }
+  return __syncthreads_or(any_zero ? 1 : 0) != 0;
+}
+
+// One CTA per matrix: storage S after gj_leaf satisfies
+// inv(A)[r][piv[k]] = S[piv[r]][k]; pivot choice max |re|+|im| among unused
+// rows (LAPACK izamax), lowest index on ties; virtual row interchanges.
+template <int NB, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    leaf_inverse_kernel(const double2* __restrict__ X, int64_t ldx, int64_t sx, double2* __restrict__ Y,
+                        int64_t ldy, int64_t sy, int n, int* flags, int64_t flag_stride) {
+  __shared__ LeafSmem<NB> L;
+  const int tid = threadIdx.x;
+  X += blockIdx.x * sx;
+  Y += blockIdx.x * sy;
+  int* flag = flags + blockIdx.x * flag_stride;
+  for (int e = tid; e < NB * NB; e += THREADS) {
+    int i = e / NB, j = e % NB;
+    if (i < n && j < n) L.a[i][j] = X[(int64_t)i * ldx + j];
+  }
+  __syncthreads();
+  const bool any_zero = gj_leaf<NB, THREADS>(L, n);
   if (tid == 0 && any_zero) atomicMax(flag, 1);
   for (int e = tid; e < NB * NB; e += THREADS) {
     int r = e / NB, k = e % NB;
-    if (r < n && k < n) Y[(int64_t)r * ldy + piv[k]] = a[piv[r]][k];
+    if (r < n && k < n) Y[(int64_t)r * ldy + L.piv[k]] = L.a[L.piv[r]][k];
   }
 }
 
@@ -209,6 +225,182 @@ __global__ void __launch_bounds__(1024)
 
 constexpr int kLeafThreads = 256;
 
+// ---------------------------------------------------------------------------
+// Persistent blocked Gauss-Jordan: ONE cooperative launch per inverse.
+//
+// For each 32-wide panel J: CTA 0 inverts the diagonal tile W[J,J] with
+// partial pivoting (gj_leaf) and publishes Dinv; after a grid barrier every
+// CTA updates its 32x32 output tiles with DMMA from shared memory:
+//   W'[J,J] = Dinv, W'[J,K] = Dinv W[J,K], W'[I,J] = -W[I,J] Dinv,
+//   W'[I,K] = W[I,K] - W[I,J] (Dinv W[J,K]),
+// ping-ponging between two n x n buffers (the last panel writes Y).  Global
+// reads of the ping-pong buffers use ld.global.cg (L2) because other SMs
+// rewrote them since this SM may have cached them in L1.
+// ---------------------------------------------------------------------------
+
+constexpr int kT = 32;
+constexpr int kTLD = kT + 2;  // 544-byte rows: conflict-free DMMA fragment loads
+
+struct PinvSmem {
+  double2 d[kT][kTLD];  // Dinv
+  double2 x[kT][kTLD];  // row-panel tile W[J,K] -> R = Dinv W[J,K]
+  double2 c[kT][kTLD];  // column-panel tile W[I,J]
+  double2 r[kT][kTLD];
+};
+
+__device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(counter, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      if (v < target) __nanosleep(64);
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Load a kT x kT tile (rows x cols valid, zero elsewhere) into smem.
+__device__ __forceinline__ void load_tile(double2 (*dst)[kTLD], const double2* src, int64_t ld, int rows, int cols) {
+  for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+    const int i = e / kT, j = e % kT;
+    dst[i][j] = (i < rows && j < cols) ? ldcg2(src + (int64_t)i * ld + j) : make_double2(0.0, 0.0);
+  }
+}
+
+// acc (warp tile 8 x 16 complex) = sA (32 x 32) . sB (32 x 32), DMMA.
+__device__ __forceinline__ void tile_mma(double (&acc)[4][2], const double2 (*sA)[kTLD], const double2 (*sB)[kTLD]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mg = warp & 3, nh = warp >> 2;
+  const unsigned maskB = ((lane & 1) == 1 && ((lane >> 2) & 1) == 0) ? 0x80000000u : 0u;
+  const double* A = reinterpret_cast<const double*>(&sA[mg * 8 + (lane >> 2)][0]);
+  const int kc0 = (lane & 3) >> 1, part = lane & 1;
+  const int comp = (lane & 1) ^ ((lane >> 2) & 1);
+  const int col0 = nh * 16 + ((lane >> 2) >> 1);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < kT / 2; ++kk) {
+    const int kc = 2 * kk + kc0;
+    const double af = A[kc * 2 + part];
+    const double* Brow = reinterpret_cast<const double*>(&sB[kc][0]);
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn) {
+      double bf = Brow[(col0 + jn * 4) * 2 + comp];
+      int hi = __double2hiint(bf) ^ (int)maskB;
+      bf = __hiloint2double(hi, __double2loint(bf));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[jn][0]), "+d"(acc[jn][1])
+                   : "d"(af), "d"(bf));
+    }
+  }
+}
+
+// Warp-tile coordinates of acc[jn]: row, col inside the 32 x 32 tile.
+__device__ __forceinline__ int acc_row() { return ((threadIdx.x >> 5) & 3) * 8 + ((threadIdx.x & 31) >> 2); }
+__device__ __forceinline__ int acc_col(int jn) { return ((threadIdx.x >> 5) >> 2) * 16 + jn * 4 + (threadIdx.x & 3); }
+
+__global__ void __launch_bounds__(256, 1)
+    persistent_inverse_kernel(const double2* __restrict__ X, int64_t ldx, double2* Y, int64_t ldy, int n,
+                              double2* work, double2* gD, unsigned* barrier, int* flag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
+  const int nt = (n + kT - 1) / kT, ntiles = nt * nt, G = gridDim.x;
+  unsigned target = 0;
+  const double2* Wc = X;
+  int64_t ldc = ldx;
+  for (int p = 0; p < nt; ++p) {
+    const int j0 = p * kT, jb = min(kT, n - j0);
+    double2* Wn = ((nt - 1 - p) % 2 == 0) ? Y : work;
+    const int64_t ldn = (Wn == Y) ? ldy : n;
+    // ---- leaf: CTA 0 inverts W[J,J] ----
+    if (blockIdx.x == 0) {
+      LeafSmem<kT>& L = *reinterpret_cast<LeafSmem<kT>*>(&S.x[0][0]);  // spans x and c
+      for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+        const int i = e / kT, j = e % kT;
+        if (i < jb && j < jb) L.a[i][j] = ldcg2(Wc + (int64_t)(j0 + i) * ldc + j0 + j);
+      }
+      __syncthreads();
+      const bool zero = gj_leaf<kT, 256>(L, jb);
+      if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
+      for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+        const int r = e / kT, k = e % kT;
+        double2 v = make_double2(0.0, 0.0);
+        // inv[r][piv[k]] = a[piv[r]][k]  ->  write Dinv[r][piv[k]]
+        if (r < jb && k < jb) gD[r * kT + L.piv[k]] = L.a[L.piv[r]][k];
+        else if (r < kT && k < kT && (r >= jb || k >= jb)) gD[r * kT + k] = v;
+      }
+    }
+    target += G;
+    grid_barrier(barrier, target);
+    // ---- update ----
+    load_tile(S.d, gD, kT, kT, kT);
+    __syncthreads();
+    int r_tk = -1;  // column tile whose R = Dinv W[J,K] is cached in S.r
+    const int chunk = (ntiles + G - 1) / G;
+    const int t_begin = blockIdx.x * chunk, t_end = min(ntiles, t_begin + chunk);
+    for (int t = t_begin; t < t_end; ++t) {
+      const int tk = t / nt, ti = t % nt;
+      const int i0 = ti * kT, k0 = tk * kT;
+      const int ib = min(kT, n - i0), kb = min(kT, n - k0);
+      double acc[4][2];
+      double2* out = Wn + (int64_t)i0 * ldn + k0;
+      const int orow = acc_row();
+      if (ti == p && tk == p) {
+        for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+          const int i = e / kT, j = e % kT;
+          if (i < ib && j < kb) out[(int64_t)i * ldn + j] = S.d[i][j];
+        }
+        continue;
+      }
+      if (tk != p && r_tk != tk) {  // R = Dinv . W[J,K]
+        __syncthreads();
+        load_tile(S.x, Wc + (int64_t)j0 * ldc + k0, ldc, jb, kb);
+        __syncthreads();
+        tile_mma(acc, S.d, S.x);
+#pragma unroll
+        for (int jn = 0; jn < 4; ++jn) S.r[orow][acc_col(jn)] = make_double2(acc[jn][0], acc[jn][1]);
+        __syncthreads();
+        r_tk = tk;
+      }
+      if (ti == p) {  // W'[J,K] = R
+        for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+          const int i = e / kT, j = e % kT;
+          if (i < ib && j < kb) out[(int64_t)i * ldn + j] = S.r[i][j];
+        }
+        continue;
+      }
+      __syncthreads();
+      load_tile(S.c, Wc + (int64_t)i0 * ldc + j0, ldc, ib, jb);
+      __syncthreads();
+      tile_mma(acc, S.c, tk == p ? S.d : S.r);
+#pragma unroll
+      for (int jn = 0; jn < 4; ++jn) {
+        const int oc = acc_col(jn);
+        if (orow < ib && oc < kb) {
+          double2 v = make_double2(-acc[jn][0], -acc[jn][1]);
+          if (tk != p) {
+            const double2 w = ldcg2(Wc + (int64_t)(i0 + orow) * ldc + k0 + oc);
+            v.x += w.x;
+            v.y += w.y;
+          }
+          out[(int64_t)orow * ldn + oc] = v;
+        }
+      }
+    }
+    target += G;
+    grid_barrier(barrier, target);
+    Wc = Wn;
+    ldc = ldn;
+  }
+}
+
+
 GemmTerm term(const double2* A, int64_t lda, uint8_t opA, const double2* B, int64_t ldb, uint8_t opB,
               int K, int sign) {
   GemmTerm t{};
@@ -225,7 +417,27 @@ GemmTerm term(const double2* A, int64_t lda, uint8_t opA, const double2* B, int6
 
 }  // namespace
 
-int64_t block_inverse_workspace(int n) { return (int64_t)n * n; }
+// work: n*n ping-pong buffer (also the exact fallback's scratch), then the
+// published Dinv tile (kT*kT) and the grid-barrier counter.
+int64_t block_inverse_workspace(int n) { return (int64_t)n * n + kT * kT + 1; }
+
+namespace {
+int coop_grid_limit() {
+  static int limit = -1;
+  if (limit < 0) {
+    int dev = 0, coop = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (cudaFuncSetAttribute(persistent_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(PinvSmem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persistent_inverse_kernel, 256,
+                                                      sizeof(PinvSmem)) != cudaSuccess)
+      per_sm = 0;
+    limit = coop ? per_sm * device_sm_count() : 0;
+  }
+  return limit;
+}
+}  // namespace
 
 cudaError_t launch_leaf_inverse_batched(const double2* X, int64_t ldx, int64_t strideX, double2* Y,
                                         int64_t ldy, int64_t strideY, int n, int batch, int* flags,
@@ -238,10 +450,12 @@ cudaError_t launch_leaf_inverse_batched(const double2* X, int64_t ldx, int64_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n,
-                                 double2* work, int* flag, unsigned long long* status,
-                                 unsigned long long key, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
+namespace {
+
+// Multi-launch variant (no cooperative launch available): per panel one leaf
+// kernel and two grouped GEMM launches.
+cudaError_t levels_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n, double2* work,
+                           int* flag, cudaStream_t stream) {
   cudaError_t err;
   const int panels = (n + kLeaf - 1) / kLeaf;
   // Ping-pong so that the last panel writes Y and X is never written.
@@ -317,6 +531,33 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     R = W;
     ldr = ldw;
   }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n,
+                                 double2* work, int* flag, unsigned long long* status,
+                                 unsigned long long key, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t err;
+  const int panels = (n + kLeaf - 1) / kLeaf;
+  const int limit = coop_grid_limit();
+  if (panels > 1 && limit > 0) {
+    double2* gD = work + (int64_t)n * n;
+    unsigned* barrier = reinterpret_cast<unsigned*>(gD + kT * kT);
+    if ((err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream)) != cudaSuccess) return err;
+    int grid = panels * panels < limit ? panels * panels : limit;
+    if (grid > device_sm_count()) grid = device_sm_count();
+    void* args[] = {(void*)&X, (void*)&ldx, (void*)&Y, (void*)&ldy, (void*)&n,
+                    (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag};
+    err = cudaLaunchCooperativeKernel((const void*)persistent_inverse_kernel, grid, 256, args, sizeof(PinvSmem),
+                                      stream);
+    count_launch();
+  } else {
+    err = levels_inverse(X, ldx, Y, ldy, n, work, flag, stream);
+  }
+  if (err != cudaSuccess) return err;
   // Exact fallback (no-op unless a leaf met an exactly zero pivot).
   const size_t smem = (size_t)n * (2 * sizeof(double2) + 2 * sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;

@@ -63,6 +63,10 @@ class Context {
   void set_stream(cudaStream_t s) { user_stream_ = s; }
   cudaStream_t stream() const { return user_stream_; }
   cudaStream_t aux() const { return aux_; }
+  // High-priority stream for the latency-critical Schur chain (pivot
+  // inverse -> elimination factors -> next pivot); its CTAs are scheduled
+  // ahead of the aux stream's throughput work as SMs free up.
+  cudaStream_t chain() const { return chain_; }
   int device() const { return device_; }
 
   // Scratch: `count` temporaries of (r x c) complex, grow-only.
@@ -87,6 +91,7 @@ class Context {
   int device_;
   cudaStream_t user_stream_ = nullptr;
   cudaStream_t aux_ = nullptr;
+  cudaStream_t chain_ = nullptr;
   double2* slots_ = nullptr;
   int64_t slot_elems_ = 0;
   int nslots_ = 0;

@@ -20,19 +20,22 @@ Mat rt(Context& ctx, int parity, int k, int r, int c) { return ctx.tmp(parity * 
 void streams_fork(Context& ctx) {
   cuda_check(cudaEventRecord(ctx.event(4), ctx.stream()), "fork");
   cuda_check(cudaStreamWaitEvent(ctx.aux(), ctx.event(4), 0), "fork wait");
+  cuda_check(cudaStreamWaitEvent(ctx.chain(), ctx.event(4), 0), "fork wait");
 }
 
 void streams_join(Context& ctx) {
   cuda_check(cudaEventRecord(ctx.event(5), ctx.aux()), "join");
   cuda_check(cudaStreamWaitEvent(ctx.stream(), ctx.event(5), 0), "join wait");
+  cuda_check(cudaEventRecord(ctx.event(6), ctx.chain()), "join");
+  cuda_check(cudaStreamWaitEvent(ctx.stream(), ctx.event(6), 0), "join wait");
 }
 
 void ring_wait(Context& ctx, int step) {
-  if (step >= 2) cuda_check(cudaStreamWaitEvent(ctx.stream(), ctx.event(2 + (step & 1)), 0), "ring wait");
+  if (step >= 2) cuda_check(cudaStreamWaitEvent(ctx.chain(), ctx.event(2 + (step & 1)), 0), "ring wait");
 }
 
 void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int parity) {
-  cudaStream_t sA = ctx.stream(), sB = ctx.aux();
+  cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
   ctx.invert(st.ad_i, st.S, order, index, sA);
   const Mat& S = st.S;
@@ -83,7 +86,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
 }
 
 void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int parity) {
-  cudaStream_t sA = ctx.stream(), sB = ctx.aux();
+  cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
   ctx.invert(st.ad_i, st.S, order, index, sA);
   const Mat& S = st.S;

@@ -22,7 +22,10 @@ namespace bsel {
 
 Context::Context(int device) : device_(device) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
-  cuda_check(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking), "aux stream");
+  int least = 0, greatest = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+  cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, least), "aux stream");
+  cuda_check(cudaStreamCreateWithPriority(&chain_, cudaStreamNonBlocking, greatest), "chain stream");
   cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "flag");
   cuda_check(cudaMalloc(&d_status_, sizeof(unsigned long long)), "status");
   events_.resize(8);
@@ -42,12 +45,14 @@ Context::~Context() {
   for (auto& e : events_) cudaEventDestroy(e);
   for (auto& t : timers_) cudaEventDestroy(t);
   if (aux_) cudaStreamDestroy(aux_);
+  if (chain_) cudaStreamDestroy(chain_);
 }
 
 void Context::reserve_slots(int nslots, int64_t slot_elems) {
   if (nslots <= nslots_ && slot_elems <= slot_elems_) return;
   cuda_check(cudaStreamSynchronize(user_stream_), "sync before realloc");
   cuda_check(cudaStreamSynchronize(aux_), "sync before realloc");
+  cuda_check(cudaStreamSynchronize(chain_), "sync before realloc");
   if (slots_) cudaFree(slots_);
   nslots_ = std::max(nslots, nslots_);
   slot_elems_ = std::max(slot_elems, slot_elems_);
@@ -62,6 +67,7 @@ Mat Context::tmp(int slot, int r, int c) {
 double2* Context::inv_work(int64_t elems) {
   if (elems > inv_work_elems_) {
     cuda_check(cudaStreamSynchronize(user_stream_), "sync before realloc");
+    cuda_check(cudaStreamSynchronize(chain_), "sync before realloc");
     if (inv_work_) cudaFree(inv_work_);
     cuda_check(cudaMalloc(&inv_work_, (size_t)elems * sizeof(double2)), "inverse workspace");
     inv_work_elems_ = elems;
@@ -117,7 +123,7 @@ void copy_block(Level& L, Mat dst, Mat src) { L.out(dst).add(+1, src); }
 // rgf.py:79-124 (Alg. 1), BT.
 void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev& F) {
   const int n = (int)A.n, b = (int)A.b;
-  cudaStream_t sA = ctx.stream(), sB = ctx.aux();
+  cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const bool fused = B != nullptr;
   ctx.reserve_slots(8, (int64_t)b * b);
   for (int i = 0; i < n - 1; ++i) {
@@ -167,7 +173,7 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
 // then the last block is eliminated into the tip and the tip is inverted.
 void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev& F) {
   const int n = (int)A.n, b = (int)A.b, a = (int)A.a;
-  cudaStream_t sA = ctx.stream(), sB = ctx.aux();
+  cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const bool fused = B != nullptr;
   const int mx = std::max(a, b);
   ctx.reserve_slots(40, (int64_t)mx * mx);

@@ -293,7 +293,7 @@ def test_device_generator_matches_host_generator():
             if k in ("diag", "tip"):
                 off = ~np.eye(x.shape[0], dtype=bool)
                 np.testing.assert_array_equal(x[off], y[off])
-                np.testing.assert_allclose(np.diagonal(x), np.diagonal(y), rtol=4e-16, atol=0)
+                np.testing.assert_allclose(np.diagonal(x), np.diagonal(y), rtol=2e-15, atol=0)  # row sums: sequential vs pairwise
             else:
                 np.testing.assert_array_equal(x, y)
         hd = bs.to_host(bs.hermitianize_device(bs.to_device(h)))
