@@ -20,105 +20,88 @@ __device__ __forceinline__ double2 crecip(double2 a) {
 }
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
 
+// 1/z via one correctly rounded reciprocal of |z|^2 (operands here are O(1)
+// pivots of diagonally dominant blocks; the exact fallback handles the rest).
+__device__ __forceinline__ double2 crecip_fast(double2 z) {
+  const double r = __drcp_rn(fma(z.x, z.x, z.y * z.y));
+  return make_double2(z.x * r, -z.y * r);
+}
+
+// 32 x 32 Gauss-Jordan with partial pivoting by 256 threads: ONE barrier per
+// pivot step (ping-pong buffers), pivot search by every warp with
+// redux.sync on the high word of |re|+|im| (monotone for non-negative
+// doubles), virtual row interchanges tracked in a register bitmask.
+// Thread t owns row t/8, columns 4*(t%8) .. +3.  Input in a[0]; the result
+// S (inv(A)[r][piv[k]] = S[piv[r]][k]) ends in a[n & 1].
+struct Leaf32 {
+  double2 a[2][32][33];
+  int piv[32];
+};
+
+__device__ bool gj_leaf32(Leaf32& L, int n) {
+  const int t = threadIdx.x, lane = t & 31;
+  const int i = t >> 3, c0 = (t & 7) * 4;
+  unsigned used = 0u;
+  bool any_zero = false;
+  for (int k = 0; k < n; ++k) {
+    const double2 (*cur)[33] = L.a[k & 1];
+    double2 (*nxt)[33] = L.a[(k + 1) & 1];
+    const bool cand = lane < n && !((used >> lane) & 1u);
+    const unsigned key = cand ? (unsigned)__double2hiint(cabs1(cur[lane][k])) + 1u : 0u;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    const unsigned ball = __ballot_sync(0xffffffffu, cand && key == kmax);
+    const int p = __ffs(ball) - 1;
+    const bool zero = kmax <= 1u;  // all candidates zero (or subnormal): let the exact path decide
+    any_zero |= zero;
+    used |= 1u << p;
+    if (t == 0) L.piv[k] = p;
+    const double2 inv = zero ? make_double2(1.0, 0.0) : crecip_fast(cur[p][k]);
+    if (i < n) {
+      const double2 fi = cur[i][k];
+#pragma unroll
+      for (int c = c0; c < c0 + 4; ++c) {
+        if (c >= n) break;
+        const double2 pr = (c == k) ? inv : cmul(cur[p][c], inv);
+        if (i == p) {
+          nxt[i][c] = pr;
+        } else {
+          double2 v = (c == k) ? make_double2(0.0, 0.0) : cur[i][c];
+          v.x -= fi.x * pr.x - fi.y * pr.y;
+          v.y -= fi.x * pr.y + fi.y * pr.x;
+          nxt[i][c] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return any_zero;
+}
+
 // In-place Gauss-Jordan with partial pivoting and *virtual* row interchanges
 // (rows are never moved: piv[k] is the physical pivot row of step k).  After
 // n steps the storage S satisfies inv(A)[r][piv[k]] = S[piv[r]][k].
 // Pivot choice: max |re|+|im| among unused rows (LAPACK izamax), lowest
 // index on ties.  Two barriers per elimination step.
-template <int NB>
-struct LeafSmem {
-  double2 a[NB][NB + 1];
-  double2 fcol[NB];
-  double2 prow[NB];
-  int piv[NB];
-  int used[NB];
-};
-
-// Gauss-Jordan with partial pivoting on L.a (n <= NB) by the whole CTA.
-// Returns true (on every thread) if an exactly zero pivot was met.
-template <int NB, int THREADS>
-__device__ bool gj_leaf(LeafSmem<NB>& L, int n) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < NB; i += THREADS) L.used[i] = 0;
-  __syncthreads();
-  bool any_zero = false;
-  for (int k = 0; k < n; ++k) {
-    if (warp == 0) {
-      double best = -1.0;
-      int bi = NB;
-      for (int i = lane; i < n; i += 32) {
-        if (!L.used[i]) {
-          double v = cabs1(L.a[i][k]);
-          if (v > best) {
-            best = v;
-            bi = i;
-          }
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        double ob = __shfl_xor_sync(0xffffffffu, best, off);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      const bool zero = !(best > 0.0);
-      int p = bi;
-      if (p >= n) p = k;  // only reachable for NaN columns
-      double2 inv = zero ? make_double2(1.0, 0.0) : crecip(L.a[p][k]);
-      for (int i = lane; i < n; i += 32) L.fcol[i] = (i == p) ? make_double2(0.0, 0.0) : L.a[i][k];
-      for (int j = lane; j < n; j += 32) L.prow[j] = (j == k) ? inv : cmul(L.a[p][j], inv);
-      if (lane == 0) {
-        L.piv[k] = p;
-        L.used[p] = 1;
-      }
-      any_zero |= zero;
-    }
-    __syncthreads();
-    const int p = L.piv[k];
-    for (int e = tid; e < NB * NB; e += THREADS) {
-      int i = e / NB, j = e % NB;
-      if (i >= n || j >= n) continue;
-      double2 pr = L.prow[j];
-      if (i == p) {
-        L.a[i][j] = pr;
-      } else {
-        double2 f = L.fcol[i];
-        double2 v = (j == k) ? make_double2(0.0, 0.0) : L.a[i][j];
-        v.x -= f.x * pr.x - f.y * pr.y;
-        v.y -= f.x * pr.y + f.y * pr.x;
-        L.a[i][j] = v;
-      }
-    }
-    __syncthreads();
-  }
-  return __syncthreads_or(any_zero ? 1 : 0) != 0;
-}
-
-// One CTA per matrix: storage S after gj_leaf satisfies
-// inv(A)[r][piv[k]] = S[piv[r]][k]; pivot choice max |re|+|im| among unused
-// rows (LAPACK izamax), lowest index on ties; virtual row interchanges.
-template <int NB, int THREADS>
-__global__ void __launch_bounds__(THREADS)
+// One CTA (256 threads) per matrix, n <= 32.
+__global__ void __launch_bounds__(256)
     leaf_inverse_kernel(const double2* __restrict__ X, int64_t ldx, int64_t sx, double2* __restrict__ Y,
                         int64_t ldy, int64_t sy, int n, int* flags, int64_t flag_stride) {
-  __shared__ LeafSmem<NB> L;
+  __shared__ Leaf32 L;
   const int tid = threadIdx.x;
   X += blockIdx.x * sx;
   Y += blockIdx.x * sy;
   int* flag = flags + blockIdx.x * flag_stride;
-  for (int e = tid; e < NB * NB; e += THREADS) {
-    int i = e / NB, j = e % NB;
-    if (i < n && j < n) L.a[i][j] = X[(int64_t)i * ldx + j];
+  for (int e = tid; e < 32 * 32; e += 256) {
+    int i = e >> 5, j = e & 31;
+    if (i < n && j < n) L.a[0][i][j] = X[(int64_t)i * ldx + j];
   }
   __syncthreads();
-  const bool any_zero = gj_leaf<NB, THREADS>(L, n);
+  const bool any_zero = gj_leaf32(L, n);
   if (tid == 0 && any_zero) atomicMax(flag, 1);
-  for (int e = tid; e < NB * NB; e += THREADS) {
-    int r = e / NB, k = e % NB;
-    if (r < n && k < n) Y[(int64_t)r * ldy + L.piv[k]] = L.a[L.piv[r]][k];
+  const double2 (*S)[33] = L.a[n & 1];
+  for (int e = tid; e < 32 * 32; e += 256) {
+    int r = e >> 5, k = e & 31;
+    if (r < n && k < n) Y[(int64_t)r * ldy + L.piv[k]] = S[L.piv[r]][k];
   }
 }
 
@@ -305,121 +288,141 @@ __device__ __forceinline__ void tile_mma(double (&acc)[4][2], const double2 (*sA
 __device__ __forceinline__ int acc_row() { return ((threadIdx.x >> 5) & 3) * 8 + ((threadIdx.x & 31) >> 2); }
 __device__ __forceinline__ int acc_col(int jn) { return ((threadIdx.x >> 5) >> 2) * 16 + jn * 4 + (threadIdx.x & 3); }
 
+// CTA-wide: invert the diagonal tile W[j0:j0+jb, j0:j0+jb] and publish the
+// zero-padded 32 x 32 Dinv to gDp.
+__device__ void leaf_publish(Leaf32& L, const double2* W, int64_t ld, int j0, int jb, double2* gDp, int* flag) {
+  for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+    const int i = e >> 5, j = e & 31;
+    L.a[0][i][j] = (i < jb && j < jb) ? ldcg2(W + (int64_t)(j0 + i) * ld + j0 + j) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const bool zero = gj_leaf32(L, jb);
+  if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
+  const double2 (*S)[33] = L.a[jb & 1];
+  for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+    const int r = e >> 5, k = e & 31;
+    if (r < jb && k < jb)
+      gDp[r * kT + L.piv[k]] = S[L.piv[r]][k];
+    else
+      gDp[r * kT + k] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+}
+
+struct TileCtx {
+  int n, nt, p, j0, jb;
+  const double2* Wc;
+  int64_t ldc;
+  double2* Wn;
+  int64_t ldn;
+  int r_tk;  // column tile whose R = Dinv W[J,K] is cached in S.r
+};
+
+// One 32 x 32 output tile of the Gauss-Jordan update of panel p.
+__device__ void gj_tile(PinvSmem& S, TileCtx& T, int t) {
+  const int tk = t / T.nt, ti = t % T.nt, p = T.p;
+  const int i0 = ti * kT, k0 = tk * kT;
+  const int ib = min(kT, T.n - i0), kb = min(kT, T.n - k0);
+  double acc[4][2];
+  double2* out = T.Wn + (int64_t)i0 * T.ldn + k0;
+  const int orow = acc_row();
+  if (ti == p && tk == p) {
+    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+      const int i = e >> 5, j = e & 31;
+      if (i < ib && j < kb) out[(int64_t)i * T.ldn + j] = S.d[i][j];
+    }
+    return;
+  }
+  if (tk != p && T.r_tk != tk) {  // R = Dinv . W[J,K]
+    __syncthreads();
+    load_tile(S.x, T.Wc + (int64_t)T.j0 * T.ldc + k0, T.ldc, T.jb, kb);
+    __syncthreads();
+    tile_mma(acc, S.d, S.x);
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn) S.r[orow][acc_col(jn)] = make_double2(acc[jn][0], acc[jn][1]);
+    __syncthreads();
+    T.r_tk = tk;
+  }
+  if (ti == p) {  // W'[J,K] = R
+    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+      const int i = e >> 5, j = e & 31;
+      if (i < ib && j < kb) out[(int64_t)i * T.ldn + j] = S.r[i][j];
+    }
+    return;
+  }
+  __syncthreads();
+  load_tile(S.c, T.Wc + (int64_t)i0 * T.ldc + T.j0, T.ldc, ib, T.jb);
+  __syncthreads();
+  tile_mma(acc, S.c, tk == p ? S.d : S.r);
+#pragma unroll
+  for (int jn = 0; jn < 4; ++jn) {
+    const int oc = acc_col(jn);
+    if (orow < ib && oc < kb) {
+      double2 v = make_double2(-acc[jn][0], -acc[jn][1]);
+      if (tk != p) {
+        const double2 w = ldcg2(T.Wc + (int64_t)(i0 + orow) * T.ldc + k0 + oc);
+        v.x += w.x;
+        v.y += w.y;
+      }
+      out[(int64_t)orow * T.ldn + oc] = v;
+    }
+  }
+}
+
+// Lookahead: during panel p, CTA 0 first computes the next diagonal tile
+// W'[p+1,p+1], immediately factors it and publishes Dinv_{p+1} (double-
+// buffered gD) while the other CTAs update the rest -> one grid barrier per
+// panel, the leaf latency hidden behind the update.
 __global__ void __launch_bounds__(256, 1)
     persistent_inverse_kernel(const double2* __restrict__ X, int64_t ldx, double2* Y, int64_t ldy, int n,
                               double2* work, double2* gD, unsigned* barrier, int* flag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
+  Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0]);  // spans x and c
   const int nt = (n + kT - 1) / kT, ntiles = nt * nt, G = gridDim.x;
   unsigned target = 0;
-  const double2* Wc = X;
-  int64_t ldc = ldx;
+  if (blockIdx.x == 0) leaf_publish(L, X, ldx, 0, min(kT, n), gD, flag);
+  target += G;
+  grid_barrier(barrier, target);
+  TileCtx T;
+  T.n = n;
+  T.nt = nt;
+  T.Wc = X;
+  T.ldc = ldx;
+  const int workers = G > 1 ? G - 1 : 1, wid = G > 1 ? (int)blockIdx.x - 1 : 0;
   for (int p = 0; p < nt; ++p) {
-    const int j0 = p * kT, jb = min(kT, n - j0);
-    double2* Wn = ((nt - 1 - p) % 2 == 0) ? Y : work;
-    const int64_t ldn = (Wn == Y) ? ldy : n;
-    // ---- leaf: CTA 0 inverts W[J,J] ----
-    if (blockIdx.x == 0) {
-      LeafSmem<kT>& L = *reinterpret_cast<LeafSmem<kT>*>(&S.x[0][0]);  // spans x and c
-      for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
-        const int i = e / kT, j = e % kT;
-        if (i < jb && j < jb) L.a[i][j] = ldcg2(Wc + (int64_t)(j0 + i) * ldc + j0 + j);
-      }
-      __syncthreads();
-      const bool zero = gj_leaf<kT, 256>(L, jb);
-      if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
-      for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
-        const int r = e / kT, k = e % kT;
-        double2 v = make_double2(0.0, 0.0);
-        // inv[r][piv[k]] = a[piv[r]][k]  ->  write Dinv[r][piv[k]]
-        if (r < jb && k < jb) gD[r * kT + L.piv[k]] = L.a[L.piv[r]][k];
-        else if (r < kT && k < kT && (r >= jb || k >= jb)) gD[r * kT + k] = v;
-      }
-    }
-    target += G;
-    grid_barrier(barrier, target);
-    // ---- update ----
-    load_tile(S.d, gD, kT, kT, kT);
+    T.p = p;
+    T.j0 = p * kT;
+    T.jb = min(kT, n - T.j0);
+    T.Wn = ((nt - 1 - p) % 2 == 0) ? Y : work;
+    T.ldn = (T.Wn == Y) ? ldy : n;
+    T.r_tk = -1;
+    load_tile(S.d, gD + (p & 1) * kT * kT, kT, kT, kT);
     __syncthreads();
-    int r_tk = -1;  // column tile whose R = Dinv W[J,K] is cached in S.r
-    const int chunk = (ntiles + G - 1) / G;
-    const int t_begin = blockIdx.x * chunk, t_end = min(ntiles, t_begin + chunk);
-    for (int t = t_begin; t < t_end; ++t) {
-      const int tk = t / nt, ti = t % nt;
-      const int i0 = ti * kT, k0 = tk * kT;
-      const int ib = min(kT, n - i0), kb = min(kT, n - k0);
-      double acc[4][2];
-      double2* out = Wn + (int64_t)i0 * ldn + k0;
-      const int orow = acc_row();
-      if (ti == p && tk == p) {
-        for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
-          const int i = e / kT, j = e % kT;
-          if (i < ib && j < kb) out[(int64_t)i * ldn + j] = S.d[i][j];
-        }
-        continue;
-      }
-      if (tk != p && r_tk != tk) {  // R = Dinv . W[J,K]
-        __syncthreads();
-        load_tile(S.x, Wc + (int64_t)j0 * ldc + k0, ldc, jb, kb);
-        __syncthreads();
-        tile_mma(acc, S.d, S.x);
-#pragma unroll
-        for (int jn = 0; jn < 4; ++jn) S.r[orow][acc_col(jn)] = make_double2(acc[jn][0], acc[jn][1]);
-        __syncthreads();
-        r_tk = tk;
-      }
-      if (ti == p) {  // W'[J,K] = R
-        for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
-          const int i = e / kT, j = e % kT;
-          if (i < ib && j < kb) out[(int64_t)i * ldn + j] = S.r[i][j];
-        }
-        continue;
-      }
+    const int sp = (p + 1 < nt) ? (p + 1) * nt + (p + 1) : -1;
+    if (blockIdx.x == 0 && sp >= 0) {
+      gj_tile(S, T, sp);
       __syncthreads();
-      load_tile(S.c, Wc + (int64_t)i0 * ldc + j0, ldc, ib, jb);
-      __syncthreads();
-      tile_mma(acc, S.c, tk == p ? S.d : S.r);
-#pragma unroll
-      for (int jn = 0; jn < 4; ++jn) {
-        const int oc = acc_col(jn);
-        if (orow < ib && oc < kb) {
-          double2 v = make_double2(-acc[jn][0], -acc[jn][1]);
-          if (tk != p) {
-            const double2 w = ldcg2(Wc + (int64_t)(i0 + orow) * ldc + k0 + oc);
-            v.x += w.x;
-            v.y += w.y;
-          }
-          out[(int64_t)orow * ldn + oc] = v;
-        }
-      }
+      leaf_publish(L, T.Wn, T.ldn, (p + 1) * kT, min(kT, n - (p + 1) * kT), gD + ((p + 1) & 1) * kT * kT, flag);
+    }
+    if (G == 1 || blockIdx.x > 0) {
+      const int chunk = (ntiles + workers - 1) / workers;
+      const int t0 = wid * chunk, t1 = min(ntiles, t0 + chunk);
+      for (int t = t0; t < t1; ++t)
+        if (t != sp || G == 1) gj_tile(S, T, t);
     }
     target += G;
     grid_barrier(barrier, target);
-    Wc = Wn;
-    ldc = ldn;
+    T.Wc = T.Wn;
+    T.ldc = T.ldn;
   }
-}
-
-
-GemmTerm term(const double2* A, int64_t lda, uint8_t opA, const double2* B, int64_t ldb, uint8_t opB,
-              int K, int sign) {
-  GemmTerm t{};
-  t.A = A;
-  t.B = B;
-  t.lda = lda;
-  t.ldb = ldb;
-  t.K = K;
-  t.opA = opA;
-  t.opB = opB;
-  t.sign = static_cast<int8_t>(sign);
-  return t;
 }
 
 }  // namespace
 
 // work: n*n ping-pong buffer (also the exact fallback's scratch), then the
-// published Dinv tile (kT*kT) and the grid-barrier counter.
-int64_t block_inverse_workspace(int n) { return (int64_t)n * n + kT * kT + 1; }
+// published Dinv tiles (2 x kT*kT, double-buffered) and the grid-barrier counter.
+int64_t block_inverse_workspace(int n) { return (int64_t)n * n + 2 * kT * kT + 1; }
 
 namespace {
 int coop_grid_limit() {
@@ -444,13 +447,26 @@ cudaError_t launch_leaf_inverse_batched(const double2* X, int64_t ldx, int64_t s
                                         cudaStream_t stream) {
   if (n <= 0 || batch <= 0) return cudaSuccess;
   if (n > kLeaf) return cudaErrorInvalidValue;
-  leaf_inverse_kernel<kLeaf, kLeafThreads>
-      <<<batch, kLeafThreads, 0, stream>>>(X, ldx, strideX, Y, ldy, strideY, n, flags, 1);
+  leaf_inverse_kernel<<<batch, kLeafThreads, 0, stream>>>(X, ldx, strideX, Y, ldy, strideY, n, flags, 1);
   count_launch();
   return cudaGetLastError();
 }
 
 namespace {
+
+GemmTerm term(const double2* A, int64_t lda, uint8_t opA, const double2* B, int64_t ldb, uint8_t opB,
+              int K, int sign) {
+  GemmTerm t{};
+  t.A = A;
+  t.B = B;
+  t.lda = lda;
+  t.ldb = ldb;
+  t.K = K;
+  t.opA = opA;
+  t.opB = opB;
+  t.sign = static_cast<int8_t>(sign);
+  return t;
+}
 
 // Multi-launch variant (no cooperative launch available): per panel one leaf
 // kernel and two grouped GEMM launches.
@@ -468,7 +484,7 @@ cudaError_t levels_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ld
     const int jb = (n - j0 < kLeaf) ? n - j0 : kLeaf;
     const int j1 = j0 + jb;
     // 1. leaf: W[J,J] = inv(R[J,J])
-    leaf_inverse_kernel<kLeaf, kLeafThreads><<<1, kLeafThreads, 0, stream>>>(
+    leaf_inverse_kernel<<<1, kLeafThreads, 0, stream>>>(
         R + (int64_t)j0 * ldr + j0, ldr, 0, W + (int64_t)j0 * ldw + j0, ldw, 0, jb, flag, 0);
     count_launch();
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
@@ -545,7 +561,7 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
   const int limit = coop_grid_limit();
   if (panels > 1 && limit > 0) {
     double2* gD = work + (int64_t)n * n;
-    unsigned* barrier = reinterpret_cast<unsigned*>(gD + kT * kT);
+    unsigned* barrier = reinterpret_cast<unsigned*>(gD + 2 * kT * kT);
     if ((err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream)) != cudaSuccess) return err;
     int grid = panels * panels < limit ? panels * panels : limit;
     if (grid > device_sm_count()) grid = device_sm_count();

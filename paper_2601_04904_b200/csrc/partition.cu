@@ -28,7 +28,7 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
   if (len < 2 || lo < 0 || hi > A.n) throw ShapeError("invalid partition range");
   if (WA.n != len || WA.b != b || WA.a != a) throw ShapeError("partition workspace shape");
   const int mx = (int)std::max(a, b);
-  ctx.reserve_slots(40, (int64_t)mx * mx);
+  ctx.reserve_slots(64, (int64_t)mx * mx);
   ctx.reset_status();
   // Working copies of the partition (dist.py:194-202) and zeroed tip deltas.
   auto stage = [&](const BtaDev& src, const BtaDev& w) {
@@ -112,7 +112,7 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
   const bool fused = F.fused;
   if (fused && (!B || !WB || !ZR || !XB)) throw ShapeError("fused factors require the right-hand side");
   const int mx = (int)std::max(a, b);
-  ctx.reserve_slots(40, (int64_t)mx * mx);
+  ctx.reserve_slots(64, (int64_t)mx * mx);
   cudaStream_t s = ctx.stream();
   cuda_check(cudaEventRecord(ctx.timer(2), s), "timer");
   const Mat ytt = XR.T();
@@ -151,12 +151,14 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       seed(k_top, lo);
     }
     L.flush();
+    BackPipe pipe(ctx);
     for (int64_t t = 0; t < len - 1; ++t) {
       const int64_t i = down ? hi - 2 - t : lo + 1 + t;
       const int64_t p = down ? i + 1 : i - 1;  // previously solved neighbour
       const int64_t e = down ? i : i - 1;
       BackStep st;
       st.k = 2;
+      st.late[0][0] = true;
       st.g = F.SA(i - lo);
       st.rs[0] = down ? A.U(e) : A.L(e), st.rs[1] = el(WA, i, false);
       st.qs[0] = down ? A.L(e) : A.U(e), st.qs[1] = el(WA, i, true);
@@ -173,7 +175,9 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
         st.zcol[0] = down ? XB->L(e) : XB->U(e), st.zcol[1] = XB->AR(i);
         st.zdiag = XB->D(i);
       }
-      back_step(ctx, s, st);
+      pipe.early(L, st, (int)(t & 1));
+      L.flush();
+      pipe.rest(L, st, (int)(t & 1));
     }
   } else {
     seed(k_top, lo);
@@ -191,11 +195,13 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       }
     }
     L.flush();
+    BackPipe pipe(ctx);
     for (int64_t i = hi - 2; i > lo; --i) {
       const int q = (int)((hi - 2 - i) & 1);
       const bool last_step = i == lo + 1;
       BackStep st;
       st.k = 3;
+      st.late[1][1] = true;
       st.g = F.SA(i - lo);
       st.rs[0] = F.FC(i - lo), st.rs[1] = A.U(i), st.rs[2] = el(WA, i, false);
       st.qs[0] = F.FR(i - lo), st.qs[1] = A.L(i), st.qs[2] = el(WA, i, true);
@@ -223,7 +229,9 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
         st.zcol[1] = XB->L(i), st.zcol[2] = XB->AR(i);
         st.zdiag = XB->D(i);
       }
-      back_step(ctx, s, st);
+      pipe.early(L, st, q);
+      L.flush();
+      pipe.rest(L, st, q);
       yfr = st.col[0], yfc = st.row[0];
       if (fused) zfr = st.zcol[0], zfc = st.zrow[0];
     }

@@ -13,7 +13,7 @@ namespace bsel {
 
 namespace {
 constexpr int kRing = 8;        // slots per ring half
-constexpr int kBackBase = 16;   // first slot used by back_step
+constexpr int kBackBase = 16;   // first slot used by back_step (2 x kBackSlots)
 Mat rt(Context& ctx, int parity, int k, int r, int c) { return ctx.tmp(parity * kRing + k, r, c); }
 }  // namespace
 
@@ -137,40 +137,71 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   cuda_check(cudaEventRecord(ctx.event(2 + parity), sB), "record B");
 }
 
-void back_step(Context& ctx, cudaStream_t s, const BackStep& st) {
-  const int k = st.k;
+namespace {
+constexpr int kBackSlots = 24;  // per parity half
+bool any_late_col(const BackStep& st, int j) {  // ya[l][j] for some l
+  for (int l = 0; l < st.k; ++l)
+    if (st.late[l][j]) return true;
+  return false;
+}
+bool any_late_row(const BackStep& st, int j) {  // ya[j][l] for some l
+  for (int l = 0; l < st.k; ++l)
+    if (st.late[j][l]) return true;
+  return false;
+}
+}  // namespace
+
+// L1 of one step: the problems that only read inputs and trailing blocks.
+// `late_pass` selects which half is emitted.
+static void back_l1(Context& ctx, Level& L, const BackStep& st, int parity, bool late_pass, Mat* RA, Mat* CA,
+                    Mat* RZ, Mat* CZ, Mat* e, Mat* f) {
+  const int k = st.k, b = st.g.r;
   const bool fused = st.sc.p != nullptr;
-  const int b = st.g.r;
-  int slot = kBackBase;
-  auto T = [&](int r, int c) { return ctx.tmp(slot++, r, c); };
-  // trailing block sizes d_l: rs_l is (b x d_l)
-  Mat RA[3], CA[3], RZ[3], CZ[3], e[3], f[3];
-  Level L(s);
-  // L1: everything that only needs inputs.
+  const int base = kBackBase + parity * kBackSlots;
   for (int j = 0; j < k; ++j) {
     const int dj = st.rs[j].c;
-    RA[j] = T(b, dj);
-    CA[j] = T(dj, b);
-    L.out(RA[j]);
-    for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, st.ya[l][j], N);
-    L.out(CA[j]);
-    for (int l = 0; l < k; ++l) L.mm(+1, st.ya[j][l], N, st.qs[l], N);
-    if (fused) {
-      RZ[j] = T(b, dj);
-      CZ[j] = T(dj, b);
+    RA[j] = ctx.tmp(base + 6 * j + 0, b, dj);
+    CA[j] = ctx.tmp(base + 6 * j + 1, dj, b);
+    if (any_late_col(st, j) == late_pass) {
+      L.out(RA[j]);
+      for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, st.ya[l][j], N);
+    }
+    if (any_late_row(st, j) == late_pass) {
+      L.out(CA[j]);
+      for (int l = 0; l < k; ++l) L.mm(+1, st.ya[j][l], N, st.qs[l], N);
+    }
+    if (!fused) continue;
+    RZ[j] = ctx.tmp(base + 6 * j + 2, b, dj);
+    CZ[j] = ctx.tmp(base + 6 * j + 3, dj, b);
+    e[j] = ctx.tmp(base + 6 * j + 4, b, dj);
+    f[j] = ctx.tmp(base + 6 * j + 5, dj, b);
+    if (any_late_col(st, j) == late_pass) {
       L.out(RZ[j]);
       for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, st.yb[l][j], N);
+    }
+    if (any_late_row(st, j) == late_pass) {
       L.out(CZ[j]);
       for (int l = 0; l < k; ++l) L.mm(+1, st.yb[j][l], N, st.rs[l], H);
-      e[j] = T(b, dj);
-      f[j] = T(dj, b);
+    }
+    if (!late_pass) {
       L.out(e[j]).mm(+1, st.g, N, st.ss[j], N).mm(-1, st.sc, N, st.qs[j], H);
       L.out(f[j]).mm(+1, st.ws[j], N, st.g, H).mm(-1, st.qs[j], N, st.sc, N);
     }
   }
+}
+
+void BackPipe::early(Level& L, const BackStep& st, int parity) {
+  back_l1(ctx_, L, st, parity, false, RA, CA, RZ, CZ, e, f);
+}
+
+void BackPipe::rest(Level& L, const BackStep& st, int parity) {
+  const int k = st.k, b = st.g.r;
+  const bool fused = st.sc.p != nullptr;
+  back_l1(ctx_, L, st, parity, true, RA, CA, RZ, CZ, e, f);
   L.flush();
   // L2: row/column blocks of X_A and X_B, and the quadratic coupling.
-  Mat quad = T(b, b);
+  const int base = kBackBase + parity * kBackSlots + 18;
+  Mat quad = ctx_.tmp(base + 0, b, b);
   for (int j = 0; j < k; ++j) {
     L.out(st.row[j]).mm(-1, st.g, N, RA[j], N);
     L.out(st.col[j]).mm(-1, CA[j], N, st.g, N);
@@ -189,7 +220,8 @@ void back_step(Context& ctx, cudaStream_t s, const BackStep& st) {
   }
   L.flush();
   // L3
-  Mat phi = T(b, b), acc1 = T(b, b), acc2 = T(b, b), gq = T(b, b);
+  Mat phi = ctx_.tmp(base + 1, b, b), acc1 = ctx_.tmp(base + 2, b, b), acc2 = ctx_.tmp(base + 3, b, b);
+  Mat gq = ctx_.tmp(base + 4, b, b);
   L.out(phi);
   for (int l = 0; l < k; ++l) L.mm(-1, st.row[l], N, st.qs[l], N);
   if (fused) {
@@ -200,7 +232,7 @@ void back_step(Context& ctx, cudaStream_t s, const BackStep& st) {
     L.out(gq).mm(+1, st.g, N, quad, N);
   }
   L.flush();
-  // L4: diagonal blocks.
+  // L4 (left pending: the caller adds the next step's early L1 before flushing)
   L.out(st.diag).add(+1, st.g).mm(+1, phi, N, st.g, N);
   if (fused) {
     L.out(st.zdiag)
@@ -211,6 +243,13 @@ void back_step(Context& ctx, cudaStream_t s, const BackStep& st) {
         .mm(+1, acc2, N, st.g, H)
         .mm(+1, gq, N, st.g, H);
   }
+}
+
+void back_step(Context& ctx, cudaStream_t s, const BackStep& st) {
+  BackPipe pipe(ctx);
+  Level L(s);
+  pipe.early(L, st, 0);
+  pipe.rest(L, st, 0);
   L.flush();
 }
 

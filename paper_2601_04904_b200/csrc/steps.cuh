@@ -40,14 +40,34 @@ void streams_join(Context& ctx);
 
 // Generic Takahashi back-substitution step with k <= 3 trailing couplings
 // (rgf.py:322-398).  sc.p == nullptr -> selected inversion only.
+// late[l][j]: ya/yb[l][j] is produced by the PREVIOUS step's last level (its
+// diagonal block); all other trailing blocks are available one level earlier.
 struct BackStep {
   int k = 0;
   Mat g, sc;
   Mat rs[3], qs[3], ss[3], ws[3];
   Mat ya[3][3], yb[3][3];
+  bool late[3][3] = {};
   // outputs
   Mat row[3], col[3], diag;
   Mat zrow[3], zcol[3], zdiag;
+};
+
+// Software-pipelined form used by the sweeps:
+//   back_step_early(L, st_t)  queues step t's L1 products that do not read a
+//                              late block (they join step t-1's pending L4);
+//   L.flush();
+//   back_step_rest(L, st_t)   late L1 -> L2 -> L3, and queues L4 (pending).
+// Temporaries of step t live in slot half `parity` (t & 1).
+class BackPipe {
+ public:
+  explicit BackPipe(Context& ctx) : ctx_(ctx) {}
+  void early(Level& L, const BackStep& st, int parity);
+  void rest(Level& L, const BackStep& st, int parity);
+
+ private:
+  Context& ctx_;
+  Mat RA[3], CA[3], RZ[3], CZ[3], e[3], f[3];
 };
 void back_step(Context& ctx, cudaStream_t s, const BackStep& st);
 

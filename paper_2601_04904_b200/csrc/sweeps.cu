@@ -176,7 +176,7 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
   cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const bool fused = B != nullptr;
   const int mx = std::max(a, b);
-  ctx.reserve_slots(40, (int64_t)mx * mx);
+  ctx.reserve_slots(64, (int64_t)mx * mx);
   for (int i = 0; i < n - 1; ++i) {
     ring_wait(ctx, i);
     EndStep st;
@@ -304,7 +304,7 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
   cudaStream_t s = ctx.stream();
   const bool fused = B != nullptr;
   const int mx = std::max(a, b);
-  ctx.reserve_slots(40, (int64_t)mx * mx);
+  ctx.reserve_slots(64, (int64_t)mx * mx);
   Mat Xtt = cm(F.tip_inv, a, a);
   Mat Ztt;
   Level L(s);
@@ -317,7 +317,9 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
     Ztt = XB->T();
   }
   L.flush();
+  BackPipe pipe(ctx);
   for (int i = n - 1; i >= 0; --i) {
+    const int parity = (n - 1 - i) & 1;
     BackStep st;
     st.g = F.SA(i);
     if (i == n - 1) {
@@ -336,6 +338,7 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
       }
     } else {
       st.k = 2;
+      st.late[0][0] = true;  // X(i+1,i+1) comes from the previous step's last level
       st.rs[0] = A.U(i), st.rs[1] = F.ACe(i);
       st.qs[0] = A.L(i), st.qs[1] = F.ARe(i);
       st.ya[0][0] = XA.D(i + 1), st.ya[0][1] = XA.AC(i + 1), st.ya[1][0] = XA.AR(i + 1), st.ya[1][1] = Xtt;
@@ -353,8 +356,11 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
     }
     st.diag = XA.D(i);
     if (fused) st.zdiag = XB->D(i);
-    back_step(ctx, s, st);
+    pipe.early(L, st, parity);
+    L.flush();
+    pipe.rest(L, st, parity);
   }
+  L.flush();
 }
 
 }  // namespace
