@@ -27,27 +27,39 @@ __device__ __forceinline__ double2 crecip_fast(double2 z) {
   return make_double2(z.x * r, -z.y * r);
 }
 
-// 32 x 32 Gauss-Jordan with partial pivoting by 256 threads: ONE barrier per
-// pivot step (ping-pong buffers), pivot search by every warp with
-// redux.sync on the high word of |re|+|im| (monotone for non-negative
-// doubles), virtual row interchanges tracked in a register bitmask.
-// Thread t owns row t/8, columns 4*(t%8) .. +3.  Input in a[0]; the result
-// S (inv(A)[r][piv[k]] = S[piv[r]][k]) ends in a[n & 1].
+// 32 x 32 Gauss-Jordan with partial pivoting by 256 threads.  Thread t owns
+// row t/8, columns 4*(t%8) .. +3 IN REGISTERS for the whole elimination;
+// per pivot step only the pivot column (for the search and the row
+// multipliers) and the pivot row go through shared memory (the row buffer is
+// skewed so the 4 reads per thread are conflict-free broadcasts).  Pivot
+// search by every warp: redux.sync on the high word of |re|+|im| (monotone
+// for non-negative doubles), lowest row on ties; virtual row interchanges
+// tracked in a register bitmask.  Input in a (rows/cols < n); on return a
+// holds S with inv(A)[r][piv[k]] = S[piv[r]][k].
 struct Leaf32 {
-  double2 a[2][32][33];
+  double2 a[32][33];  // input, then (after the elimination) the result S
+  double2 col[2][32];
+  double2 row[2][32];
   int piv[32];
 };
+
+__device__ __forceinline__ int row_slot(int c) { return (c & 3) * 8 + (c >> 2); }
 
 __device__ bool gj_leaf32(Leaf32& L, int n) {
   const int t = threadIdx.x, lane = t & 31;
   const int i = t >> 3, c0 = (t & 7) * 4;
+  double2 v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    v[q] = (i < n && c0 + q < n) ? L.a[i][c0 + q] : make_double2(0.0, 0.0);
+  if ((t & 7) == 0) L.col[0][i] = v[0];
+  __syncthreads();
   unsigned used = 0u;
   bool any_zero = false;
   for (int k = 0; k < n; ++k) {
-    const double2 (*cur)[33] = L.a[k & 1];
-    double2 (*nxt)[33] = L.a[(k + 1) & 1];
+    const int buf = k & 1;
     const bool cand = lane < n && !((used >> lane) & 1u);
-    const unsigned key = cand ? (unsigned)__double2hiint(cabs1(cur[lane][k])) + 1u : 0u;
+    const unsigned key = cand ? (unsigned)__double2hiint(cabs1(L.col[buf][lane])) + 1u : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
     const unsigned ball = __ballot_sync(0xffffffffu, cand && key == kmax);
     const int p = __ffs(ball) - 1;
@@ -55,33 +67,38 @@ __device__ bool gj_leaf32(Leaf32& L, int n) {
     any_zero |= zero;
     used |= 1u << p;
     if (t == 0) L.piv[k] = p;
-    const double2 inv = zero ? make_double2(1.0, 0.0) : crecip_fast(cur[p][k]);
-    if (i < n) {
-      const double2 fi = cur[i][k];
+    if (i == p) {
 #pragma unroll
-      for (int c = c0; c < c0 + 4; ++c) {
-        if (c >= n) break;
-        const double2 pr = (c == k) ? inv : cmul(cur[p][c], inv);
-        if (i == p) {
-          nxt[i][c] = pr;
-        } else {
-          double2 v = (c == k) ? make_double2(0.0, 0.0) : cur[i][c];
-          v.x -= fi.x * pr.x - fi.y * pr.y;
-          v.y -= fi.x * pr.y + fi.y * pr.x;
-          nxt[i][c] = v;
-        }
-      }
+      for (int q = 0; q < 4; ++q) L.row[buf][row_slot(c0 + q)] = v[q];
     }
+    const double2 inv = zero ? make_double2(1.0, 0.0) : crecip_fast(L.col[buf][p]);
+    const double2 m = cmul(L.col[buf][i], inv);
+    __syncthreads();
+    // pivot row: a'[p][c] = inv * a[p][c]; other rows: a'[i][c] = a[i][c] - m a[p][c];
+    // column k: inv resp. -m.  One complex FMA per entry: a' = base + coef * a[p][c].
+    const bool prow = i == p;
+    const double2 coef = prow ? inv : make_double2(-m.x, -m.y);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + q;
+      const double2 pr = L.row[buf][row_slot(c)];
+      const double bx = prow ? 0.0 : v[q].x, by = prow ? 0.0 : v[q].y;
+      double2 nv;
+      nv.x = fma(coef.x, pr.x, fma(-coef.y, pr.y, bx));
+      nv.y = fma(coef.x, pr.y, fma(coef.y, pr.x, by));
+      if (c == k) nv = coef;
+      if (c < n && i < n) v[q] = nv;
+    }
+    const int q1 = k + 1 - c0;  // publish column k+1 (static selects keep v[] in registers)
+    if (q1 >= 0 && q1 < 4) L.col[buf ^ 1][i] = q1 == 0 ? v[0] : q1 == 1 ? v[1] : q1 == 2 ? v[2] : v[3];
     __syncthreads();
   }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) L.a[i][c0 + q] = v[q];
+  __syncthreads();
   return any_zero;
 }
 
-// In-place Gauss-Jordan with partial pivoting and *virtual* row interchanges
-// (rows are never moved: piv[k] is the physical pivot row of step k).  After
-// n steps the storage S satisfies inv(A)[r][piv[k]] = S[piv[r]][k].
-// Pivot choice: max |re|+|im| among unused rows (LAPACK izamax), lowest
-// index on ties.  Two barriers per elimination step.
 // One CTA (256 threads) per matrix, n <= 32.
 __global__ void __launch_bounds__(256)
     leaf_inverse_kernel(const double2* __restrict__ X, int64_t ldx, int64_t sx, double2* __restrict__ Y,
@@ -93,12 +110,12 @@ __global__ void __launch_bounds__(256)
   int* flag = flags + blockIdx.x * flag_stride;
   for (int e = tid; e < 32 * 32; e += 256) {
     int i = e >> 5, j = e & 31;
-    if (i < n && j < n) L.a[0][i][j] = X[(int64_t)i * ldx + j];
+    if (i < n && j < n) L.a[i][j] = X[(int64_t)i * ldx + j];
   }
   __syncthreads();
   const bool any_zero = gj_leaf32(L, n);
   if (tid == 0 && any_zero) atomicMax(flag, 1);
-  const double2 (*S)[33] = L.a[n & 1];
+  const double2 (*S)[33] = L.a;
   for (int e = tid; e < 32 * 32; e += 256) {
     int r = e >> 5, k = e & 31;
     if (r < n && k < n) Y[(int64_t)r * ldy + L.piv[k]] = S[L.piv[r]][k];
@@ -224,12 +241,15 @@ constexpr int kLeafThreads = 256;
 constexpr int kT = 32;
 constexpr int kTLD = kT + 2;  // 544-byte rows: conflict-free DMMA fragment loads
 
+struct PinvSmem;
 struct PinvSmem {
   double2 d[kT][kTLD];  // Dinv
   double2 x[kT][kTLD];  // row-panel tile W[J,K] -> R = Dinv W[J,K]
   double2 c[kT][kTLD];  // column-panel tile W[I,J]
   double2 r[kT][kTLD];
 };
+
+static_assert(sizeof(Leaf32) <= 2 * sizeof(double2) * kT * kTLD, "leaf scratch must fit in PinvSmem::x and ::c");
 
 __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 
@@ -293,12 +313,12 @@ __device__ __forceinline__ int acc_col(int jn) { return ((threadIdx.x >> 5) >> 2
 __device__ void leaf_publish(Leaf32& L, const double2* W, int64_t ld, int j0, int jb, double2* gDp, int* flag) {
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int i = e >> 5, j = e & 31;
-    L.a[0][i][j] = (i < jb && j < jb) ? ldcg2(W + (int64_t)(j0 + i) * ld + j0 + j) : make_double2(0.0, 0.0);
+    L.a[i][j] = (i < jb && j < jb) ? ldcg2(W + (int64_t)(j0 + i) * ld + j0 + j) : make_double2(0.0, 0.0);
   }
   __syncthreads();
   const bool zero = gj_leaf32(L, jb);
   if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
-  const double2 (*S)[33] = L.a[jb & 1];
+  const double2 (*S)[33] = L.a;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int r = e >> 5, k = e & 31;
     if (r < jb && k < jb)
@@ -375,7 +395,18 @@ __device__ void gj_tile(PinvSmem& S, TileCtx& T, int t) {
 // panel, the leaf latency hidden behind the update.
 __global__ void __launch_bounds__(256, 1)
     persistent_inverse_kernel(const double2* __restrict__ X, int64_t ldx, double2* Y, int64_t ldy, int n,
-                              double2* work, double2* gD, unsigned* barrier, int* flag) {
+                              double2* work, double2* gD, unsigned* barrier, int* flag,
+                              unsigned long long* trace) {
+  // trace (debug, may be null): per panel p, [8p+0] CTA0 start, [+1] after the
+  // lookahead tile, [+2] after the leaf, [+3] CTA0 at barrier, [+4] CTA1 done
+  // with its tiles, [+5] CTA1 after barrier (globaltimer ns).
+  auto stamp = [&](int slot) {
+    if (trace && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[slot] = t;
+    }
+  };
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
   Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0]);  // spans x and c
@@ -400,10 +431,13 @@ __global__ void __launch_bounds__(256, 1)
     load_tile(S.d, gD + (p & 1) * kT * kT, kT, kT, kT);
     __syncthreads();
     const int sp = (p + 1 < nt) ? (p + 1) * nt + (p + 1) : -1;
+    if (blockIdx.x == 0) stamp(8 * p + 0);
     if (blockIdx.x == 0 && sp >= 0) {
       gj_tile(S, T, sp);
       __syncthreads();
+      stamp(8 * p + 1);
       leaf_publish(L, T.Wn, T.ldn, (p + 1) * kT, min(kT, n - (p + 1) * kT), gD + ((p + 1) & 1) * kT * kT, flag);
+      stamp(8 * p + 2);
     }
     if (G == 1 || blockIdx.x > 0) {
       const int chunk = (ntiles + workers - 1) / workers;
@@ -411,8 +445,11 @@ __global__ void __launch_bounds__(256, 1)
       for (int t = t0; t < t1; ++t)
         if (t != sp || G == 1) gj_tile(S, T, t);
     }
+    if (blockIdx.x == 0) stamp(8 * p + 3);
+    if (blockIdx.x == 1) stamp(8 * p + 4);
     target += G;
     grid_barrier(barrier, target);
+    if (blockIdx.x == 1) stamp(8 * p + 5);
     T.Wc = T.Wn;
     T.ldc = T.ldn;
   }
@@ -422,6 +459,8 @@ __global__ void __launch_bounds__(256, 1)
 
 // work: n*n ping-pong buffer (also the exact fallback's scratch), then the
 // published Dinv tiles (2 x kT*kT, double-buffered) and the grid-barrier counter.
+unsigned long long* g_inverse_trace = nullptr;
+
 int64_t block_inverse_workspace(int n) { return (int64_t)n * n + 2 * kT * kT + 1; }
 
 namespace {
@@ -565,8 +604,9 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     if ((err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream)) != cudaSuccess) return err;
     int grid = panels * panels < limit ? panels * panels : limit;
     if (grid > device_sm_count()) grid = device_sm_count();
+    unsigned long long* trace = g_inverse_trace;
     void* args[] = {(void*)&X, (void*)&ldx, (void*)&Y, (void*)&ldy, (void*)&n,
-                    (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag};
+                    (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag, (void*)&trace};
     err = cudaLaunchCooperativeKernel((const void*)persistent_inverse_kernel, grid, 256, args, sizeof(PinvSmem),
                                       stream);
     count_launch();

@@ -20,6 +20,10 @@ namespace bsel {
 
 constexpr int kLeaf = 32;
 
+// Debug: when non-null (device buffer of 8*panels u64), the persistent
+// inverse records per-panel globaltimer stamps there.
+extern unsigned long long* g_inverse_trace;
+
 // Workspace (complex elements) needed by launch_block_inverse for one n x n.
 int64_t block_inverse_workspace(int n);
 
