@@ -300,7 +300,7 @@ def main():
                        "tip": a, "mode": "siq", "parallelism": f"partitions{world}" if world > 1 else "single",
                        "l2": "inputs 32 GiB >> 126 MB L2 (no flush needed)" if args.workload == "cfg4" else "inputs > L2"},
             "fp64_tflops_step": achieved_step,
-            "pct_fp64_peak_step": 100.0 * achieved_step / peak,
+            "pct_fp64_peak_step": 100.0 * achieved_step / (peak * world),  # of the N-GPU aggregate peak
             "flops_per_step": F,
             "roofline": {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA)", "achieved": gemm_tflops,
                          "peak": peak, "unit": "TFLOP/s", "frac": (gemm_tflops / peak) if gemm_tflops else None,
