@@ -247,6 +247,13 @@ def main():
         ms = float(t.item())
     clocks = clk.summary()
 
+    phases = {}
+    if world == 1:
+        bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, timings=phases)
+    else:
+        phases = solver.phase_seconds()
+    phases = {k: v * 1e3 for k, v in phases.items()}
+
     # ---- live per-kernel timing of the dominant kernel (one extra step) ----
     prof = _native.Profile()
     lib = _native.load_library()
@@ -307,6 +314,7 @@ def main():
                          "traffic": None, "peak_source": peak_src,
                          "share_of_step": prof.gemm_ms / ms if ms else None,
                          "inverse_ms_per_step": prof.inverse_ms, "gemm_launches_per_step": prof.gemm_launches},
+            "phases_ms": phases,
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,

@@ -1,4 +1,6 @@
 // Complex128 block inverse (see inverse.cuh).
+#include <cstdlib>
+
 #include "inverse.cuh"
 #include "zgemm.cuh"
 
@@ -464,6 +466,18 @@ unsigned long long* g_inverse_trace = nullptr;
 int64_t block_inverse_workspace(int n) { return (int64_t)n * n + 2 * kT * kT + 1; }
 
 namespace {
+// CTAs of the persistent inverse: all SMs by default; BSEL_INV_GRID caps it
+// (fewer CTAs become co-resident sooner while the aux stream holds SMs).
+int inverse_grid_cap() {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("BSEL_INV_GRID");
+    cap = e ? atoi(e) : 0;
+    if (cap <= 0 || cap > device_sm_count()) cap = device_sm_count();
+  }
+  return cap;
+}
+
 int coop_grid_limit() {
   static int limit = -1;
   if (limit < 0) {
@@ -603,7 +617,7 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     unsigned* barrier = reinterpret_cast<unsigned*>(gD + 2 * kT * kT);
     if ((err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream)) != cudaSuccess) return err;
     int grid = panels * panels < limit ? panels * panels : limit;
-    if (grid > device_sm_count()) grid = device_sm_count();
+    if (grid > inverse_grid_cap()) grid = inverse_grid_cap();
     unsigned long long* trace = g_inverse_trace;
     void* args[] = {(void*)&X, (void*)&ldx, (void*)&Y, (void*)&ldy, (void*)&n,
                     (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag, (void*)&trace};

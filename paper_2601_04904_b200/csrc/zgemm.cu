@@ -22,16 +22,16 @@ namespace bsel {
 
 namespace {
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, int BK_ = 8>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
-  static constexpr int BK = 8;                 // complex k per stage
+  static constexpr int BK = BK_;               // complex k per stage
   static constexpr int THREADS = 32 * WM * WN;
   static constexpr int WTM = BM / WM;          // warp tile rows (complex)
   static constexpr int WTN = BN / WN;          // warp tile cols (complex)
   static constexpr int FM = WTM / 8;           // DMMA row fragments per warp
   static constexpr int FN = WTN / 4;           // DMMA col fragments per warp (4 complex cols)
-  static constexpr int SA_LD = BK + 2;         // 160 B rows: conflict-free A fragments
+  static constexpr int SA_LD = BK + 2;         // 160 / 288 B rows (== 32 mod 128): conflict-free A fragments
   static constexpr int SB_LD = BN + 2;         // == 32 mod 128 B: conflict-free B fragments
   static constexpr int SA_ELEMS = BM * SA_LD;
   static constexpr int SB_ELEMS = BK * SB_LD;
@@ -43,7 +43,7 @@ struct Cfg {
   static_assert(FM * 8 == WTM && FN * 4 == WTN, "warp tile");
 };
 
-using Cfg64 = Cfg<64, 64, 2, 4, 4, 2>;
+using Cfg64 = Cfg<64, 64, 2, 4, 3, 2, 16>;
 using Cfg32 = Cfg<32, 32, 2, 2, 4, 4>;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
