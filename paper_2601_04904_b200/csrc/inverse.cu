@@ -466,13 +466,14 @@ unsigned long long* g_inverse_trace = nullptr;
 int64_t block_inverse_workspace(int n) { return (int64_t)n * n + 2 * kT * kT + 1; }
 
 namespace {
-// CTAs of the persistent inverse: all SMs by default; BSEL_INV_GRID caps it
-// (fewer CTAs become co-resident sooner while the aux stream holds SMs).
+// CTAs of the persistent inverse.  Default 64: fewer CTAs become co-resident
+// sooner while the aux stream's GEMM tiles hold SMs (measured on cfg4: 64
+// beats 148/96/32).  BSEL_INV_GRID overrides.
 int inverse_grid_cap() {
   static int cap = -1;
   if (cap < 0) {
     const char* e = getenv("BSEL_INV_GRID");
-    cap = e ? atoi(e) : 0;
+    cap = e ? atoi(e) : 64;
     if (cap <= 0 || cap > device_sm_count()) cap = device_sm_count();
   }
   return cap;

@@ -54,7 +54,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     return;
   }
   Mat f = rt(ctx, parity, 0, b, b), g = rt(ctx, parity, 1, a, b), w = rt(ctx, parity, 2, b, b);
-  Mat p = rt(ctx, parity, 3, a, b), k = rt(ctx, parity, 4, b, a), v = rt(ctx, parity, 5, b, b);
+  Mat p = rt(ctx, parity, 3, a, b), k = rt(ctx, parity, 4, b, a), q = rt(ctx, parity, 5, b, b);
   {
     Level L(sA);
     L.out(f).mm(+1, st.Lk, N, S, N);
@@ -67,20 +67,20 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
     L.flush();
   }
+  // B side in two levels: v Lk^H = Lk S_B Lk^H = f (Bd f^H) = f q removes the
+  // reference's serial chain w -> S_B -> v -> Bd (same product count).
   cuda_check(cudaStreamWaitEvent(sB, ctx.event(parity), 0), "wait A");
   Level L(sB);
   L.out(w).mm(+1, S, N, st.bd_i, N);
   L.out(p).mm(+1, g, N, st.bd_i, N);
   L.out(k).mm(+1, st.bd_i, N, g, H);
+  L.out(q).mm(+1, st.bd_i, N, f, H);
   L.flush();
   L.out(st.sb).mm(+1, w, N, S, H);
-  L.flush();
-  L.out(v).mm(+1, st.Lk, N, st.sb, N);
+  L.out(st.bd_j).add(+1, st.bd_j).mm(+1, f, N, q, N).mm(-1, st.BL, N, f, H).mm(-1, f, N, st.BU, N);
   L.out(st.br_j).add(+1, st.br_j).mm(-1, g, N, st.BU, N).mm(+1, p, N, f, H).mm(-1, st.br_i, N, f, H);
   L.out(st.bc_j).add(+1, st.bc_j).mm(-1, f, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, f, N, k, N);
   L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
-  L.flush();
-  L.out(st.bd_j).add(+1, st.bd_j).mm(+1, v, N, st.Lk, H).mm(-1, st.BL, N, f, H).mm(-1, f, N, st.BU, N);
   L.flush();
   cuda_check(cudaEventRecord(ctx.event(2 + parity), sB), "record B");
 }
@@ -111,28 +111,27 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   }
   if (!fused) return;
   cuda_check(cudaStreamWaitEvent(sB, ctx.event(parity), 0), "wait A");
-  Mat w = rt(ctx, parity, 3, b, b), v0 = rt(ctx, parity, 4, b, b), vn = rt(ctx, parity, 5, b, b);
-  Mat p = rt(ctx, parity, 6, a, b);
+  // v_n = L S_B, v_0 = fill_r S_B enter only as v_x y^H = f_x (Bd f_y^H):
+  // two levels instead of the reference's w -> S_B -> v -> update chain.
+  Mat w = rt(ctx, parity, 3, b, b), qn = rt(ctx, parity, 4, b, b), qr = rt(ctx, parity, 5, b, b);
+  Mat p = rt(ctx, parity, 6, a, b), kk = rt(ctx, parity, 7, b, a);
   Level L(sB);
   L.out(w).mm(+1, S, N, st.bd_i, N);
   L.out(p).mm(+1, g, N, st.bd_i, N);
+  L.out(qn).mm(+1, st.bd_i, N, fn, H);
+  L.out(qr).mm(+1, st.bd_i, N, fr, H);
+  L.out(kk).mm(+1, st.bd_i, N, g, H);
   L.flush();
   L.out(st.sb).mm(+1, w, N, S, H);
-  L.flush();
-  L.out(v0).mm(+1, st.fill_r, N, st.sb, N);
-  L.out(vn).mm(+1, st.L, N, st.sb, N);
   L.out(st.br_n).add(+1, st.br_n).mm(-1, g, N, st.BU, N).mm(-1, st.br_i, N, fn, H).mm(+1, p, N, fn, H);
   L.out(st.br_lo).add(+1, st.br_lo).mm(-1, g, N, st.bfill_c, N).mm(-1, st.br_i, N, fr, H).mm(+1, p, N, fr, H);
   L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
-  L.flush();
-  L.out(st.bd_n).add(+1, st.bd_n).mm(-1, fn, N, st.BU, N).mm(-1, st.BL, N, fn, H).mm(+1, vn, N, st.L, H);
-  L.out(st.nbfill_c).mm(-1, fn, N, st.bfill_c, N).mm(-1, st.BL, N, fr, H).mm(+1, vn, N, st.fill_r, H);
-  L.out(st.nbfill_r).mm(-1, fr, N, st.BU, N).mm(-1, st.bfill_r, N, fn, H).mm(+1, v0, N, st.L, H);
-  L.out(st.bd_lo).add(+1, st.bd_lo).mm(-1, fr, N, st.bfill_c, N).mm(-1, st.bfill_r, N, fr, H)
-      .mm(+1, v0, N, st.fill_r, H);
-  L.out(st.bc_n).add(+1, st.bc_n).mm(-1, fn, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, vn, N, st.ar_i, H);
-  L.out(st.bc_lo).add(+1, st.bc_lo).mm(-1, fr, N, st.bc_i, N).mm(-1, st.bfill_r, N, g, H)
-      .mm(+1, v0, N, st.ar_i, H);
+  L.out(st.bd_n).add(+1, st.bd_n).mm(-1, fn, N, st.BU, N).mm(-1, st.BL, N, fn, H).mm(+1, fn, N, qn, N);
+  L.out(st.nbfill_c).mm(-1, fn, N, st.bfill_c, N).mm(-1, st.BL, N, fr, H).mm(+1, fn, N, qr, N);
+  L.out(st.nbfill_r).mm(-1, fr, N, st.BU, N).mm(-1, st.bfill_r, N, fn, H).mm(+1, fr, N, qn, N);
+  L.out(st.bd_lo).add(+1, st.bd_lo).mm(-1, fr, N, st.bfill_c, N).mm(-1, st.bfill_r, N, fr, H).mm(+1, fr, N, qr, N);
+  L.out(st.bc_n).add(+1, st.bc_n).mm(-1, fn, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, fn, N, kk, N);
+  L.out(st.bc_lo).add(+1, st.bc_lo).mm(-1, fr, N, st.bc_i, N).mm(-1, st.bfill_r, N, g, H).mm(+1, fr, N, kk, N);
   L.flush();
   cuda_check(cudaEventRecord(ctx.event(2 + parity), sB), "record B");
 }

@@ -144,17 +144,16 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
     }
     if (fused) {
       cuda_check(cudaStreamWaitEvent(sB, ctx.event(i & 1), 0), "wait A");
-      Mat w = ctx.tmp(r + 1, b, b), v = ctx.tmp(r + 2, b, b), sb = F.SB(i);
+      // v L^H = L S_B L^H = t1 (Bd t1^H): two levels (same product count).
+      Mat w = ctx.tmp(r + 1, b, b), q = ctx.tmp(r + 2, b, b), sb = F.SB(i);
       Level L(sB);
       L.out(w).mm(+1, S, N, B->D(i), N);
+      L.out(q).mm(+1, B->D(i), N, t1, H);
       L.flush();
       L.out(sb).mm(+1, w, N, S, H);
-      L.flush();
-      L.out(v).mm(+1, A.L(i), N, sb, N);
-      L.flush();
       L.out(B->D(i + 1))
           .add(+1, B->D(i + 1))
-          .mm(+1, v, N, A.L(i), H)
+          .mm(+1, t1, N, q, N)
           .mm(-1, B->L(i), N, t1, H)
           .mm(-1, t1, N, B->U(i), N);
       L.flush();
