@@ -166,6 +166,82 @@ def run_reference(args, n, b, a):
     print(json.dumps(line), flush=True)
 
 
+def rank_slices(plan, rank, n):
+    """Block ranges one rank needs (inputs) and owns (outputs) in the
+    distributed scheme: its partition, the separators next to it, and every
+    partition separator (reduced-system assembly, dist.py:479-486)."""
+    lo, hi = plan.ranges[rank]
+    off = (max(lo - 1, 0), min(hi, n - 1))
+    ins = {"diag": [(lo, hi)], "arrow_row": [(lo, hi)], "arrow_col": [(lo, hi)], "lower": [off], "upper": [off]}
+    for p in range(plan.num_parts - 1):
+        g = plan.ranges[p][1] - 1
+        if not off[0] <= g < off[1]:
+            ins["lower"].append((g, g + 1))
+            ins["upper"].append((g, g + 1))
+    mine = (lo, min(hi, n - 1))
+    outs = {"diag": [(lo, hi)], "arrow_row": [(lo, hi)], "arrow_col": [(lo, hi)], "lower": [mine], "upper": [mine]}
+    return ins, outs
+
+
+def dist_e2e(args, solver, A, B, n, world, rank, dev, dist):
+    """N>1 end-to-end: every step each rank copies the input blocks it needs
+    from pinned host memory, runs its part of the distributed solve, and
+    copies the solution blocks it owns back (outputs stay sharded)."""
+    import torch
+
+    ins, outs = rank_slices(solver.plan, rank, n)
+
+    def pinned_like(t):
+        return torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+
+    h2d, d2h = [], []  # (device view, pinned host buffer)
+    for M in (A, B):
+        for kind, ranges in ins.items():
+            for s, e in ranges:
+                if e > s:
+                    view = getattr(M, kind)[s:e]
+                    host = pinned_like(view)
+                    host.copy_(view)
+                    h2d.append((view, host))
+        host = pinned_like(M.tip)
+        host.copy_(M.tip)
+        h2d.append((M.tip, host))
+    for X in solver.out:
+        for kind, ranges in outs.items():
+            for s, e in ranges:
+                if e > s:
+                    view = getattr(X, kind)[s:e]
+                    d2h.append((view, pinned_like(view)))
+        if rank == 0:
+            d2h.append((X.tip, pinned_like(X.tip)))
+
+    def step():
+        for view, host in h2d:
+            view.copy_(host, non_blocking=True)
+        solver.solve()
+        for view, host in d2h:
+            host.copy_(view, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    stats = torch.tensor([ms, sum(h.numel() * 16 for _, h in h2d), sum(h.numel() * 16 for _, h in d2h)],
+                         dtype=torch.float64, device=dev)
+    mx = stats[:1].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+    return {"value": float(mx.item()), "unit": "ms", "h2d_bytes_per_step": int(stats[1].item()),
+            "d2h_bytes_per_step": int(stats[2].item()),
+            "note": "per rank: H2D of its partition + separators, D2H of its owned solution blocks; max over ranks"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -288,6 +364,8 @@ def main():
         e2e_ms = s2.elapsed_time(e2) / args.steps
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": hA.nbytes + hB.nbytes,
                "d2h_bytes_per_step": hXA.nbytes + hXB.nbytes}
+    elif not args.no_e2e:
+        e2e = dist_e2e(args, solver, A, B, n, world, rank, dev, dist)
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
     cpu = None

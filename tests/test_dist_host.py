@@ -158,3 +158,29 @@ def test_partition_counts_match_reference(name):
     record_sweep(c, nr, b, a, mode, "forward")
     record_sweep(c, nr, b, a, mode, "backward")
     assert c.as_dict() == meta["counts"]
+
+
+@pytest.mark.parametrize("n,parts", [(1024, 8), (1024, 4), (12, 3), (8, 4), (20, 2)])
+def test_bench_rank_slices_cover_pattern(n, parts):
+    """bench.py's N>1 end-to-end copies: the owned output blocks of all ranks
+    partition the pattern exactly; every rank's inputs include its partition,
+    its neighbouring separators and all partition separators."""
+    import bench
+    from paper_2601_04904_b200 import plan_partitions
+    plan = plan_partitions(n, parts, "siq")
+    owned = {k: [] for k in ("diag", "arrow_row", "arrow_col", "lower", "upper")}
+    seps = [plan.ranges[p][1] - 1 for p in range(parts - 1)]
+    for r in range(parts):
+        ins, outs = bench.rank_slices(plan, r, n)
+        for k, rs in outs.items():
+            for s, e in rs:
+                owned[k].extend(range(s, e))
+        lo, hi = plan.ranges[r]
+        need_off = set(range(max(lo - 1, 0), min(hi, n - 1))) | set(seps)
+        have_off = {g for s, e in ins["lower"] for g in range(s, e)}
+        assert need_off <= have_off
+        assert {g for s, e in ins["diag"] for g in range(s, e)} == set(range(lo, hi))
+    for k in ("diag", "arrow_row", "arrow_col"):
+        assert sorted(owned[k]) == list(range(n))
+    for k in ("lower", "upper"):
+        assert sorted(owned[k]) == list(range(n - 1))
