@@ -253,6 +253,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=8)
+    ap.add_argument("--partitions", type=int, default=None,
+                    help="N=1: in-GPU partitions of solve_selected (default: library default)")
+    ap.add_argument("--no-seq", action="store_true", help="skip the extra sequential-RGF measurement")
     args = ap.parse_args()
     n, b, a, cfg_idx = WORKLOADS[args.workload]
     if args.n:
@@ -284,13 +287,16 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
 
+    parts = 1
     if world == 1:
         XA, XB = bs.DeviceBta.empty(n, b, a, dev, zero=False), bs.DeviceBta.empty(n, b, a, dev, zero=False)
         ctx = _native.Context.get(local)
         ws = torch.empty(ctx.workspace_bytes(n, b, a, True), dtype=torch.uint8, device=dev)
 
+        parts = args.partitions if args.partitions else bs.default_partitions(n)
+
         def step():
-            bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws)
+            bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, partitions=parts)
     else:
         solver = bdist.DistSolver(A, B, "siq", world, rank, dev)
 
@@ -324,8 +330,19 @@ def main():
     clocks = clk.summary()
 
     phases = {}
+    seq_ms = None
     if world == 1:
-        bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, timings=phases)
+        bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, timings=phases, partitions=parts)
+        if parts > 1 and not args.no_seq:
+            # the pure sequential RGF sweeps (rgf.py order), for reference
+            bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, partitions=1)
+            s1, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s1.record()
+            for _ in range(2):
+                bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, partitions=1)
+            e1.record()
+            torch.cuda.synchronize()
+            seq_ms = s1.elapsed_time(e1) / 2
     else:
         phases = solver.phase_seconds()
     phases = {k: v * 1e3 for k, v in phases.items()}
@@ -353,12 +370,12 @@ def main():
         torch.cuda.empty_cache()
         hXA = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
         hXB = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
-        bs.solve_selected(hA, hB, "siq", out=(hXA, hXB), workspace=ws)  # warm allocator
+        bs.solve_selected(hA, hB, "siq", out=(hXA, hXB), workspace=ws, partitions=parts)  # warm allocator
         torch.cuda.synchronize()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record()
         for _ in range(args.steps):
-            bs.solve_selected(hA, hB, "siq", out=(hXA, hXB), workspace=ws)
+            bs.solve_selected(hA, hB, "siq", out=(hXA, hXB), workspace=ws, partitions=parts)
         e2.record()
         torch.cuda.synchronize()
         e2e_ms = s2.elapsed_time(e2) / args.steps
@@ -382,7 +399,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic (device splitmix64 generator, bench protocol seeds 0/1)",
             "config": {"workload": f"{args.workload}: BASELINE.json configs[{cfg_idx}]", "n_blocks": n, "block": b,
-                       "tip": a, "mode": "siq", "parallelism": f"partitions{world}" if world > 1 else "single",
+                       "tip": a, "mode": "siq",
+                       "parallelism": (f"partitions{world} (one per GPU)" if world > 1 else
+                                       f"1 GPU, {parts} concurrent in-GPU partitions (paper's scheme)" if parts > 1
+                                       else "1 GPU, sequential RGF"),
                        "l2": "inputs 32 GiB >> 126 MB L2 (no flush needed)" if args.workload == "cfg4" else "inputs > L2"},
             "fp64_tflops_step": achieved_step,
             "pct_fp64_peak_step": 100.0 * achieved_step / (peak * world),  # of the N-GPU aggregate peak
@@ -393,6 +413,7 @@ def main():
                          "share_of_step": prof.gemm_ms / ms if ms else None,
                          "inverse_ms_per_step": prof.inverse_ms, "gemm_launches_per_step": prof.gemm_launches},
             "phases_ms": phases,
+            "value_sequential_rgf_ms": seq_ms,
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,

@@ -29,9 +29,11 @@ from .matrix import BtaMatrix, SelectedSolution, generate_dd_bta, hermitianize, 
 from .partition import PartitionPlan, plan_partitions
 from .kernels import OpCounter, block_inverse, block_multiply_acc, mm
 from .device import DeviceBta, generate_dd_bta_device, hermitianize_device, kernel_launches, to_device, to_host
-from .rgf import RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, solve_selected
+from .rgf import (RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, default_partitions,
+                  release_caches, solve_selected)
 from .collectives import Collectives, LocalHub, TorchCollectives, TraceEvent
-from .dist import (BoundaryPayload, DistSolver, LocalFactors, ReducedSystem, assemble_reduced, dist_solve,
+from .dist import (BoundaryPayload, DistSolver, InGpuPartitions, LocalFactors, ReducedSystem, assemble_reduced,
+                   dist_solve,
                    local_backward, local_forward, solve_reduced)
 
 __version__ = "0.1.0"
@@ -40,7 +42,8 @@ __all__ = [
     "BtaMatrix", "SelectedSolution", "RgfFactors", "OpCounter", "PartitionPlan", "DeviceBta",
     "generate_dd_bta", "hermitianize", "to_dense", "mask_to_pattern", "to_device", "to_host",
     "block_multiply_acc", "mm", "block_inverse",
-    "bt_forward", "bt_backward", "bta_forward", "bta_backward", "solve_selected",
+    "bt_forward", "bt_backward", "bta_forward", "bta_backward", "solve_selected", "default_partitions",
+    "release_caches", "InGpuPartitions",
     "plan_partitions", "dist_solve", "local_forward", "assemble_reduced", "solve_reduced", "local_backward",
     "BoundaryPayload", "LocalFactors", "ReducedSystem", "DistSolver", "Collectives", "TorchCollectives",
     "LocalHub", "TraceEvent", "generate_dd_bta_device", "hermitianize_device", "kernel_launches",

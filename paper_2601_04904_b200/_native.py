@@ -181,9 +181,16 @@ def raise_for_status(code: int, st: Status) -> None:
 
 
 class Context:
-    """One bsel_context per device; calls run on torch's current stream."""
+    """A bsel_context per (device, lane); calls run on torch's current stream.
+
+    Lane 0 is the default.  Extra lanes (own streams, slot pools and
+    inverse workspaces inside the native context) let independent partitions
+    of the distributed scheme run concurrently on one GPU from separate
+    Python threads (ctypes releases the GIL during native calls).
+    """
 
     _per_device: dict = {}
+    _lock = threading.Lock()
 
     def __init__(self, device: int):
         self.lib = load_library()
@@ -194,18 +201,19 @@ class Context:
         self.handle = handle
 
     @classmethod
-    def get(cls, device: int | None = None) -> "Context":
+    def get(cls, device: int | None = None, lane: int = 0) -> "Context":
         import torch
 
         if not torch.cuda.is_available():
             raise NativeUnavailableError("no CUDA device: the B200 solver has no CPU fallback")
         if device is None:
             device = torch.cuda.current_device()
-        ctx = cls._per_device.get(device)
-        if ctx is None:
-            with torch.cuda.device(device):
-                ctx = cls(device)
-            cls._per_device[device] = ctx
+        with cls._lock:
+            ctx = cls._per_device.get((device, lane))
+            if ctx is None:
+                with torch.cuda.device(device):
+                    ctx = cls(device)
+                cls._per_device[(device, lane)] = ctx
         ctx.bind_stream()
         return ctx
 

@@ -31,7 +31,7 @@ from .partition import PartitionPlan, plan_partitions
 from .rgf import solve_selected
 
 __all__ = ["BoundaryPayload", "LocalFactors", "ReducedSystem", "local_forward", "assemble_reduced",
-           "solve_reduced", "local_backward", "dist_solve", "DistSolver", "record_partition"]
+           "solve_reduced", "local_backward", "dist_solve", "DistSolver", "InGpuPartitions", "record_partition"]
 
 _KIND_CODES = {"first": 0, "middle": 1, "last": 2}
 _KIND_NAMES = {v: k for k, v in _KIND_CODES.items()}
@@ -206,7 +206,8 @@ def _as_device(m, device=None):
     return to_device(m, device)
 
 
-def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | None = None, *, _factors=None):
+def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | None = None, *, _factors=None,
+                  _ctx=None):
     """Eliminate one partition's interior blocks on the GPU (dist.py:172-416).
 
     Returns ``(payload, tip_delta, factors)``; inputs are never mutated.
@@ -234,7 +235,7 @@ def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | Non
         fac = LocalFactors(kind=kind, lo=lo, hi=hi, mode="siq" if fused else "si", tensors=t,
                            work_a=_Strips(length, bs, asz, dev), work_b=_Strips(length, bs, asz, dev) if fused else None)
     WA, WB = fac.work_a, fac.work_b
-    ctx = _native.Context.get(dev.index)
+    ctx = _ctx or _native.Context.get(dev.index)
     ad, wad, fd = A.desc(), WA.desc(), fac.desc()
     bd = B.desc() if fused else None
     wbd = WB.desc() if fused else None
@@ -338,7 +339,7 @@ def solve_reduced(reduced: ReducedSystem, mode: str, counter=None, recursive_par
 
 
 def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, reduced: ReducedSystem,
-                   red_sol: SelectedSolution, counter=None, *, out=None):
+                   red_sol: SelectedSolution, counter=None, *, out=None, _ctx=None):
     """Back-substitute one partition seeded with the reduced solution
     (dist.py:542-744).  Writes this rank's pattern blocks (and, on rank 0,
     the tip) into ``out`` = (x_a, x_b) full-size DeviceBta (allocated zeroed
@@ -358,7 +359,7 @@ def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, 
     kind = plan.kinds[rank]
     k_top = reduced.index.get((rank, "top"), -1)
     k_bot = reduced.index.get((rank, "bottom"), -1)
-    ctx = _native.Context.get(A.device.index)
+    ctx = _ctx or _native.Context.get(A.device.index)
     ad, fd, wad = A.desc(), factors.desc(), factors.work_a.desc()
     xrd, xad = red_sol.x_a.desc(), XA.desc()
     bd = B.desc() if fused else None
@@ -376,6 +377,107 @@ def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, 
 # ---------------------------------------------------------------------------
 # Facade
 # ---------------------------------------------------------------------------
+
+
+class _Lanes:
+    """Run one callable per partition concurrently on one GPU: each partition
+    gets its own native context (lane) and CUDA stream and runs in its own
+    thread; the lanes start after, and the caller's stream waits for, all
+    work previously queued on the caller's stream."""
+
+    def __init__(self, device, count):
+        self.device = device
+        self.count = count
+        self.streams = [torch.cuda.Stream(device) for _ in range(count)]
+
+    def run(self, fn) -> list:
+        import threading
+
+        main = torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        errors = []
+
+        def work(rank):
+            try:
+                with torch.cuda.device(self.device), torch.cuda.stream(self.streams[rank]):
+                    self.streams[rank].wait_event(start)
+                    fn(rank, _native.Context.get(self.device.index, lane=rank))
+            except Exception as exc:  # noqa: BLE001 - rank attribution
+                errors.append((rank, exc))
+
+        threads = [threading.Thread(target=work, args=(r,)) for r in range(self.count)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for s in self.streams:
+            main.wait_stream(s)
+        return errors
+
+
+class InGpuPartitions:
+    """The paper's partitioned scheme with every partition on ONE GPU, the
+    partitions running concurrently (one lane = native context + stream +
+    thread each).  With 2 partitions (first + last, no middle-partition work
+    inflation) the two Schur chains run side by side, which fills the SMs the
+    latency-bound chain of a single sweep leaves idle.  Factor buffers are
+    kept between runs for repeated solves of one shape."""
+
+    def __init__(self, shape, mode, parts, device, plan=None):
+        self.n, self.b, self.a = shape
+        self.mode = mode
+        self.parts = parts
+        self.device = device
+        self.plan = plan or plan_partitions(self.n, parts, mode)
+        self.lanes = _Lanes(device, parts)
+        self._factors = [None] * parts
+        self.counters = []
+        self.reduced = None
+        self._tm = None
+
+    def run(self, A, B, out=None, hub=None, recursive_parts=None):
+        plan, parts, mode = self.plan, self.parts, self.mode
+        B = B if mode == "siq" else None
+        hub = hub or LocalHub(parts)
+        tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
+        self.counters = counters = [OpCounter(b=A.b, a=A.a) for _ in range(parts)]
+        results = [None] * parts
+        tm.start("forward")
+
+        def fwd(rank, ctx):
+            results[rank] = local_forward(A, B, plan, rank, counters[rank], _factors=self._factors[rank], _ctx=ctx)
+            self._factors[rank] = results[rank][2]
+
+        errors = self.lanes.run(fwd)
+        tm.stop("forward")
+        if errors:
+            primary = [e for e in errors if not isinstance(e[1], ProtocolError)]
+            rank, exc = min(primary or errors, key=lambda e: e[0])
+            raise WorkerError(rank, exc) from exc
+        tm.start("communication")
+        gathered = hub.all_gather_all([r[0] for r in results])
+        tip_sum = hub.all_reduce_all([r[1] for r in results]) if A.a > 0 else None
+        self.reduced = reduced = _assemble(gathered, A, B, plan, tip_sum)
+        tm.stop("communication")
+        tm.start("reduced")
+        red_sol = solve_reduced(reduced, mode, None, recursive_parts)
+        tm.stop("reduced")
+        tm.start("backward")
+        if out is None:
+            out = (DeviceBta.empty(A.n, A.b, A.a, self.device),
+                   DeviceBta.empty(A.n, A.b, A.a, self.device) if B is not None else None)
+        errors = self.lanes.run(lambda rank, ctx: local_backward(A, B, plan, rank, results[rank][2], reduced, red_sol,
+                                                                 counters[rank], out=out, _ctx=ctx))
+        if errors:
+            rank, exc = min(errors, key=lambda e: e[0])
+            raise WorkerError(rank, exc) from exc
+        tm.stop("backward")
+        self._tm = tm
+        return out
+
+    def phase_seconds(self):
+        return self._tm.seconds()
 
 
 class _PhaseTimer:
@@ -476,42 +578,16 @@ def dist_solve(a, b=None, num_parts=2, mode=None, transport=None, *, counter=Non
     dev = a.device if isinstance(a, DeviceBta) else torch.device("cuda", torch.cuda.current_device())
     A = _as_device(a, dev)
     B = _as_device(b, dev) if b is not None else None
-    tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
-    counters = [OpCounter(b=A.b, a=A.a) for _ in range(num_parts)]
-    results, errors = [], []
-    tm.start("forward")
-    for rank in range(num_parts):
-        try:
-            results.append(local_forward(A, B, plan, rank, counters[rank]))
-        except Exception as exc:  # noqa: BLE001 - rank attribution
-            errors.append((rank, exc))
-            results.append(None)
-    tm.stop("forward")
-    if errors:
-        primary = [e for e in errors if not isinstance(e[1], ProtocolError)]
-        rank, exc = min(primary or errors, key=lambda e: e[0])
-        raise WorkerError(rank, exc) from exc
-    tm.start("communication")
-    gathered = hub.all_gather_all([r[0] for r in results])
-    tip_sum = hub.all_reduce_all([r[1] for r in results]) if A.a > 0 else None
-    reduced = _assemble(gathered, A, B, plan, tip_sum)
-    tm.stop("communication")
-    tm.start("reduced")
-    red_sol = solve_reduced(reduced, mode, None, recursive_parts)
-    tm.stop("reduced")
-    tm.start("backward")
-    out = (DeviceBta.empty(A.n, A.b, A.a, dev), DeviceBta.empty(A.n, A.b, A.a, dev) if B is not None else None)
-    for rank in range(num_parts):
-        local_backward(A, B, plan, rank, results[rank][2], reduced, red_sol, counters[rank], out=out)
-    tm.stop("backward")
+    runner = InGpuPartitions(A.shape_params, mode, num_parts, dev, plan=plan)
+    out = runner.run(A, B, hub=hub, recursive_parts=recursive_parts)
     if timings is not None:
-        timings.update(tm.seconds())
+        timings.update(runner.phase_seconds())
     if counter is not None:
-        for c in counters:
+        for c in runner.counters:
             counter.merge(c)
-        counter.merge(_reduced_counts(reduced, mode))
+        counter.merge(_reduced_counts(runner.reduced, mode))
     if rank_counters is not None:
-        rank_counters.extend(counters)
+        rank_counters.extend(runner.counters)
     XA, XB = out
     if host:
         return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if XB is not None else None, mode=mode)

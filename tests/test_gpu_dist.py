@@ -160,3 +160,22 @@ def test_dist_device_inputs_stay_on_device():
     assert isinstance(got.x_a, bs.DeviceBta)
     seq = bs.solve_selected(A, B, "siq")
     assert max_block_rel_err(bs.to_host(got.x_b), bs.to_host(seq.x_b)) <= 1e-9
+
+
+@pytest.mark.parametrize("n,b,a,mode", [(64, 32, 16, "siq"), (70, 24, 0, "siq"), (66, 16, 8, "si"), (9, 8, 4, "siq")])
+def test_solve_selected_partitions_match_sequential(n, b, a, mode):
+    """solve_selected(partitions=2): the 2-partition scheme run concurrently
+    on one GPU agrees with the sequential sweeps (and the oracle)."""
+    A = bs.generate_dd_bta(n, b, a, seed=5)
+    B = bs.hermitianize(bs.generate_dd_bta(n, b, a, seed=6)) if mode == "siq" else None
+    seq = bs.solve_selected(A, B, mode, partitions=1)
+    par = bs.solve_selected(A, B, mode, partitions=2)
+    assert max_block_rel_err(par.x_a, seq.x_a) <= 1e-12
+    if mode == "siq":
+        assert max_block_rel_err(par.x_b, seq.x_b) <= 1e-12
+    cnt1, cnt2 = bs.OpCounter(b=b, a=a), bs.OpCounter(b=b, a=a)
+    t = {}
+    bs.solve_selected(A, B, mode, partitions=1, counter=cnt1)
+    d = bs.solve_selected(A, B, mode, partitions=2, counter=cnt2, timings=t, diagonal_only=True)
+    assert cnt1.as_dict() == cnt2.as_dict() and set(t) == {"forward", "backward"}
+    assert all(np.all(blk == 0) for blk in d.x_a.lower)
