@@ -470,18 +470,16 @@ namespace {
 // sooner while the aux stream's GEMM tiles hold SMs (measured on cfg4: 64
 // beats 148/96/32).  BSEL_INV_GRID overrides.
 int inverse_grid_cap() {
-  static int cap = -1;
-  if (cap < 0) {
+  static const int cap = [] {
     const char* e = getenv("BSEL_INV_GRID");
-    cap = e ? atoi(e) : 64;
-    if (cap <= 0 || cap > device_sm_count()) cap = device_sm_count();
-  }
+    int c = e ? atoi(e) : 64;
+    return (c <= 0 || c > device_sm_count()) ? device_sm_count() : c;
+  }();
   return cap;
 }
 
 int coop_grid_limit() {
-  static int limit = -1;
-  if (limit < 0) {
+  static const int limit = [] {
     int dev = 0, coop = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
@@ -490,8 +488,8 @@ int coop_grid_limit() {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persistent_inverse_kernel, 256,
                                                       sizeof(PinvSmem)) != cudaSuccess)
       per_sm = 0;
-    limit = coop ? per_sm * device_sm_count() : 0;
-  }
+    return coop ? per_sm * device_sm_count() : 0;
+  }();
   return limit;
 }
 }  // namespace
@@ -632,11 +630,9 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
   // Exact fallback (no-op unless a leaf met an exactly zero pivot).
   const size_t smem = (size_t)n * (2 * sizeof(double2) + 2 * sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    cudaFuncSetAttribute(exact_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set = smem;
-  }
+  static const cudaError_t smem_attr =  // thread-safe one-time init, sized for n <= 2048
+      cudaFuncSetAttribute(exact_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (smem_attr != cudaSuccess) return smem_attr;
   exact_inverse_kernel<<<1, 1024, smem, stream>>>(X, ldx, Y, ldy, n, work, flag, status, key);
   count_launch();
   return cudaGetLastError();

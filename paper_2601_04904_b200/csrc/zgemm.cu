@@ -16,7 +16,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
-#include <vector>
+#include <deque>
+#include <mutex>
 
 namespace bsel {
 
@@ -264,13 +265,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 
 template <class C>
 cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_grouped_kernel<C>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  // thread-safe one-time init (partitions may launch from several threads)
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(zgemm_grouped_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (attr != cudaSuccess) return attr;
   int tiles = 0;
   for (int i = 0; i < batch.nproblems; ++i) {
     GemmProblem& P = batch.p[i];
@@ -309,10 +307,14 @@ struct ProfRec {
   int kind;
   double flops;
 };
+// Partitions of one solve may run in concurrent host threads (dist.py
+// _Lanes): records are appended under a mutex (deque: stable references),
+// the suspend flag is per thread.
 bool g_prof_on = false;
-bool g_prof_suspended = false;
-std::vector<ProfRec> g_prof;
+thread_local bool g_prof_suspended = false;
+std::deque<ProfRec> g_prof;
 size_t g_prof_used = 0;
+std::mutex g_prof_mu;
 }  // namespace
 
 void profile_begin() {
@@ -323,6 +325,7 @@ bool profiling() { return g_prof_on && !g_prof_suspended; }
 void profile_suspend(bool on) { g_prof_suspended = on; }
 int profile_open(cudaStream_t s) {
   if (!g_prof_on || g_prof_suspended) return -1;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   if (g_prof_used == g_prof.size()) {
     ProfRec r{};
     cudaEventCreate(&r.t0);
@@ -335,6 +338,7 @@ int profile_open(cudaStream_t s) {
 }
 void profile_close(int id, cudaStream_t s, int kind, double flops) {
   if (id < 0) return;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   g_prof[id].kind = kind;
   g_prof[id].flops = flops;
   cudaEventRecord(g_prof[id].t1, s);
@@ -342,6 +346,7 @@ void profile_close(int id, cudaStream_t s, int kind, double flops) {
 ProfileTotals profile_end() {
   ProfileTotals t{};
   cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   for (size_t i = 0; i < g_prof_used; ++i) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, g_prof[i].t0, g_prof[i].t1);
@@ -362,13 +367,12 @@ void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxe
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int device_sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
+  static const int sms = [] {
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
   return sms;
 }
 
