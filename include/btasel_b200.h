@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BSEL_ABI_VERSION 1
+#define BSEL_ABI_VERSION 2
 
 typedef enum {
   BSEL_OK = 0,
@@ -140,13 +140,39 @@ typedef struct {
   double* b_fill_row; /* [len][b][b]  (middle, fused)                    */
   double* b_fill_col; /* [len][b][b]  (middle, fused)                    */
 } bsel_local_factors_t;
+/* Optional end-to-end mode (no reference counterpart; the reference moves
+ * whole matrices with cupy before/after its sweeps): the full-size matrices
+ * stay in (pinned) host memory and move in chunks of chunk_blocks partition
+ * blocks on the context's copy stream, overlapped with the sweeps.
+ * local_forward reads a/b (host inputs; copy_tip = this partition also
+ * moves the tips) -- the device a/b then only provide storage for the
+ * couplings and tip, their diag/arrow arrays are not read; local_backward
+ * writes x_a/x_b (host outputs; the tip when write_tip).  copy_stream
+ * (cudaStream_t, NULL = the context's own): partitions running
+ * concurrently on one GPU should share one input copy stream -- the chunks
+ * are queued a few chunks ahead of each sweep, so a shared stream
+ * interleaves them in progress order (separate streams are drained one
+ * after the other by the copy engine).  The calling stream waits for every
+ * copy.  NULL io = no host transfers.                                      */
+typedef struct {
+  const bsel_bta_t* a;   /* host inputs  (local_forward)  */
+  const bsel_bta_t* b;
+  const bsel_bta_t* x_a; /* host outputs (local_backward) */
+  const bsel_bta_t* x_b;
+  int64_t chunk_blocks;
+  int32_t copy_tip;
+  int32_t reserved;
+  void* copy_stream;
+} bsel_host_io_t;
+
 /* local_forward (dist.py:172-416): a, b = full original matrices (read
  * only); a_work/b_work = partition working arrays (n = hi-lo; diag, arrow
  * strips; tip receives the rank's tip contribution).  Afterwards the work
  * arrays hold the retained strips and the boundary payload.  Synchronizes;
  * singular pivot -> BSEL_ERR_SINGULAR with the global block index.        */
 int bsel_local_forward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b, const bsel_bta_t* a_work,
-                       const bsel_bta_t* b_work, const bsel_local_factors_t* f, bsel_status_t* st);
+                       const bsel_bta_t* b_work, const bsel_local_factors_t* f, const bsel_host_io_t* io,
+                       bsel_status_t* st);
 /* local_backward (dist.py:542-744): seeded from the reduced solution
  * (x_red, z_red; boundary indices k_top/k_bot), writes this partition's
  * pattern blocks of the full-size outputs x_a/x_b (and the tip if
@@ -154,7 +180,8 @@ int bsel_local_forward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_
 int bsel_local_backward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b,
                         const bsel_local_factors_t* f, const bsel_bta_t* a_work, const bsel_bta_t* b_work,
                         const bsel_bta_t* x_red, const bsel_bta_t* z_red, int64_t k_top, int64_t k_bot,
-                        int write_tip, const bsel_bta_t* x_a, const bsel_bta_t* x_b, bsel_status_t* st);
+                        int write_tip, const bsel_bta_t* x_a, const bsel_bta_t* x_b,
+                        const bsel_host_io_t* io, bsel_status_t* st);
 
 /* ---- synthetic inputs (matrix.py) --------------------------------------- */
 /* generate_dd_bta (matrix.py:224-284) written straight into device arrays:

@@ -85,6 +85,32 @@ class Factors(ctypes.Structure):
     ]
 
 
+class HostIo(ctypes.Structure):
+    """bsel_host_io_t: host matrices streamed behind the partition sweeps."""
+
+    _fields_ = [
+        ("a", ctypes.POINTER(Bta)),
+        ("b", ctypes.POINTER(Bta)),
+        ("x_a", ctypes.POINTER(Bta)),
+        ("x_b", ctypes.POINTER(Bta)),
+        ("chunk_blocks", ctypes.c_int64),
+        ("copy_tip", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("copy_stream", ctypes.c_void_p),
+    ]
+
+
+def host_desc(m) -> Bta:
+    """bsel_bta_t over a host BtaMatrix's stacked (C-contiguous) arrays."""
+    d = Bta()
+    d.n, d.b, d.a = m.n, m.b, m.a
+    for k, arr in m.stacked().items():
+        if arr.size and not arr.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"host {k} array must be C-contiguous")
+        setattr(d, k, arr.ctypes.data if arr.size else None)
+    return d
+
+
 class LocalFactors(ctypes.Structure):
     _fields_ = [
         ("lo", ctypes.c_int64),
@@ -149,8 +175,9 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         }
         lf = ctypes.POINTER(LocalFactors)
         pb = ctypes.POINTER(Bta)
-        sig["bsel_local_forward"] = ([vp, pb, pb, pb, pb, lf, st], i32)
-        sig["bsel_local_backward"] = ([vp, pb, pb, lf, pb, pb, pb, pb, i64, i64, i32, pb, pb, st], i32)
+        ts = ctypes.POINTER(HostIo)
+        sig["bsel_local_forward"] = ([vp, pb, pb, pb, pb, lf, ts, st], i32)
+        sig["bsel_local_backward"] = ([vp, pb, pb, lf, pb, pb, pb, pb, i64, i64, i32, pb, pb, ts, st], i32)
         sig["bsel_generate_dd_bta"] = ([vp, ctypes.POINTER(Bta), ctypes.c_uint64, ctypes.c_double, st], i32)
         sig["bsel_hermitianize"] = ([vp, ctypes.POINTER(Bta), st], i32)
         sig["bsel_kernel_launches"] = ([], ctypes.c_uint64)
@@ -160,7 +187,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res
-        if lib.bsel_abi_version() != 1:
+        if lib.bsel_abi_version() != 2:
             raise NativeUnavailableError("ABI version mismatch")
         if path is None:
             _lib = lib

@@ -431,8 +431,35 @@ static LocalFactorsDev to_dev(const bsel_local_factors_t& f, int64_t b, int64_t 
   return d;
 }
 
+// Host end-to-end descriptors (pointers are host memory; shapes must match).
+struct HostIoArgs {
+  BtaDev a, b, xa, xb;
+  HostIo io;
+};
+
+static const HostIo* to_io(const bsel_host_io_t* h, const bsel_bta_t* like, HostIoArgs& out) {
+  if (!h) return nullptr;
+  if (h->chunk_blocks <= 0) throw ArgError("chunk_blocks must be positive");
+  auto one = [&](const bsel_bta_t* m, BtaDev& d, const char* what) -> const BtaDev* {
+    if (!m) return nullptr;
+    check_same(like, m);
+    (void)what;
+    d = to_dev(*m);
+    return &d;
+  };
+  out.io.ha = one(h->a, out.a, "a");
+  out.io.hb = one(h->b, out.b, "b");
+  out.io.hxa = one(h->x_a, out.xa, "x_a");
+  out.io.hxb = one(h->x_b, out.xb, "x_b");
+  out.io.chunk = h->chunk_blocks;
+  out.io.copy_tip = h->copy_tip != 0;
+  out.io.copy_stream = static_cast<cudaStream_t>(h->copy_stream);
+  return &out.io;
+}
+
 int bsel_local_forward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b, const bsel_bta_t* a_work,
-                       const bsel_bta_t* b_work, const bsel_local_factors_t* f, bsel_status_t* st) {
+                       const bsel_bta_t* b_work, const bsel_local_factors_t* f, const bsel_host_io_t* io,
+                       bsel_status_t* st) {
   return guarded(st, [&] {
     if (!ctx || !f) throw ArgError("NULL argument");
     check_shape(a, "a");
@@ -446,7 +473,8 @@ int bsel_local_forward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_
       B = to_dev(*b);
       WB = to_dev(*b_work);
     }
-    local_forward(*ctx->impl, A, b ? &B : nullptr, WA, b ? &WB : nullptr, to_dev(*f, a->b, a->a));
+    HostIoArgs hio;
+    local_forward(*ctx->impl, A, b ? &B : nullptr, WA, b ? &WB : nullptr, to_dev(*f, a->b, a->a), to_io(io, a, hio));
     raise_if_singular(*ctx->impl, a->n);
   });
 }
@@ -454,7 +482,8 @@ int bsel_local_forward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_
 int bsel_local_backward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta_t* b,
                         const bsel_local_factors_t* f, const bsel_bta_t* a_work, const bsel_bta_t* b_work,
                         const bsel_bta_t* x_red, const bsel_bta_t* z_red, int64_t k_top, int64_t k_bot,
-                        int write_tip, const bsel_bta_t* x_a, const bsel_bta_t* x_b, bsel_status_t* st) {
+                        int write_tip, const bsel_bta_t* x_a, const bsel_bta_t* x_b,
+                        const bsel_host_io_t* io, bsel_status_t* st) {
   return guarded(st, [&] {
     if (!ctx || !f) throw ArgError("NULL argument");
     check_shape(a, "a");
@@ -463,6 +492,8 @@ int bsel_local_backward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
     const bool fused = f->fused != 0;
     if (fused && (!b || !b_work || !z_red || !x_b)) throw ShapeError("fused factors require the right-hand side");
     BtaDev A = to_dev(*a), WA = to_dev(*a_work), XR = to_dev(*x_red), XA = to_dev(*x_a), B, WB, ZR, XB;
+    HostIoArgs hio;
+    const HostIo* hp = to_io(io, a, hio);
     if (fused) {
       B = to_dev(*b);
       WB = to_dev(*b_work);
@@ -470,7 +501,7 @@ int bsel_local_backward(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
       XB = to_dev(*x_b);
     }
     local_backward(*ctx->impl, A, fused ? &B : nullptr, to_dev(*f, a->b, a->a), WA, fused ? &WB : nullptr, XR,
-                   fused ? &ZR : nullptr, k_top, k_bot, write_tip != 0, XA, fused ? &XB : nullptr);
+                   fused ? &ZR : nullptr, k_top, k_bot, write_tip != 0, XA, fused ? &XB : nullptr, hp);
     cuda_check(cudaGetLastError(), "local backward");
   });
 }

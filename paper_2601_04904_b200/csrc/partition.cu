@@ -3,6 +3,10 @@
 // hi-1, last: upward into lo, middle: downward with fill-in to lo) and the
 // seeded local back-substitution.  The collectives between the two phases
 // live in the host layer (NCCL through torch.distributed).
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "partition.cuh"
 #include "steps.cuh"
 
@@ -19,10 +23,66 @@ void copy_blocks(Context& ctx, double2* dst, const double2* src, int64_t elems) 
                "partition copy");
 }
 
+void copy_async(cudaStream_t s, double2* dst, const double2* src, int64_t elems) {
+  if (elems > 0)
+    cuda_check(cudaMemcpyAsync(dst, src, (size_t)elems * sizeof(double2), cudaMemcpyDefault, s), "host copy");
+}
+
+// Blocks [g0, g1) and couplings [e0, e1) of one transfer chunk.
+struct ChunkRange {
+  int64_t g0, g1, e0, e1;
+};
+
+// Forward chunk c: processing positions [c*C, (c+1)*C) and the couplings of
+// the same blocks (all the sweep touches up to position (c+1)*C - 1).
+ChunkRange in_chunk(PartKind kind, int64_t lo, int64_t hi, int64_t n, int64_t C, int64_t c) {
+  const int64_t len = hi - lo, p0 = c * C, p1 = std::min((c + 1) * C, len);
+  ChunkRange r;
+  if (kind == kLast) r.g0 = hi - p1, r.g1 = hi - p0;
+  else r.g0 = lo + p0, r.g1 = lo + p1;
+  r.e0 = r.g0, r.e1 = std::min(r.g1, n - 1);
+  return r;
+}
+
+// Backward chunk c of nc: the outputs final after backward steps
+// [c*C, (c+1)*C).  Backward position q: block hi-1-q (first / middle,
+// descending) or lo+q (last, ascending; its couplings lag one step).
+ChunkRange out_chunk(PartKind kind, int64_t lo, int64_t hi, int64_t n, int64_t C, int64_t c, int64_t nc) {
+  const int64_t len = hi - lo;
+  const bool last = c == nc - 1;
+  const int64_t q0 = c == 0 ? 0 : c * C + 1, q1 = last ? len - 1 : std::min((c + 1) * C, len - 1);
+  ChunkRange r;
+  if (kind == kLast) {
+    r.g0 = lo + q0, r.g1 = lo + q1 + 1;
+    r.e0 = lo + c * C, r.e1 = lo + (last ? len - 1 : (c + 1) * C);
+  } else {
+    r.g0 = hi - 1 - q1, r.g1 = hi - q0;
+    r.e0 = r.g0, r.e1 = r.g1;
+  }
+  r.e1 = std::min(r.e1, n - 1);
+  return r;
+}
+
+// Copy the diag / arrow strips (dst indexed from block strip_lo: work arrays
+// start at the partition) and / or the couplings of one chunk.
+void copy_chunk(cudaStream_t s, const BtaDev& dst, const BtaDev& src, const ChunkRange& r, int64_t strip_lo,
+                bool strips, bool couplings) {
+  const int64_t b = src.b, a = src.a, nb = r.g1 - r.g0, d0 = r.g0 - strip_lo, s0 = r.g0;
+  if (strips) {
+    copy_async(s, dst.diag + d0 * b * b, src.diag + s0 * b * b, nb * b * b);
+    copy_async(s, dst.arrow_row + d0 * a * b, src.arrow_row + s0 * a * b, nb * a * b);
+    copy_async(s, dst.arrow_col + d0 * b * a, src.arrow_col + s0 * b * a, nb * b * a);
+  }
+  if (couplings && r.e1 > r.e0) {
+    copy_async(s, dst.lower + r.e0 * b * b, src.lower + r.e0 * b * b, (r.e1 - r.e0) * b * b);
+    copy_async(s, dst.upper + r.e0 * b * b, src.upper + r.e0 * b * b, (r.e1 - r.e0) * b * b);
+  }
+}
+
 }  // namespace
 
 void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev& WA, const BtaDev* WB,
-                   const LocalFactorsDev& F) {
+                   const LocalFactorsDev& F, const HostIo* io) {
   const int64_t lo = F.lo, hi = F.hi, len = hi - lo, b = A.b, a = A.a;
   const bool fused = B != nullptr;
   if (len < 2 || lo < 0 || hi > A.n) throw ShapeError("invalid partition range");
@@ -37,14 +97,71 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
     copy_blocks(ctx, w.arrow_col, src.arrow_col + lo * b * a, len * b * a);
     if (a > 0) cuda_check(cudaMemsetAsync(w.tip, 0, (size_t)(a * a) * sizeof(double2), ctx.stream()), "tip");
   };
-  stage(A, WA);
-  if (fused) stage(*B, *WB);
+  // End-to-end mode: input chunks are queued on the copy stream a few
+  // chunks ahead of the sweep's launches (so partitions sharing one copy
+  // stream interleave their chunks in progress order instead of one
+  // partition's whole input arriving first); the chain waits for chunk c
+  // before the first step that touches it.
+  const bool streamed = io && io->ha && io->chunk > 0;
+  if (streamed && (fused != (io->hb != nullptr))) throw ShapeError("host right-hand side disagrees with factors");
+  const int64_t C = streamed ? io->chunk : 1, n_in = streamed ? (len + C - 1) / C : 0;
+  constexpr int64_t kLookahead = 3;  // chunks queued ahead of the sweep
+  cudaStream_t xs = streamed ? (io->copy_stream ? io->copy_stream : ctx.xfer()) : nullptr;
+  // BSEL_XFER_TRACE=1: print chunk arrival vs. chain progress (debug only).
+  static const bool trace = getenv("BSEL_XFER_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tin, tstep;
+  auto tev = [](std::vector<cudaEvent_t>& v, cudaStream_t st) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "trace event");
+    cuda_check(cudaEventRecord(e, st), "trace event");
+    v.push_back(e);
+  };
+  if (trace) tev(tstep, ctx.stream());
+  int64_t issued = 0;
+  auto issue = [&](int64_t upto) {  // queue input chunks [issued, upto]
+    for (; streamed && issued <= std::min(upto, n_in - 1); ++issued) {
+      const int64_t c = issued;
+      const ChunkRange r = in_chunk((PartKind)F.kind, lo, hi, A.n, C, c);
+      copy_chunk(xs, WA, *io->ha, r, lo, true, false);
+      copy_chunk(xs, A, *io->ha, r, 0, false, true);
+      if (fused) {
+        copy_chunk(xs, *WB, *io->hb, r, lo, true, false);
+        copy_chunk(xs, *B, *io->hb, r, 0, false, true);
+      }
+      if (c == 0 && io->copy_tip && a > 0) {
+        copy_async(xs, A.tip, io->ha->tip, a * a);
+        if (fused) copy_async(xs, B->tip, io->hb->tip, a * a);
+      }
+      cuda_check(cudaEventRecord(ctx.xfer_event((int)c), xs), "chunk record");
+      if (trace) tev(tin, xs);
+    }
+  };
+  int waited = -1;  // last input chunk the chain stream waited for
+  auto need = [&](cudaStream_t s, int64_t pos) {
+    if (!streamed) return;
+    const int c = (int)std::min<int64_t>(pos / C, n_in - 1);
+    issue(c + kLookahead);
+    for (int k = waited + 1; k <= c; ++k) cuda_check(cudaStreamWaitEvent(s, ctx.xfer_event(k), 0), "chunk wait");
+    waited = std::max(waited, c);
+  };
+  if (streamed) {
+    cuda_check(cudaEventRecord(ctx.event(7), ctx.stream()), "xfer fork");
+    cuda_check(cudaStreamWaitEvent(xs, ctx.event(7), 0), "xfer fork");  // buffers free
+    issue(kLookahead);
+    for (auto* w : {&WA, WB})
+      if (w && a > 0) cuda_check(cudaMemsetAsync(w->tip, 0, (size_t)(a * a) * sizeof(double2), ctx.stream()), "tip");
+  } else {
+    stage(A, WA);
+    if (fused) stage(*B, *WB);
+  }
   cuda_check(cudaEventRecord(ctx.timer(0), ctx.stream()), "timer");
   auto d = [&](const BtaDev& w, int64_t i) { return w.D(i - lo); };
   auto ar = [&](const BtaDev& w, int64_t i) { return w.AR(i - lo); };
   auto ac = [&](const BtaDev& w, int64_t i) { return w.AC(i - lo); };
 
   if (F.kind == kMiddle) {
+    need(ctx.stream(), 1);
+    waited = -1;  // the chain stream still has to wait for itself
     Level L(ctx.stream());
     L.out(F.FR(1)).add(+1, A.U(lo));
     L.out(F.FC(1)).add(+1, A.L(lo));
@@ -62,6 +179,7 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
       const int64_t j = down ? i + 1 : i - 1;
       const int64_t e = down ? i : i - 1;  // index of the coupling pair
       ring_wait(ctx, (int)s);
+      need(ctx.chain(), s + 1);
       EndStep st;
       st.Lk = down ? A.L(e) : A.U(e);
       st.Uk = down ? A.U(e) : A.L(e);
@@ -76,11 +194,13 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.sb = F.SB(i - lo);
       }
       end_step(ctx, st, fused, (uint64_t)s, i, (int)(s & 1));
+      if (trace && (s + 1) % C == 0) tev(tstep, ctx.chain());
     }
   } else {
     for (int64_t i = lo + 1; i < hi - 1; ++i) {
       const int64_t s = i - lo - 1;
       ring_wait(ctx, (int)s);
+      need(ctx.chain(), i + 1 - lo);
       MiddleStep st;
       st.L = A.L(i), st.U = A.U(i);
       st.ad_i = d(WA, i), st.ad_n = d(WA, i + 1), st.ad_lo = d(WA, lo);
@@ -102,12 +222,29 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
     }
   }
   streams_join(ctx);
+  if (streamed) {
+    issue(n_in - 1);
+    cuda_check(cudaStreamWaitEvent(ctx.stream(), ctx.xfer_event((int)n_in - 1), 0), "copies done");
+  }
+  if (trace) {
+    tev(tstep, ctx.stream());
+    cuda_check(cudaStreamSynchronize(ctx.stream()), "trace sync");
+    fprintf(stderr, "[xfer] part lo=%lld kind=%d: chunk arrival / chain step-block done (ms)\n", (long long)lo, F.kind);
+    for (size_t k = 1; k < std::max(tin.size() + 1, tstep.size()); ++k) {
+      float a_ms = -1, s_ms = -1;
+      if (k - 1 < tin.size()) cudaEventElapsedTime(&a_ms, tstep[0], tin[k - 1]);
+      if (k < tstep.size()) cudaEventElapsedTime(&s_ms, tstep[0], tstep[k]);
+      fprintf(stderr, "[xfer] %zu %.2f %.2f\n", k - 1, a_ms, s_ms);
+    }
+    for (auto e : tin) cudaEventDestroy(e);
+    for (auto e : tstep) cudaEventDestroy(e);
+  }
   cuda_check(cudaEventRecord(ctx.timer(1), ctx.stream()), "timer");
 }
 
 void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalFactorsDev& F, const BtaDev& WA,
                     const BtaDev* WB, const BtaDev& XR, const BtaDev* ZR, int64_t k_top, int64_t k_bot,
-                    bool write_tip, const BtaDev& XA, const BtaDev* XB) {
+                    bool write_tip, const BtaDev& XA, const BtaDev* XB, const HostIo* io) {
   const int64_t lo = F.lo, hi = F.hi, len = hi - lo, b = A.b, a = A.a;
   const bool fused = F.fused;
   if (fused && (!B || !WB || !ZR || !XB)) throw ShapeError("fused factors require the right-hand side");
@@ -115,6 +252,33 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
   ctx.reserve_slots(64, (int64_t)mx * mx);
   cudaStream_t s = ctx.stream();
   cuda_check(cudaEventRecord(ctx.timer(2), s), "timer");
+  // End-to-end mode: move each chunk of finished outputs to the host on the
+  // copy stream while the sweep continues.
+  const bool streamed = io && io->hxa && io->chunk > 0;
+  if (streamed && fused && !io->hxb) throw ShapeError("host output for the quadratic solution missing");
+  const int64_t C = streamed ? io->chunk : 1, n_out = std::max<int64_t>(1, (len - 1 + C - 1) / C);
+  int64_t sent = 0;  // chunks queued
+  auto send = [&](int64_t steps, bool final) {  // backward steps [0, steps) are complete
+    if (!streamed) return;
+    while (sent < n_out && (final || (sent + 1) * C <= steps) && (final || sent < n_out - 1)) {
+      cudaEvent_t ev = ctx.xfer_event((int)sent);
+      cuda_check(cudaEventRecord(ev, s), "chunk record");
+      cudaStream_t xs = ctx.xfer();
+      cuda_check(cudaStreamWaitEvent(xs, ev, 0), "chunk wait");
+      const ChunkRange r = out_chunk((PartKind)F.kind, lo, hi, A.n, C, sent, n_out);
+      copy_chunk(xs, *io->hxa, XA, r, 0, true, true);
+      if (fused) copy_chunk(xs, *io->hxb, *XB, r, 0, true, true);
+      if (sent == 0 && write_tip && a > 0) {
+        copy_async(xs, io->hxa->tip, XA.tip, a * a);
+        if (fused) copy_async(xs, io->hxb->tip, XB->tip, a * a);
+      }
+      ++sent;
+    }
+    if (final) {
+      cuda_check(cudaEventRecord(ctx.event(7), ctx.xfer()), "copies done");
+      cuda_check(cudaStreamWaitEvent(s, ctx.event(7), 0), "copies done");
+    }
+  };
   const Mat ytt = XR.T();
   const Mat ztt = fused ? ZR->T() : Mat{};
   Level L(s);
@@ -178,6 +342,10 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       pipe.early(L, st, (int)(t & 1));
       L.flush();
       pipe.rest(L, st, (int)(t & 1));
+      if (streamed && (t + 1) % C == 0) {
+        L.flush();
+        send(t + 1, false);
+      }
     }
   } else {
     seed(k_top, lo);
@@ -232,11 +400,17 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       pipe.early(L, st, q);
       L.flush();
       pipe.rest(L, st, q);
+      const int64_t t = hi - 2 - i;
+      if (streamed && (t + 1) % C == 0) {
+        L.flush();
+        send(t + 1, false);
+      }
       yfr = st.col[0], yfc = st.row[0];
       if (fused) zfr = st.zcol[0], zfc = st.zrow[0];
     }
   }
   L.flush();
+  send(len - 1, true);
   cuda_check(cudaEventRecord(ctx.timer(3), s), "timer");
 }
 

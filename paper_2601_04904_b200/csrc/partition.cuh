@@ -28,18 +28,38 @@ struct LocalFactorsDev {
   Mat BFC(int64_t k) const { return blk(b_fill_col, k, (int)b, (int)b); }
 };
 
+// Optional end-to-end mode: the full-size matrices live in (pinned) host
+// memory and move chunk by chunk on the context's copy stream, overlapped
+// with the sweeps.  A chunk = `chunk` consecutive partition blocks in
+// processing order (first/middle partitions ascending from lo, last
+// partition descending from hi-1).  local_forward: chunk c's diag / arrow
+// strips go straight into the work arrays and its couplings into A/B (device
+// storage; their diag/arrow arrays are not read), each sweep step waits for
+// its chunk.  local_backward: after backward steps [c*chunk, (c+1)*chunk)
+// (chunk 0 also the seeds, the last chunk everything) the finished output
+// blocks are copied to hx_a/hx_b.  The calling stream waits for every copy.
+struct HostIo {
+  const BtaDev* ha = nullptr;   // host inputs (forward)
+  const BtaDev* hb = nullptr;
+  const BtaDev* hxa = nullptr;  // host outputs (backward)
+  const BtaDev* hxb = nullptr;
+  int64_t chunk = 0;
+  bool copy_tip = false;                // forward: this partition moves the input tips
+  cudaStream_t copy_stream = nullptr;   // shared copy stream (nullptr: the context's own)
+};
+
 // dist.py:172-416.  A, B: full original matrices (read only).  WA/WB: the
 // partition's working copies (n = hi - lo blocks; diag / arrow strips; tip
 // receives this rank's tip contribution).  After the call WA/WB hold the
 // eliminated strips and the updated boundary blocks (the payload).
 void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev& WA, const BtaDev* WB,
-                   const LocalFactorsDev& F);
+                   const LocalFactorsDev& F, const HostIo* io = nullptr);
 
 // dist.py:542-744.  XR/ZR: reduced solution; k_top/k_bot: reduced indices of
 // this partition's boundaries; XA/XB: full-size outputs (only this rank's
 // pattern blocks are written; rank 0 also writes the tip).
 void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalFactorsDev& F, const BtaDev& WA,
                     const BtaDev* WB, const BtaDev& XR, const BtaDev* ZR, int64_t k_top, int64_t k_bot,
-                    bool write_tip, const BtaDev& XA, const BtaDev* XB);
+                    bool write_tip, const BtaDev& XA, const BtaDev* XB, const HostIo* io = nullptr);
 
 }  // namespace bsel

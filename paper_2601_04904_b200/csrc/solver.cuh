@@ -81,6 +81,10 @@ class Context {
   void invert(Mat X, Mat Y, uint64_t order, int64_t index, cudaStream_t s);
   SingularInfo read_status();  // synchronizes the user stream
 
+  // Copy stream for host<->device transfers overlapped with the sweeps and
+  // a pool of ordering events for them (created on first use).
+  cudaStream_t xfer();
+  cudaEvent_t xfer_event(int i);
   // Events for cross-stream ordering.
   cudaEvent_t event(int i);
   cudaEvent_t timer(int i);
@@ -100,6 +104,8 @@ class Context {
   int* d_flag_ = nullptr;
   unsigned long long* d_status_ = nullptr;
   std::vector<cudaEvent_t> events_;
+  std::vector<cudaEvent_t> xfer_events_;
+  cudaStream_t xfer_ = nullptr;
   cudaEvent_t timers_[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 

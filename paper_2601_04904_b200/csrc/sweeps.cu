@@ -44,8 +44,24 @@ Context::~Context() {
   if (d_status_) cudaFree(d_status_);
   for (auto& e : events_) cudaEventDestroy(e);
   for (auto& t : timers_) cudaEventDestroy(t);
+  for (auto& e : xfer_events_) cudaEventDestroy(e);
+  if (xfer_) cudaStreamDestroy(xfer_);
   if (aux_) cudaStreamDestroy(aux_);
   if (chain_) cudaStreamDestroy(chain_);
+}
+
+cudaStream_t Context::xfer() {
+  if (!xfer_) cuda_check(cudaStreamCreateWithFlags(&xfer_, cudaStreamNonBlocking), "copy stream");
+  return xfer_;
+}
+
+cudaEvent_t Context::xfer_event(int i) {
+  while ((int)xfer_events_.size() <= i) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    xfer_events_.push_back(e);
+  }
+  return xfer_events_[i];
 }
 
 void Context::reserve_slots(int nslots, int64_t slot_elems) {

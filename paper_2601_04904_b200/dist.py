@@ -17,6 +17,7 @@ the in-process ``LocalHub`` (all partitions on one GPU, the default).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -206,8 +207,24 @@ def _as_device(m, device=None):
     return to_device(m, device)
 
 
+def _alloc_factors(kind, lo, hi, fused, bs, asz, dev) -> "LocalFactors":
+    length = hi - lo
+    c128 = dict(dtype=torch.complex128, device=dev)
+    t = {"s_a": torch.empty((length, bs, bs), **c128)}
+    if fused:
+        t["s_b"] = torch.empty((length, bs, bs), **c128)
+    if kind == "middle":
+        t["fill_row"] = torch.empty((length, bs, bs), **c128)
+        t["fill_col"] = torch.empty((length, bs, bs), **c128)
+        if fused:
+            t["b_fill_row"] = torch.empty((length, bs, bs), **c128)
+            t["b_fill_col"] = torch.empty((length, bs, bs), **c128)
+    return LocalFactors(kind=kind, lo=lo, hi=hi, mode="siq" if fused else "si", tensors=t,
+                        work_a=_Strips(length, bs, asz, dev), work_b=_Strips(length, bs, asz, dev) if fused else None)
+
+
 def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | None = None, *, _factors=None,
-                  _ctx=None):
+                  _ctx=None, _sync=None):
     """Eliminate one partition's interior blocks on the GPU (dist.py:172-416).
 
     Returns ``(payload, tip_delta, factors)``; inputs are never mutated.
@@ -220,20 +237,7 @@ def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | Non
     n, bs, asz = A.shape_params
     length = hi - lo
     dev = A.device
-    fac = _factors
-    if fac is None:
-        c128 = dict(dtype=torch.complex128, device=dev)
-        t = {"s_a": torch.empty((length, bs, bs), **c128)}
-        if fused:
-            t["s_b"] = torch.empty((length, bs, bs), **c128)
-        if kind == "middle":
-            t["fill_row"] = torch.empty((length, bs, bs), **c128)
-            t["fill_col"] = torch.empty((length, bs, bs), **c128)
-            if fused:
-                t["b_fill_row"] = torch.empty((length, bs, bs), **c128)
-                t["b_fill_col"] = torch.empty((length, bs, bs), **c128)
-        fac = LocalFactors(kind=kind, lo=lo, hi=hi, mode="siq" if fused else "si", tensors=t,
-                           work_a=_Strips(length, bs, asz, dev), work_b=_Strips(length, bs, asz, dev) if fused else None)
+    fac = _factors or _alloc_factors(kind, lo, hi, fused, bs, asz, dev)
     WA, WB = fac.work_a, fac.work_b
     ctx = _ctx or _native.Context.get(dev.index)
     ad, wad, fd = A.desc(), WA.desc(), fac.desc()
@@ -241,7 +245,7 @@ def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | Non
     wbd = WB.desc() if fused else None
     ctx.bind_stream()
     ctx.call("bsel_local_forward", ctypes.byref(ad), ctypes.byref(bd) if fused else None, ctypes.byref(wad),
-             ctypes.byref(wbd) if fused else None, ctypes.byref(fd))
+             ctypes.byref(wbd) if fused else None, ctypes.byref(fd), ctypes.byref(_sync) if _sync else None)
     record_partition(counter, kind, length, bs, asz, fac.mode, "forward")
     bnd = {"first": [hi - 1], "last": [lo], "middle": [lo, hi - 1]}[kind]
     pay = BoundaryPayload(rank=rank, kind=kind, b=bs, a=asz, fused=fused)
@@ -339,7 +343,7 @@ def solve_reduced(reduced: ReducedSystem, mode: str, counter=None, recursive_par
 
 
 def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, reduced: ReducedSystem,
-                   red_sol: SelectedSolution, counter=None, *, out=None, _ctx=None):
+                   red_sol: SelectedSolution, counter=None, *, out=None, _ctx=None, _sync=None):
     """Back-substitute one partition seeded with the reduced solution
     (dist.py:542-744).  Writes this rank's pattern blocks (and, on rank 0,
     the tip) into ``out`` = (x_a, x_b) full-size DeviceBta (allocated zeroed
@@ -369,7 +373,7 @@ def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, 
     ref = lambda x: ctypes.byref(x) if x is not None else None  # noqa: E731
     ctx.bind_stream()
     ctx.call("bsel_local_backward", ref(ad), ref(bd), ref(fd), ref(wad), ref(wbd), ref(xrd), ref(zrd),
-             k_top, k_bot, int(rank == 0), ref(xad), ref(xbd))
+             k_top, k_bot, int(rank == 0), ref(xad), ref(xbd), ref(_sync))
     record_partition(counter, kind, hi - lo, bs, asz, factors.mode, "backward")
     return out
 
@@ -416,6 +420,23 @@ class _Lanes:
         return errors
 
 
+def _host_io(chunk, a=None, b=None, x_a=None, x_b=None, copy_tip=False, stream=None):
+    """bsel_host_io_t for local_forward / local_backward end-to-end mode
+    (the descriptors are kept alive on the returned struct)."""
+    io = _native.HostIo()
+    keep = []
+    for k, m in (("a", a), ("b", b), ("x_a", x_a), ("x_b", x_b)):
+        if m is not None:
+            d = _native.host_desc(m)
+            keep.append(d)
+            setattr(io, k, ctypes.pointer(d))
+    io.chunk_blocks = int(chunk)
+    io.copy_tip = int(bool(copy_tip))
+    io.copy_stream = stream.cuda_stream if stream is not None else None
+    io._keep = keep
+    return io
+
+
 class InGpuPartitions:
     """The paper's partitioned scheme with every partition on ONE GPU, the
     partitions running concurrently (one lane = native context + stream +
@@ -432,13 +453,24 @@ class InGpuPartitions:
         self.plan = plan or plan_partitions(self.n, parts, mode)
         self.lanes = _Lanes(device, parts)
         self._factors = [None] * parts
+        self.chunk = None
+        self.copy_stream = torch.cuda.Stream(device)  # shared by the partitions' input chunks
         self.counters = []
         self.reduced = None
         self._tm = None
 
-    def run(self, A, B, out=None, hub=None, recursive_parts=None):
+    def run(self, A, B, out=None, hub=None, recursive_parts=None, host_in=None, host_out=None):
+        """One solve.  ``host_in`` = (a, b) host BtaMatrix (pinned for full
+        overlap): the inputs are streamed in chunk by chunk behind the
+        forward sweeps instead of being resident in A/B beforehand (A/B then
+        only provide device storage for the couplings and the tip);
+        ``host_out`` = (x_a, x_b) host BtaMatrix receiving the solution,
+        streamed out behind the backward sweeps."""
         plan, parts, mode = self.plan, self.parts, self.mode
         B = B if mode == "siq" else None
+        # Chunk of the host transfers (blocks): small enough that the first
+        # chunk arrives fast, large enough to amortise the copy calls.
+        chunk = self.chunk or int(os.environ.get("BSEL_STREAM_CHUNK", "8"))
         hub = hub or LocalHub(parts)
         tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
         self.counters = counters = [OpCounter(b=A.b, a=A.a) for _ in range(parts)]
@@ -446,7 +478,12 @@ class InGpuPartitions:
         tm.start("forward")
 
         def fwd(rank, ctx):
-            results[rank] = local_forward(A, B, plan, rank, counters[rank], _factors=self._factors[rank], _ctx=ctx)
+            sync = None
+            if host_in is not None:
+                sync = _host_io(chunk, a=host_in[0], b=host_in[1] if B is not None else None, copy_tip=rank == 0,
+                                stream=self.copy_stream)
+            results[rank] = local_forward(A, B, plan, rank, counters[rank], _factors=self._factors[rank], _ctx=ctx,
+                                          _sync=sync)
             self._factors[rank] = results[rank][2]
 
         errors = self.lanes.run(fwd)
@@ -467,8 +504,11 @@ class InGpuPartitions:
         if out is None:
             out = (DeviceBta.empty(A.n, A.b, A.a, self.device),
                    DeviceBta.empty(A.n, A.b, A.a, self.device) if B is not None else None)
-        errors = self.lanes.run(lambda rank, ctx: local_backward(A, B, plan, rank, results[rank][2], reduced, red_sol,
-                                                                 counters[rank], out=out, _ctx=ctx))
+        io_out = None
+        if host_out is not None:
+            io_out = _host_io(chunk, x_a=host_out[0], x_b=host_out[1] if B is not None else None)
+        errors = self.lanes.run(lambda rank, ctx: local_backward(
+            A, B, plan, rank, results[rank][2], reduced, red_sol, counters[rank], out=out, _ctx=ctx, _sync=io_out))
         if errors:
             rank, exc = min(errors, key=lambda e: e[0])
             raise WorkerError(rank, exc) from exc

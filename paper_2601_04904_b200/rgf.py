@@ -240,6 +240,11 @@ def bta_backward(factors, a, b=None, counter=None, *, diagonal_only=False) -> Se
 _PARTITIONED = {}
 
 
+def _pinned(m) -> bool:
+    """True when every array of host BtaMatrix ``m`` is page-locked."""
+    return all(torch.from_numpy(x).is_pinned() for x in m.stacked().values() if x.size)
+
+
 def default_partitions(n: int) -> int:
     """Partitions used by ``solve_selected(partitions=None)``: the 2-partition
     scheme run concurrently on one GPU once the chain is long enough to
@@ -334,16 +339,39 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out):
     fused = b is not None
     _, device = _ctx_for(a)
     host = not isinstance(a, DeviceBta)
-    A = DeviceBta.empty(n, bs, asz, device, zero=False).copy_from_host(a) if host else a
+    # Pinned host inputs are streamed in behind the forward sweeps and pinned
+    # host outputs out behind the backward sweeps (bsel_host_io_t); pageable
+    # memory would make every chunk copy synchronous, so it is moved whole.
+    stream_in = host and _pinned(a) and (b is None or _pinned(b))
+    host_out = out if (out is not None and not isinstance(out[0], DeviceBta)) else None
+    stream_out = host_out is not None and not diagonal_only and all(_pinned(x) for x in host_out if x is not None)
+    A = a if not host else DeviceBta.empty(n, bs, asz, device, zero=False)
+    if host and not stream_in:
+        A.copy_from_host(a)
     B = None
     if fused:
-        B = DeviceBta.empty(n, bs, asz, device, zero=False).copy_from_host(b) if host else b
+        B = b if not host else DeviceBta.empty(n, bs, asz, device, zero=False)
+        if host and not stream_in:
+            B.copy_from_host(b)
     key = (device.index, n, bs, asz, mode, parts)
     runner = _PARTITIONED.get(key)
     if runner is None:
         runner = _PARTITIONED[key] = InGpuPartitions((n, bs, asz), mode, parts, device)
     dev_out = out if (out is not None and isinstance(out[0], DeviceBta)) else None
-    XA, XB = runner.run(A, B, out=dev_out)
+    if stream_in or stream_out:
+        XA, XB = runner.run(A, B, out=dev_out, host_in=(a, b) if stream_in else None,
+                            host_out=host_out if stream_out else None)
+    else:
+        XA, XB = runner.run(A, B, out=dev_out)
+    if stream_out:
+        record_sweep(counter, n, bs, asz, mode, "forward")
+        record_sweep(counter, n, bs, asz, mode, "backward")
+        if timings is not None:
+            ph = runner.phase_seconds()
+            timings["forward"] = ph["forward"] + ph["communication"] + ph["reduced"]
+            timings["backward"] = ph["backward"]
+        torch.cuda.current_stream(device).synchronize()
+        return SelectedSolution(x_a=host_out[0], x_b=host_out[1] if fused else None, mode=mode)
     if diagonal_only:
         for X in (XA, XB) if fused else (XA,):
             X.lower.zero_()
