@@ -84,6 +84,10 @@ int bsel_context_create(int device, bsel_context_t** out, bsel_status_t* st);
 int bsel_context_destroy(bsel_context_t* ctx);
 /* Run subsequent calls on `cuda_stream` (cudaStream_t; NULL = legacy default). */
 int bsel_context_set_stream(bsel_context_t* ctx, void* cuda_stream);
+/* CTAs of the persistent block inverse on this context (0 = default: 64 or
+ * BSEL_INV_GRID).  Contexts sweeping concurrently on one GPU (in-GPU
+ * partitions) use fewer so the chains leave SMs to each other's GEMMs.    */
+int bsel_context_set_inverse_grid(bsel_context_t* ctx, int ctas);
 /* Synchronizes; reports deferred device errors (singular pivots). */
 int bsel_synchronize(bsel_context_t* ctx, bsel_status_t* st);
 /* Device time of the last forward / backward sweep in ms (synchronizes). */
@@ -202,6 +206,8 @@ typedef struct {
   double gemm_ms;        /* sum of their CUDA-event durations              */
   int64_t inverse_calls; /* block inverses                                  */
   double inverse_ms;     /* sum of their CUDA-event durations              */
+  double gemm_bytes;     /* compulsory bytes of the GEMM launches: every  */
+                         /* operand read once, outputs written once       */
 } bsel_profile_t;
 /* Bracket every launch with CUDA events on its stream until _end (which
  * synchronizes the device and returns the totals).                        */

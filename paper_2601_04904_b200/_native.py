@@ -25,6 +25,7 @@ EXPORTS = (
     "bsel_context_create",
     "bsel_context_destroy",
     "bsel_context_set_stream",
+    "bsel_context_set_inverse_grid",
     "bsel_synchronize",
     "bsel_last_timings",
     "bsel_block_multiply_acc",
@@ -133,6 +134,7 @@ class Profile(ctypes.Structure):
         ("gemm_ms", ctypes.c_double),
         ("inverse_calls", ctypes.c_int64),
         ("inverse_ms", ctypes.c_double),
+        ("gemm_bytes", ctypes.c_double),
     ]
 
 
@@ -160,6 +162,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             "bsel_context_create": ([i32, ctypes.POINTER(vp), st], i32),
             "bsel_context_destroy": ([vp], i32),
             "bsel_context_set_stream": ([vp, vp], i32),
+            "bsel_context_set_inverse_grid": ([vp, i32], i32),
             "bsel_synchronize": ([vp, st], i32),
             "bsel_last_timings": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], i32),
             "bsel_block_multiply_acc": (
@@ -249,6 +252,11 @@ class Context:
 
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.lib.bsel_context_set_stream(self.handle, ctypes.c_void_p(s.cuda_stream))
+
+    def set_inverse_grid(self, ctas: int) -> None:
+        """CTAs of the persistent block inverse on this context (0 = default)."""
+        if self.lib.bsel_context_set_inverse_grid(self.handle, int(ctas)) != 0:
+            raise ValueError(f"invalid inverse grid {ctas}")
 
     def call(self, name: str, *args) -> None:
         st = Status()

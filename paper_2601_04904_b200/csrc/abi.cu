@@ -204,6 +204,12 @@ int bsel_context_set_stream(bsel_context_t* ctx, void* cuda_stream) {
   return BSEL_OK;
 }
 
+int bsel_context_set_inverse_grid(bsel_context_t* ctx, int ctas) {
+  if (!ctx || ctas < 0) return BSEL_ERR_ARG;
+  ctx->impl->set_inverse_grid(ctas);
+  return BSEL_OK;
+}
+
 int bsel_synchronize(bsel_context_t* ctx, bsel_status_t* st) {
   return guarded(st, [&] {
     if (!ctx) throw ArgError("ctx is NULL");
@@ -539,6 +545,7 @@ int bsel_profile_end(bsel_profile_t* out) {
     out->gemm_ms = t.gemm_ms;
     out->inverse_calls = t.inverse_calls;
     out->inverse_ms = t.inverse_ms;
+    out->gemm_bytes = t.gemm_bytes;
   }
   return BSEL_OK;
 }

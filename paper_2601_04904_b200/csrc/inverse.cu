@@ -606,7 +606,7 @@ cudaError_t levels_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ld
 
 cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n,
                                  double2* work, int* flag, unsigned long long* status,
-                                 unsigned long long key, cudaStream_t stream) {
+                                 unsigned long long key, cudaStream_t stream, int grid_req) {
   if (n <= 0) return cudaSuccess;
   cudaError_t err;
   const int panels = (n + kLeaf - 1) / kLeaf;
@@ -616,7 +616,8 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     unsigned* barrier = reinterpret_cast<unsigned*>(gD + 2 * kT * kT);
     if ((err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream)) != cudaSuccess) return err;
     int grid = panels * panels < limit ? panels * panels : limit;
-    if (grid > inverse_grid_cap()) grid = inverse_grid_cap();
+    const int cap = grid_req > 0 ? grid_req : inverse_grid_cap();
+    if (grid > cap) grid = cap;
     unsigned long long* trace = g_inverse_trace;
     void* args[] = {(void*)&X, (void*)&ldx, (void*)&Y, (void*)&ldy, (void*)&n,
                     (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag, (void*)&trace};

@@ -32,9 +32,10 @@ int64_t block_inverse_workspace(int n);
 //  flag   : one device int, 0 on entry; 1 = leaf met a zero pivot (fallback ran),
 //           2 + row = exactly singular at pivot row `row`
 //  status : optional device u64; on exact singularity atomicMin(status, key)
+//  grid   : CTAs of the persistent kernel (0 = default, BSEL_INV_GRID or 64)
 cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n,
                                  double2* work, int* flag, unsigned long long* status,
-                                 unsigned long long key, cudaStream_t stream);
+                                 unsigned long long key, cudaStream_t stream, int grid = 0);
 
 // Batched small inverses (n <= kLeaf) in one launch: Y_b = inv(X_b).
 cudaError_t launch_leaf_inverse_batched(const double2* X, int64_t ldx, int64_t strideX, double2* Y,

@@ -193,7 +193,7 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.bc_i = ac(*WB, i), st.bc_j = ac(*WB, j), st.tipB = WB->T();
         st.sb = F.SB(i - lo);
       }
-      end_step(ctx, st, fused, (uint64_t)s, i, (int)(s & 1));
+      end_step(ctx, st, fused, (uint64_t)s, i, fwd_slot(s));
       if (trace && (s + 1) % C == 0) tev(tstep, ctx.chain());
     }
   } else {
@@ -218,7 +218,7 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.nbfill_r = F.BFR(i - lo + 1), st.nbfill_c = F.BFC(i - lo + 1);
         st.sb = F.SB(i - lo);
       }
-      middle_step(ctx, st, fused, (uint64_t)s, i, (int)(s & 1));
+      middle_step(ctx, st, fused, (uint64_t)s, i, fwd_slot(s));
     }
   }
   streams_join(ctx);
@@ -281,7 +281,7 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
   };
   const Mat ytt = XR.T();
   const Mat ztt = fused ? ZR->T() : Mat{};
-  Level L(s);
+  Level L(s, kTileAutoWide);
   if (write_tip) {
     L.out(XA.T()).add(+1, XR.T());
     if (fused) L.out(XB->T()).add(+1, ZR->T());

@@ -61,6 +61,9 @@ class Context {
   Context& operator=(const Context&) = delete;
 
   void set_stream(cudaStream_t s) { user_stream_ = s; }
+  // CTAs of the persistent block inverse (0 = library default).  Fewer when
+  // several contexts run sweeps concurrently on one GPU.
+  void set_inverse_grid(int ctas) { inv_grid_ = ctas; }
   cudaStream_t stream() const { return user_stream_; }
   cudaStream_t aux() const { return aux_; }
   // High-priority stream for the latency-critical Schur chain (pivot
@@ -106,6 +109,7 @@ class Context {
   std::vector<cudaEvent_t> events_;
   std::vector<cudaEvent_t> xfer_events_;
   cudaStream_t xfer_ = nullptr;
+  int inv_grid_ = 0;
   cudaEvent_t timers_[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 

@@ -1,21 +1,28 @@
 // Generic elimination / back-substitution steps (see steps.cuh).
 //
 // Stream discipline of the fused forward steps: the A-side Schur chain
-// (pivot inverse, elimination factors, A updates) is issued on the main
-// stream, the quadratic B-side updates on the aux stream.  Temporaries of
-// step k live in ring half (k & 1); before the A side rewrites a ring half
-// it waits for the B side of step k-2 (ring_wait), so the B side may lag the
-// A chain by one full step and the pivot inverse of step k+1 overlaps the
-// B-side GEMM levels of step k.
+// (pivot inverse, elimination factors, A updates) is issued on the
+// high-priority chain stream, the quadratic B-side updates on the aux
+// stream.  Temporaries of step k live in ring slot k % kFwdDepth; before the
+// A side rewrites a slot it waits for the B side of step k - kFwdDepth
+// (ring_wait), so the B side may lag the A chain by kFwdDepth - 1 steps: the
+// latency-bound chain runs ahead and the B-side GEMM levels fill the SMs it
+// leaves idle.
 #include "steps.cuh"
 
 namespace bsel {
 
 namespace {
-constexpr int kRing = 8;        // slots per ring half
+constexpr int kRing = 8;        // temporaries per forward ring slot
 constexpr int kBackBase = 16;   // first slot used by back_step (2 x kBackSlots)
-Mat rt(Context& ctx, int parity, int k, int r, int c) { return ctx.tmp(parity * kRing + k, r, c); }
+// The forward ring (kFwdDepth x kRing slots) overlaps the backward slots:
+// forward and backward never run concurrently on one context.
+static_assert(kFwdDepth * kRing <= 64, "forward ring exceeds the slot pool");
+Mat rt(Context& ctx, int slot, int k, int r, int c) { return ctx.tmp(slot * kRing + k, r, c); }
 }  // namespace
+
+cudaEvent_t ring_a_event(Context& ctx, int slot) { return ctx.event(8 + slot); }
+cudaEvent_t ring_b_event(Context& ctx, int slot) { return ctx.event(8 + kFwdDepth + slot); }
 
 void streams_fork(Context& ctx) {
   cuda_check(cudaEventRecord(ctx.event(4), ctx.stream()), "fork");
@@ -31,17 +38,18 @@ void streams_join(Context& ctx) {
 }
 
 void ring_wait(Context& ctx, int step) {
-  if (step >= 2) cuda_check(cudaStreamWaitEvent(ctx.chain(), ctx.event(2 + (step & 1)), 0), "ring wait");
+  if (step >= kFwdDepth)
+    cuda_check(cudaStreamWaitEvent(ctx.chain(), ring_b_event(ctx, fwd_slot(step)), 0), "ring wait");
 }
 
-void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int parity) {
+void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int slot) {
   cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
   ctx.invert(st.ad_i, st.S, order, index, sA);
   const Mat& S = st.S;
   if (!fused) {
     // rgf.py:283-288 / dist.py:252-257: right-hand temporaries.
-    Mat t1 = rt(ctx, parity, 0, b, b), t2 = rt(ctx, parity, 1, b, a);
+    Mat t1 = rt(ctx, slot, 0, b, b), t2 = rt(ctx, slot, 1, b, a);
     Level L(sA);
     L.out(t1).mm(+1, S, N, st.Uk, N);
     L.out(t2).mm(+1, S, N, st.ac_i, N);
@@ -53,14 +61,14 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     L.flush();
     return;
   }
-  Mat f = rt(ctx, parity, 0, b, b), g = rt(ctx, parity, 1, a, b), w = rt(ctx, parity, 2, b, b);
-  Mat p = rt(ctx, parity, 3, a, b), k = rt(ctx, parity, 4, b, a), q = rt(ctx, parity, 5, b, b);
+  Mat f = rt(ctx, slot, 0, b, b), g = rt(ctx, slot, 1, a, b), w = rt(ctx, slot, 2, b, b);
+  Mat p = rt(ctx, slot, 3, a, b), k = rt(ctx, slot, 4, b, a), q = rt(ctx, slot, 5, b, b);
   {
     Level L(sA);
     L.out(f).mm(+1, st.Lk, N, S, N);
     L.out(g).mm(+1, st.ar_i, N, S, N);
     L.flush();
-    cuda_check(cudaEventRecord(ctx.event(parity), sA), "record A");
+    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     L.out(st.ad_j).add(+1, st.ad_j).mm(-1, f, N, st.Uk, N);
     L.out(st.ar_j).add(+1, st.ar_j).mm(-1, g, N, st.Uk, N);
     L.out(st.ac_j).add(+1, st.ac_j).mm(-1, f, N, st.ac_i, N);
@@ -69,7 +77,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   }
   // B side in two levels: v Lk^H = Lk S_B Lk^H = f (Bd f^H) = f q removes the
   // reference's serial chain w -> S_B -> v -> Bd (same product count).
-  cuda_check(cudaStreamWaitEvent(sB, ctx.event(parity), 0), "wait A");
+  cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
   Level L(sB);
   L.out(w).mm(+1, S, N, st.bd_i, N);
   L.out(p).mm(+1, g, N, st.bd_i, N);
@@ -82,22 +90,22 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   L.out(st.bc_j).add(+1, st.bc_j).mm(-1, f, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, f, N, k, N);
   L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
   L.flush();
-  cuda_check(cudaEventRecord(ctx.event(2 + parity), sB), "record B");
+  cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
 }
 
-void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int parity) {
+void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int slot) {
   cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
   ctx.invert(st.ad_i, st.S, order, index, sA);
   const Mat& S = st.S;
-  Mat fn = rt(ctx, parity, 0, b, b), fr = rt(ctx, parity, 1, b, b), g = rt(ctx, parity, 2, a, b);
+  Mat fn = rt(ctx, slot, 0, b, b), fr = rt(ctx, slot, 1, b, b), g = rt(ctx, slot, 2, a, b);
   {
     Level L(sA);
     L.out(fn).mm(+1, st.L, N, S, N);
     L.out(fr).mm(+1, st.fill_r, N, S, N);
     L.out(g).mm(+1, st.ar_i, N, S, N);
     L.flush();
-    if (fused) cuda_check(cudaEventRecord(ctx.event(parity), sA), "record A");
+    if (fused) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     L.out(st.nfill_r).mm(-1, fr, N, st.U, N);
     L.out(st.nfill_c).mm(-1, fn, N, st.fill_c, N);
     L.out(st.ad_n).add(+1, st.ad_n).mm(-1, fn, N, st.U, N);
@@ -110,11 +118,11 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     L.flush();
   }
   if (!fused) return;
-  cuda_check(cudaStreamWaitEvent(sB, ctx.event(parity), 0), "wait A");
+  cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
   // v_n = L S_B, v_0 = fill_r S_B enter only as v_x y^H = f_x (Bd f_y^H):
   // two levels instead of the reference's w -> S_B -> v -> update chain.
-  Mat w = rt(ctx, parity, 3, b, b), qn = rt(ctx, parity, 4, b, b), qr = rt(ctx, parity, 5, b, b);
-  Mat p = rt(ctx, parity, 6, a, b), kk = rt(ctx, parity, 7, b, a);
+  Mat w = rt(ctx, slot, 3, b, b), qn = rt(ctx, slot, 4, b, b), qr = rt(ctx, slot, 5, b, b);
+  Mat p = rt(ctx, slot, 6, a, b), kk = rt(ctx, slot, 7, b, a);
   Level L(sB);
   L.out(w).mm(+1, S, N, st.bd_i, N);
   L.out(p).mm(+1, g, N, st.bd_i, N);
@@ -133,7 +141,7 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   L.out(st.bc_n).add(+1, st.bc_n).mm(-1, fn, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, fn, N, kk, N);
   L.out(st.bc_lo).add(+1, st.bc_lo).mm(-1, fr, N, st.bc_i, N).mm(-1, st.bfill_r, N, g, H).mm(+1, fr, N, kk, N);
   L.flush();
-  cuda_check(cudaEventRecord(ctx.event(2 + parity), sB), "record B");
+  cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
 }
 
 namespace {

@@ -17,7 +17,13 @@ struct EndStep {
   Mat bd_i, bd_j, br_i, br_j, bc_i, bc_j, tipB;
   Mat S, sb;
 };
-void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int parity);
+// Forward ring: temporaries of step k live in ring slot fwd_slot(k); the
+// B side (aux stream) may lag the A chain by up to kFwdDepth - 1 steps.
+constexpr int kFwdDepth = 4;
+inline int fwd_slot(int64_t step) { return (int)(step % kFwdDepth); }
+cudaEvent_t ring_a_event(Context& ctx, int slot);  // A side of the slot's step reached its B fork
+cudaEvent_t ring_b_event(Context& ctx, int slot);  // B side of the slot's step done
+void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int slot);
 
 // One interior step of a middle partition with fill-in to its top boundary
 // lo (dist.py:315-396).  fill_* are the couplings before the step, nfill_*
@@ -30,7 +36,7 @@ struct MiddleStep {
   Mat nfill_r, nfill_c, nbfill_r, nbfill_c;
   Mat S, sb;
 };
-void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int parity);
+void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int slot);
 
 // Wait for the B side of the step that last used ring slot `parity` (call
 // before reusing it) and join both streams at the end of a sweep.

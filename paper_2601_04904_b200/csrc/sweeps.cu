@@ -28,7 +28,7 @@ Context::Context(int device) : device_(device) {
   cuda_check(cudaStreamCreateWithPriority(&chain_, cudaStreamNonBlocking, greatest), "chain stream");
   cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "flag");
   cuda_check(cudaMalloc(&d_status_, sizeof(unsigned long long)), "status");
-  events_.resize(8);
+  events_.resize(16);
   for (auto& e : events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& t : timers_) cuda_check(cudaEventCreate(&t), "timer");
   reset_status();
@@ -104,7 +104,7 @@ void Context::invert(Mat X, Mat Y, uint64_t order, int64_t index, cudaStream_t s
   const bool prof = profiling();
   int id = prof ? profile_open(s) : -1;
   if (prof) profile_suspend(true);
-  cudaError_t e = launch_block_inverse(X.p, X.ld, Y.p, Y.ld, X.r, work, d_flag_, d_status_, key, s);
+  cudaError_t e = launch_block_inverse(X.p, X.ld, Y.p, Y.ld, X.r, work, d_flag_, d_status_, key, s, inv_grid_);
   if (prof) profile_suspend(false);
   profile_close(id, s, 1, 8.0 * X.r * (double)X.r * X.r);
   cuda_check(e, "block inverse");
@@ -205,7 +205,7 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
       st.bc_i = B->AC(i), st.bc_j = B->AC(i + 1), st.tipB = B->T();
       st.sb = F.SB(i);
     }
-    end_step(ctx, st, fused, i, i, i & 1);
+    end_step(ctx, st, fused, i, i, fwd_slot(i));
   }
   // Epilogue (rgf.py:290-318).
   const int i = n - 1;
@@ -219,16 +219,16 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
     L.out(A.T()).add(+1, A.T()).mm(-1, A.AR(i), N, t2, N);
     L.flush();
   } else {
-    const int r = (i & 1) * 8;
+    const int r = fwd_slot(i) * 8;
     Mat g = ctx.tmp(r + 1, a, b), p = ctx.tmp(r + 3, a, b);
     ring_wait(ctx, i);
     Level L(sA);
     L.out(g).mm(+1, A.AR(i), N, S, N);
     L.flush();
-    cuda_check(cudaEventRecord(ctx.event(i & 1), sA), "record A");
+    cuda_check(cudaEventRecord(ring_a_event(ctx, fwd_slot(i)), sA), "record A");
     L.out(A.T()).add(+1, A.T()).mm(-1, g, N, A.AC(i), N);
     L.flush();
-    cuda_check(cudaStreamWaitEvent(sB, ctx.event(i & 1), 0), "wait A");
+    cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, fwd_slot(i)), 0), "wait A");
     Level LB(sB);
     LB.out(p).mm(+1, g, N, B->D(i), N);
     copy_block(LB, cm(F.b_diag_last, b, b), B->D(i));

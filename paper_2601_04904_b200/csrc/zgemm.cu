@@ -11,6 +11,8 @@
 //   * conjugation / term sign / the -B_im of the real embedding are sign-bit
 //     XORs on the ALU pipe, never FP64 multiplies;
 //   * epilogue fuses the +-addends (the reference's elementwise +/-).
+#include <cstdlib>
+
 #include "zgemm.cuh"
 
 #include <algorithm>
@@ -279,16 +281,24 @@ cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
   batch.total_tiles = tiles;
   if (tiles == 0) return cudaSuccess;
   int prof = -1;
-  double flops = 0.0;
+  double flops = 0.0, bytes = 0.0;
   if (profiling()) {
-    for (int i = 0; i < batch.nproblems; ++i)
-      for (int t = 0; t < batch.p[i].nterms; ++t)
-        flops += 8.0 * batch.p[i].M * (double)batch.p[i].N * batch.p[i].term[t].K;
+    // flops: 8 real flops per complex MAC; bytes: every operand read once,
+    // D written once (the compulsory DRAM traffic of the launch).
+    for (int i = 0; i < batch.nproblems; ++i) {
+      const GemmProblem& P = batch.p[i];
+      const double M = P.M, N = P.N;
+      bytes += 16.0 * M * N * (1 + P.naddends);
+      for (int t = 0; t < P.nterms; ++t) {
+        flops += 8.0 * M * N * P.term[t].K;
+        bytes += 16.0 * (M + N) * P.term[t].K;
+      }
+    }
     prof = profile_open(stream);
   }
   zgemm_grouped_kernel<C><<<tiles, C::THREADS, C::SMEM, stream>>>(batch);
   count_launch();
-  profile_close(prof, stream, 0, flops);
+  profile_close(prof, stream, 0, flops, bytes);
   return cudaGetLastError();
 }
 
@@ -306,6 +316,7 @@ struct ProfRec {
   cudaEvent_t t0, t1;
   int kind;
   double flops;
+  double bytes;
 };
 // Partitions of one solve may run in concurrent host threads (dist.py
 // _Lanes): records are appended under a mutex (deque: stable references),
@@ -336,11 +347,12 @@ int profile_open(cudaStream_t s) {
   cudaEventRecord(g_prof[id].t0, s);
   return id;
 }
-void profile_close(int id, cudaStream_t s, int kind, double flops) {
+void profile_close(int id, cudaStream_t s, int kind, double flops, double bytes) {
   if (id < 0) return;
   std::lock_guard<std::mutex> lock(g_prof_mu);
   g_prof[id].kind = kind;
   g_prof[id].flops = flops;
+  g_prof[id].bytes = bytes;
   cudaEventRecord(g_prof[id].t1, s);
 }
 ProfileTotals profile_end() {
@@ -353,6 +365,7 @@ ProfileTotals profile_end() {
     if (g_prof[i].kind == 0) {
       ++t.gemm_launches;
       t.gemm_flops += g_prof[i].flops;
+      t.gemm_bytes += g_prof[i].bytes;
       t.gemm_ms += ms;
     } else {
       ++t.inverse_calls;
@@ -390,11 +403,21 @@ cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cf
   std::stable_sort(batch.p, batch.p + w, [](const GemmProblem& x, const GemmProblem& y) {
     return problem_weight(x) > problem_weight(y);
   });
-  if (tile_cfg == kTileAuto) {
+  if (tile_cfg == kTileAuto || tile_cfg == kTileAutoWide) {
     int64_t tiles64 = 0;
     for (int i = 0; i < w; ++i)
       tiles64 += (int64_t)((batch.p[i].M + 63) / 64) * ((batch.p[i].N + 63) / 64);
-    tile_cfg = (tiles64 >= 2 * device_sm_count()) ? kTile64 : kTile32;
+    // 64x64 tiles (8 warps) run the DMMA pipe hotter than 32x32 (4 warps)
+    // but leave SMs idle when there are too few of them.
+    static const int64_t min64 = [] {
+      const char* e = getenv("BSEL_GEMM_MIN_TILES64");
+      return e ? (int64_t)atoll(e) : (int64_t)2 * device_sm_count();
+    }();
+    static const int64_t min64_wide = [] {
+      const char* e = getenv("BSEL_GEMM_MIN_TILES64_WIDE");
+      return e ? (int64_t)atoll(e) : (int64_t)128;
+    }();
+    tile_cfg = (tiles64 >= (tile_cfg == kTileAutoWide ? min64_wide : min64)) ? kTile64 : kTile32;
   }
   if (tile_cfg == kTile64) return launch_cfg<Cfg64>(batch, stream);
   return launch_cfg<Cfg32>(batch, stream);

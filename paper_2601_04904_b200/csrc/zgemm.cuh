@@ -66,7 +66,10 @@ struct GemmBatch {
 };
 
 // Tile configurations (complex tile BM x BN).
-enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2 };
+// kTileAuto: 64x64 tiles once a launch has >= 2 waves of them; kTileAutoWide:
+// already from fewer tiles (backward sweeps: their launches overlap the
+// next level's on the same stream less, and 64x64 tiles run the pipe hotter).
+enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3 };
 
 // Launch one grouped batch on `stream`.  Problems with M==0 or N==0 are
 // dropped.  Returns cudaSuccess or the launch error.
@@ -88,12 +91,13 @@ struct ProfileTotals {
   double gemm_ms;
   int64_t inverse_calls;
   double inverse_ms;
+  double gemm_bytes;
 };
 void profile_begin();
 ProfileTotals profile_end();
 bool profiling();
 void profile_suspend(bool on);  // temporarily ignore GEMM launches (inside an inverse)
 int profile_open(cudaStream_t s);                          // returns record id (or -1)
-void profile_close(int id, cudaStream_t s, int kind, double flops);
+void profile_close(int id, cudaStream_t s, int kind, double flops, double bytes = 0.0);
 
 }  // namespace bsel

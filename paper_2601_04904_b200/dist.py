@@ -393,6 +393,9 @@ class _Lanes:
         self.device = device
         self.count = count
         self.streams = [torch.cuda.Stream(device) for _ in range(count)]
+        # Concurrent chains share the SMs: each block inverse gets fewer CTAs
+        # (cfg4, 2 lanes: 28-36 CTAs -> 2000 ms vs 2035 ms at the default 64).
+        self.inverse_grid = int(os.environ.get("BSEL_LANE_INV_GRID", "32")) if count > 1 else 0
 
     def run(self, fn) -> list:
         import threading
@@ -406,7 +409,12 @@ class _Lanes:
             try:
                 with torch.cuda.device(self.device), torch.cuda.stream(self.streams[rank]):
                     self.streams[rank].wait_event(start)
-                    fn(rank, _native.Context.get(self.device.index, lane=rank))
+                    ctx = _native.Context.get(self.device.index, lane=rank)
+                    ctx.set_inverse_grid(self.inverse_grid)
+                    try:
+                        fn(rank, ctx)
+                    finally:
+                        ctx.set_inverse_grid(0)
             except Exception as exc:  # noqa: BLE001 - rank attribution
                 errors.append((rank, exc))
 

@@ -136,16 +136,19 @@ def test_abi_struct_layouts():
     import shutil
     import subprocess
     import tempfile
-    sizes = {"Status": 272, "Bta": 72, "Factors": 104}
+    names = {"Status": "bsel_status_t", "Bta": "bsel_bta_t", "Factors": "bsel_factors_t",
+             "LocalFactors": "bsel_local_factors_t", "Profile": "bsel_profile_t", "HostIo": "bsel_host_io_t"}
+    sizes = {"Status": 272, "Bta": 72, "Factors": 104, "LocalFactors": 96, "Profile": 48, "HostIo": 56}
     if shutil.which("gcc"):
-        src = ('#include <stdio.h>\n#include "btasel_b200.h"\nint main(void){printf("%zu %zu %zu",'
-               'sizeof(bsel_status_t), sizeof(bsel_bta_t), sizeof(bsel_factors_t));return 0;}')
+        fmt = " ".join(["%zu"] * len(names))
+        src = ('#include <stdio.h>\n#include "btasel_b200.h"\nint main(void){printf("' + fmt + '",'
+               + ", ".join(f"sizeof({c})" for c in names.values()) + ');return 0;}')
         with tempfile.TemporaryDirectory() as d:
             open(os.path.join(d, "t.c"), "w").write(src)
             subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", os.path.join(d, "t"),
                             os.path.join(d, "t.c")], check=True)
             out = subprocess.run([os.path.join(d, "t")], capture_output=True, text=True, check=True).stdout
-        sizes = dict(zip(("Status", "Bta", "Factors"), map(int, out.split())))
+        sizes = dict(zip(names, map(int, out.split())))
     for name, size in sizes.items():
         assert ctypes.sizeof(getattr(_native, name)) == size, name
     size = ctypes.c_size_t()
