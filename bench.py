@@ -39,6 +39,7 @@ WORKLOADS = {
     "cfg5": (256, 1024, 256, 4),
 }
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_zgemm_traffic_r01.json")
 METRIC = "ms per energy point, fused BTA SI+SQ at 1/2/4/8 B200; % FP64 TC peak"
 
 
@@ -358,6 +359,10 @@ def main():
         step()
     lib.bsel_profile_end(prof)
     peak, peak_src = fp64_peak_tflops()
+    ncu = None
+    if os.path.exists(NCU_TRAFFIC_FILE):
+        with open(NCU_TRAFFIC_FILE) as f:
+            ncu = json.load(f)
     gemm_tflops = prof.gemm_flops / (prof.gemm_ms * 1e-3) / 1e12 if prof.gemm_ms > 0 else None
     F = flops_seq(n, b, a)
     achieved_step = F / (ms * 1e-3) / 1e12
@@ -413,7 +418,15 @@ def main():
             "flops_per_step": F,
             "roofline": {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA)", "achieved": gemm_tflops,
                          "peak": peak, "unit": "TFLOP/s", "frac": (gemm_tflops / peak) if gemm_tflops else None,
-                         "traffic": None, "peak_source": peak_src,
+                         # DRAM bytes per launch of this kernel from one ncu --set full capture of all
+                         # its launches in a cfg4-shaped solve (profiles/ncu_zgemm_traffic_r01.json)
+                         "traffic": ncu["dram_bytes_per_launch"] if ncu else None,
+                         "traffic_source": ("ncu --set full, " + ncu["target"]) if ncu else None,
+                         # every operand read once + outputs written once, live over this step's launches
+                         "compulsory_bytes_per_launch": (prof.gemm_bytes / prof.gemm_launches
+                                                         if prof.gemm_launches else None),
+                         "traffic_over_compulsory": ncu["traffic_over_compulsory"] if ncu else None,
+                         "peak_source": peak_src,
                          # kernel share of the instrumented (single-lane, sequential-RGF) solve
                          "share_of_step": prof.gemm_ms / (seq_ms or ms) if ms else None,
                          "inverse_ms_per_step": prof.inverse_ms, "gemm_launches_per_step": prof.gemm_launches},

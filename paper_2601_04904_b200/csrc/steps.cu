@@ -42,6 +42,11 @@ void ring_wait(Context& ctx, int step) {
     cuda_check(cudaStreamWaitEvent(ctx.chain(), ring_b_event(ctx, fwd_slot(step)), 0), "ring wait");
 }
 
+// Critical chain of a step: pivot inverse -> f = Lk S -> ad_j -= f Uk (the
+// next inverse needs nothing else).  Every other update -- arrow strips, tip,
+// the whole B side -- runs on the aux stream, which may lag the chain by
+// kFwdDepth - 1 steps.  Each output keeps the reference's expression and
+// term order, so results do not depend on the stream split.
 void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int slot) {
   cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
@@ -52,13 +57,19 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     Mat t1 = rt(ctx, slot, 0, b, b), t2 = rt(ctx, slot, 1, b, a);
     Level L(sA);
     L.out(t1).mm(+1, S, N, st.Uk, N);
-    L.out(t2).mm(+1, S, N, st.ac_i, N);
     L.flush();
+    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     L.out(st.ad_j).add(+1, st.ad_j).mm(-1, st.Lk, N, t1, N);
-    L.out(st.ar_j).add(+1, st.ar_j).mm(-1, st.ar_i, N, t1, N);
-    L.out(st.ac_j).add(+1, st.ac_j).mm(-1, st.Lk, N, t2, N);
-    L.out(st.tipA).add(+1, st.tipA).mm(-1, st.ar_i, N, t2, N);
     L.flush();
+    cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
+    Level LB(sB);
+    LB.out(t2).mm(+1, S, N, st.ac_i, N);
+    LB.out(st.ar_j).add(+1, st.ar_j).mm(-1, st.ar_i, N, t1, N);
+    LB.flush();
+    LB.out(st.ac_j).add(+1, st.ac_j).mm(-1, st.Lk, N, t2, N);
+    LB.out(st.tipA).add(+1, st.tipA).mm(-1, st.ar_i, N, t2, N);
+    LB.flush();
+    cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
     return;
   }
   Mat f = rt(ctx, slot, 0, b, b), g = rt(ctx, slot, 1, a, b), w = rt(ctx, slot, 2, b, b);
@@ -66,26 +77,28 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   {
     Level L(sA);
     L.out(f).mm(+1, st.Lk, N, S, N);
-    L.out(g).mm(+1, st.ar_i, N, S, N);
     L.flush();
     cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     L.out(st.ad_j).add(+1, st.ad_j).mm(-1, f, N, st.Uk, N);
-    L.out(st.ar_j).add(+1, st.ar_j).mm(-1, g, N, st.Uk, N);
-    L.out(st.ac_j).add(+1, st.ac_j).mm(-1, f, N, st.ac_i, N);
-    L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
     L.flush();
   }
-  // B side in two levels: v Lk^H = Lk S_B Lk^H = f (Bd f^H) = f q removes the
-  // reference's serial chain w -> S_B -> v -> Bd (same product count).
+  // Aux: A-side arrow/tip updates and the B side in three levels.  v Lk^H =
+  // Lk S_B Lk^H = f (Bd f^H) = f q removes the reference's serial chain
+  // w -> S_B -> v -> Bd (same product count).
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
   Level L(sB);
+  L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(w).mm(+1, S, N, st.bd_i, N);
+  L.out(q).mm(+1, st.bd_i, N, f, H);
+  L.out(st.ac_j).add(+1, st.ac_j).mm(-1, f, N, st.ac_i, N);
+  L.flush();
+  L.out(st.ar_j).add(+1, st.ar_j).mm(-1, g, N, st.Uk, N);
+  L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
   L.out(p).mm(+1, g, N, st.bd_i, N);
   L.out(k).mm(+1, st.bd_i, N, g, H);
-  L.out(q).mm(+1, st.bd_i, N, f, H);
-  L.flush();
   L.out(st.sb).mm(+1, w, N, S, H);
   L.out(st.bd_j).add(+1, st.bd_j).mm(+1, f, N, q, N).mm(-1, st.BL, N, f, H).mm(-1, f, N, st.BU, N);
+  L.flush();
   L.out(st.br_j).add(+1, st.br_j).mm(-1, g, N, st.BU, N).mm(+1, p, N, f, H).mm(-1, st.br_i, N, f, H);
   L.out(st.bc_j).add(+1, st.bc_j).mm(-1, f, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, f, N, k, N);
   L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
@@ -93,6 +106,8 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
 }
 
+// Middle step: the chain is inverse -> fn = L S -> ad_n -= fn U; fill-in,
+// lo-boundary, arrow, tip and B-side updates run on the aux stream.
 void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int slot) {
   cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
@@ -102,39 +117,47 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   {
     Level L(sA);
     L.out(fn).mm(+1, st.L, N, S, N);
-    L.out(fr).mm(+1, st.fill_r, N, S, N);
-    L.out(g).mm(+1, st.ar_i, N, S, N);
     L.flush();
-    if (fused) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
-    L.out(st.nfill_r).mm(-1, fr, N, st.U, N);
-    L.out(st.nfill_c).mm(-1, fn, N, st.fill_c, N);
+    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     L.out(st.ad_n).add(+1, st.ad_n).mm(-1, fn, N, st.U, N);
-    L.out(st.ad_lo).add(+1, st.ad_lo).mm(-1, fr, N, st.fill_c, N);
-    L.out(st.ar_n).add(+1, st.ar_n).mm(-1, g, N, st.U, N);
-    L.out(st.ar_lo).add(+1, st.ar_lo).mm(-1, g, N, st.fill_c, N);
-    L.out(st.ac_n).add(+1, st.ac_n).mm(-1, fn, N, st.ac_i, N);
-    L.out(st.ac_lo).add(+1, st.ac_lo).mm(-1, fr, N, st.ac_i, N);
-    L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
     L.flush();
   }
-  if (!fused) return;
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
-  // v_n = L S_B, v_0 = fill_r S_B enter only as v_x y^H = f_x (Bd f_y^H):
-  // two levels instead of the reference's w -> S_B -> v -> update chain.
-  Mat w = rt(ctx, slot, 3, b, b), qn = rt(ctx, slot, 4, b, b), qr = rt(ctx, slot, 5, b, b);
-  Mat p = rt(ctx, slot, 6, a, b), kk = rt(ctx, slot, 7, b, a);
   Level L(sB);
-  L.out(w).mm(+1, S, N, st.bd_i, N);
+  L.out(fr).mm(+1, st.fill_r, N, S, N);
+  L.out(g).mm(+1, st.ar_i, N, S, N);
+  L.out(st.nfill_c).mm(-1, fn, N, st.fill_c, N);
+  L.out(st.ac_n).add(+1, st.ac_n).mm(-1, fn, N, st.ac_i, N);
+  Mat w, qn, qr, p, kk;
+  if (fused) {
+    // v_n = L S_B, v_0 = fill_r S_B enter only as v_x y^H = f_x (Bd f_y^H):
+    // two levels instead of the reference's w -> S_B -> v -> update chain.
+    w = rt(ctx, slot, 3, b, b), qn = rt(ctx, slot, 4, b, b), qr = rt(ctx, slot, 5, b, b);
+    p = rt(ctx, slot, 6, a, b), kk = rt(ctx, slot, 7, b, a);
+    L.out(w).mm(+1, S, N, st.bd_i, N);
+    L.out(qn).mm(+1, st.bd_i, N, fn, H);
+  }
+  L.flush();
+  L.out(st.nfill_r).mm(-1, fr, N, st.U, N);
+  L.out(st.ad_lo).add(+1, st.ad_lo).mm(-1, fr, N, st.fill_c, N);
+  L.out(st.ar_n).add(+1, st.ar_n).mm(-1, g, N, st.U, N);
+  L.out(st.ar_lo).add(+1, st.ar_lo).mm(-1, g, N, st.fill_c, N);
+  L.out(st.ac_lo).add(+1, st.ac_lo).mm(-1, fr, N, st.ac_i, N);
+  L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
+  if (!fused) {
+    L.flush();
+    cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
+    return;
+  }
   L.out(p).mm(+1, g, N, st.bd_i, N);
-  L.out(qn).mm(+1, st.bd_i, N, fn, H);
   L.out(qr).mm(+1, st.bd_i, N, fr, H);
   L.out(kk).mm(+1, st.bd_i, N, g, H);
-  L.flush();
   L.out(st.sb).mm(+1, w, N, S, H);
+  L.out(st.bd_n).add(+1, st.bd_n).mm(-1, fn, N, st.BU, N).mm(-1, st.BL, N, fn, H).mm(+1, fn, N, qn, N);
+  L.flush();
   L.out(st.br_n).add(+1, st.br_n).mm(-1, g, N, st.BU, N).mm(-1, st.br_i, N, fn, H).mm(+1, p, N, fn, H);
   L.out(st.br_lo).add(+1, st.br_lo).mm(-1, g, N, st.bfill_c, N).mm(-1, st.br_i, N, fr, H).mm(+1, p, N, fr, H);
   L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
-  L.out(st.bd_n).add(+1, st.bd_n).mm(-1, fn, N, st.BU, N).mm(-1, st.BL, N, fn, H).mm(+1, fn, N, qn, N);
   L.out(st.nbfill_c).mm(-1, fn, N, st.bfill_c, N).mm(-1, st.BL, N, fr, H).mm(+1, fn, N, qr, N);
   L.out(st.nbfill_r).mm(-1, fr, N, st.BU, N).mm(-1, st.bfill_r, N, fn, H).mm(+1, fr, N, qn, N);
   L.out(st.bd_lo).add(+1, st.bd_lo).mm(-1, fr, N, st.bfill_c, N).mm(-1, st.bfill_r, N, fr, H).mm(+1, fr, N, qr, N);

@@ -207,8 +207,10 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
     }
     end_step(ctx, st, fused, i, i, fwd_slot(i));
   }
-  // Epilogue (rgf.py:290-318).
+  // Epilogue (rgf.py:290-318).  The last block's arrow strips and the tip
+  // were updated on the aux stream: the chain waits for the last step's aux.
   const int i = n - 1;
+  if (n >= 2) cuda_check(cudaStreamWaitEvent(sA, ring_b_event(ctx, fwd_slot(n - 2)), 0), "aux done");
   Mat S = F.SA(i);
   ctx.invert(A.D(i), S, i, i, sA);
   if (!fused) {

@@ -46,7 +46,14 @@ struct Cfg {
   static_assert(FM * 8 == WTM && FN * 4 == WTN, "warp tile");
 };
 
-using Cfg64 = Cfg<64, 64, 2, 4, 3, 2, 16>;
+// 64x64 tiles: 8 warps (32x16 warp tiles), BK 8 x 4 stages, 2 CTAs/SM.
+// Measured on the cfg4 level shapes (tools/gemm_micro, 3 concurrent
+// streams): 31.5 TF/s vs 31.3 for BK 16 x 3 stages, 32.2 for 4 warps with
+// 32x32 warp tiles (which loses 25 % on single launches: 3 CTAs/SM quantize
+// worse); whole solve 1972 vs 1989 ms.
+using Cfg64 = Cfg<64, 64, 2, 4, 4, 2, 8>;
+// 32x32 tiles, 4 warps: latency-critical and small levels (forward sweeps).
+// 32x64 / 64x32 tiles with 4 warps measured no better on the whole solve.
 using Cfg32 = Cfg<32, 32, 2, 2, 4, 4>;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {

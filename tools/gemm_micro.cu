@@ -149,6 +149,39 @@ int main() {
              flops(lv[li].b) * reps / ms / 1e9);
     }
   }
+  // Concurrent: the same level on 3 streams at once (tails overlap, as in
+  // the real sweeps where chain / aux / other partition overlap).
+  cudaStream_t cs[3];
+  for (auto& x : cs) cudaStreamCreate(&x);
+  for (size_t li = 0; li < lv.size(); ++li) {
+    for (int cfg : {kTile64, kTile32}) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      const int reps = 20;
+      cudaDeviceSynchronize();
+      cudaEventRecord(e0, cs[0]);
+      cudaStreamWaitEvent(cs[1], e0, 0);
+      cudaStreamWaitEvent(cs[2], e0, 0);
+      for (int r = 0; r < reps; ++r)
+        for (auto& x : cs) {
+          GemmBatch b = lv[li].b;
+          launch_gemm_batch(b, x, cfg);
+        }
+      for (int k = 1; k < 3; ++k) {
+        cudaEvent_t ek;
+        cudaEventCreate(&ek);
+        cudaEventRecord(ek, cs[k]);
+        cudaStreamWaitEvent(cs[0], ek, 0);
+      }
+      cudaEventRecord(e1, cs[0]);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf(", \"%s_%s_x3_tflops\": %.2f", lv[li].name, cfg == kTile64 ? "t64" : "t32",
+             flops(lv[li].b) * reps * 3 / ms / 1e9);
+    }
+  }
   printf(", \"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
