@@ -29,6 +29,9 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# NCCL's version banner goes to stdout, which must carry only the JSON line.
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
@@ -167,80 +170,43 @@ def run_reference(args, n, b, a):
     print(json.dumps(line), flush=True)
 
 
-def rank_slices(plan, rank, n):
-    """Block ranges one rank needs (inputs) and owns (outputs) in the
-    distributed scheme: its partition, the separators next to it, and every
-    partition separator (reduced-system assembly, dist.py:479-486)."""
-    lo, hi = plan.ranges[rank]
-    off = (max(lo - 1, 0), min(hi, n - 1))
-    ins = {"diag": [(lo, hi)], "arrow_row": [(lo, hi)], "arrow_col": [(lo, hi)], "lower": [off], "upper": [off]}
-    for p in range(plan.num_parts - 1):
-        g = plan.ranges[p][1] - 1
-        if not off[0] <= g < off[1]:
-            ins["lower"].append((g, g + 1))
-            ins["upper"].append((g, g + 1))
-    mine = (lo, min(hi, n - 1))
-    outs = {"diag": [(lo, hi)], "arrow_row": [(lo, hi)], "arrow_col": [(lo, hi)], "lower": [mine], "upper": [mine]}
-    return ins, outs
-
-
 def dist_e2e(args, solver, A, B, n, world, rank, dev, dist):
-    """N>1 end-to-end: every step each rank copies the input blocks it needs
-    from pinned host memory, runs its part of the distributed solve, and
-    copies the solution blocks it owns back (outputs stay sharded)."""
+    """N>1 end-to-end through DistSolver.solve(host_in, host_out): every step
+    each rank streams the input blocks it needs from pinned host memory
+    (its partition chunk by chunk behind its forward sweep, plus the other
+    partitions' separators and the tip) and streams the solution blocks it
+    owns back behind its backward sweep (outputs stay sharded).  Host
+    storage per rank = HostWindow (only the blocks that rank touches)."""
     import torch
+    import paper_2601_04904_b200 as bs
 
-    ins, outs = rank_slices(solver.plan, rank, n)
-
-    def pinned_like(t):
-        return torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-
-    h2d, d2h = [], []  # (device view, pinned host buffer)
-    for M in (A, B):
-        for kind, ranges in ins.items():
-            for s, e in ranges:
-                if e > s:
-                    view = getattr(M, kind)[s:e]
-                    host = pinned_like(view)
-                    host.copy_(view)
-                    h2d.append((view, host))
-        host = pinned_like(M.tip)
-        host.copy_(M.tip)
-        h2d.append((M.tip, host))
-    for X in solver.out:
-        for kind, ranges in outs.items():
-            for s, e in ranges:
-                if e > s:
-                    view = getattr(X, kind)[s:e]
-                    d2h.append((view, pinned_like(view)))
-        if rank == 0:
-            d2h.append((X.tip, pinned_like(X.tip)))
-
-    def step():
-        for view, host in h2d:
-            view.copy_(host, non_blocking=True)
-        solver.solve()
-        for view, host in d2h:
-            host.copy_(view, non_blocking=True)
-
-    step()
+    lo, hi = solver.plan.ranges[rank]
+    seps = [solver.plan.ranges[p][1] - 1 for p in range(world - 1)]
+    hin = tuple(bs.HostWindow(n, A.b, A.a, lo, hi, seps).fill_from(M) for M in (A, B))
+    hout = tuple(bs.HostWindow(n, A.b, A.a, lo, hi) for _ in (A, B))
+    torch.cuda.synchronize()
+    solver.solve(host_in=hin, host_out=hout)
     torch.cuda.synchronize()
     dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(args.steps):
-        step()
+        solver.solve(host_in=hin, host_out=hout)
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / args.steps
-    stats = torch.tensor([ms, sum(h.numel() * 16 for _, h in h2d), sum(h.numel() * 16 for _, h in d2h)],
-                         dtype=torch.float64, device=dev)
+    # bytes actually moved per step: inputs of the window (tip once per rank),
+    # outputs = the blocks this rank owns (+ the tip on rank 0)
+    h2d = sum(w.nbytes for w in hin)
+    d2h = sum(w.nbytes - w.tip.numel() * 16 * (rank != 0) for w in hout)
+    stats = torch.tensor([ms, h2d, d2h], dtype=torch.float64, device=dev)
     mx = stats[:1].clone()
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     dist.all_reduce(stats, op=dist.ReduceOp.SUM)
     return {"value": float(mx.item()), "unit": "ms", "h2d_bytes_per_step": int(stats[1].item()),
             "d2h_bytes_per_step": int(stats[2].item()),
-            "note": "per rank: H2D of its partition + separators, D2H of its owned solution blocks; max over ranks"}
+            "note": "per rank: its partition + separators + tip streamed in behind the forward, its owned "
+                    "solution blocks streamed out behind the backward; max over ranks"}
 
 
 def main():

@@ -32,7 +32,7 @@ from .device import DeviceBta, generate_dd_bta_device, hermitianize_device, kern
 from .rgf import (RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, default_partitions,
                   release_caches, solve_selected)
 from .collectives import Collectives, LocalHub, TorchCollectives, TraceEvent
-from .dist import (BoundaryPayload, DistSolver, InGpuPartitions, LocalFactors, ReducedSystem, assemble_reduced,
+from .dist import (BoundaryPayload, DistSolver, HostWindow, InGpuPartitions, LocalFactors, ReducedSystem, assemble_reduced,
                    dist_solve,
                    local_backward, local_forward, solve_reduced)
 
@@ -45,7 +45,7 @@ __all__ = [
     "bt_forward", "bt_backward", "bta_forward", "bta_backward", "solve_selected", "default_partitions",
     "release_caches", "InGpuPartitions",
     "plan_partitions", "dist_solve", "local_forward", "assemble_reduced", "solve_reduced", "local_backward",
-    "BoundaryPayload", "LocalFactors", "ReducedSystem", "DistSolver", "Collectives", "TorchCollectives",
+    "BoundaryPayload", "LocalFactors", "ReducedSystem", "DistSolver", "HostWindow", "Collectives", "TorchCollectives",
     "LocalHub", "TraceEvent", "generate_dd_bta_device", "hermitianize_device", "kernel_launches",
     "BtaselError", "ShapeMismatchError", "SingularBlockError", "DenseGuardError", "ProtocolError",
     "WorkerError", "NativeUnavailableError",

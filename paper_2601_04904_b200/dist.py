@@ -428,6 +428,70 @@ class _Lanes:
         return errors
 
 
+class HostWindow:
+    """Pinned host storage for the blocks of a full-size BTA matrix that ONE
+    rank of the distributed solve touches: its partition's diagonal / arrow
+    blocks and couplings, the separators of the other partitions (the
+    replicated reduced system needs them) and the tip.  Its descriptor
+    (``desc()``) addresses blocks by their GLOBAL index, so it can stand in
+    for a full-size host matrix in ``DistSolver.solve`` without pinning the
+    whole matrix on every rank (only the window's blocks are ever touched)."""
+
+    def __init__(self, n, b, a, lo, hi, separators=()):
+        self.n, self.b, self.a, self.lo, self.hi = n, b, a, lo, hi
+        self.c_hi = min(hi, n - 1)
+        pin = dict(dtype=torch.complex128, pin_memory=torch.cuda.is_available())
+        self.diag = torch.empty((hi - lo, b, b), **pin)
+        self.arrow_row = torch.empty((hi - lo, a, b), **pin)
+        self.arrow_col = torch.empty((hi - lo, b, a), **pin)
+        self.lower = torch.empty((max(self.c_hi - lo, 0), b, b), **pin)
+        self.upper = torch.empty((max(self.c_hi - lo, 0), b, b), **pin)
+        self.tip = torch.empty((a, a), **pin)
+        self.separators = {g: (torch.empty((b, b), **pin), torch.empty((b, b), **pin))
+                           for g in separators if not lo <= g < self.c_hi}
+
+    @property
+    def shape_params(self):
+        return self.n, self.b, self.a
+
+    def fill_from(self, m: DeviceBta) -> "HostWindow":
+        """Copy the window's blocks out of a full-size device matrix."""
+        lo, hi, c = self.lo, self.hi, self.c_hi
+        self.diag.copy_(m.diag[lo:hi])
+        self.arrow_row.copy_(m.arrow_row[lo:hi])
+        self.arrow_col.copy_(m.arrow_col[lo:hi])
+        if c > lo:
+            self.lower.copy_(m.lower[lo:c])
+            self.upper.copy_(m.upper[lo:c])
+        self.tip.copy_(m.tip)
+        for g, (lw, up) in self.separators.items():
+            lw.copy_(m.lower[g])
+            up.copy_(m.upper[g])
+        return self
+
+    def separator(self, g):
+        if self.lo <= g < self.c_hi:
+            return self.lower[g - self.lo], self.upper[g - self.lo]
+        return self.separators[g]
+
+    def desc(self) -> _native.Bta:
+        d = _native.Bta()
+        d.n, d.b, d.a = self.n, self.b, self.a
+        for k in ("diag", "arrow_row", "arrow_col", "lower", "upper"):
+            t = getattr(self, k)
+            per = t[0].numel() * 16 if t.numel() else 0
+            # global block g lives at base + (g - lo) * per
+            setattr(d, k, (t.data_ptr() - self.lo * per) if t.numel() else None)
+        d.tip = self.tip.data_ptr() if self.tip.numel() else None
+        return d
+
+    @property
+    def nbytes(self):
+        ts = [self.diag, self.arrow_row, self.arrow_col, self.lower, self.upper, self.tip]
+        ts += [x for pair in self.separators.values() for x in pair]
+        return sum(t.numel() * 16 for t in ts)
+
+
 def _host_io(chunk, a=None, b=None, x_a=None, x_b=None, copy_tip=False, stream=None):
     """bsel_host_io_t for local_forward / local_backward end-to-end mode
     (the descriptors are kept alive on the returned struct)."""
@@ -435,7 +499,7 @@ def _host_io(chunk, a=None, b=None, x_a=None, x_b=None, copy_tip=False, stream=N
     keep = []
     for k, m in (("a", a), ("b", b), ("x_a", x_a), ("x_b", x_b)):
         if m is not None:
-            d = _native.host_desc(m)
+            d = m.desc() if isinstance(m, HostWindow) else _native.host_desc(m)
             keep.append(d)
             setattr(io, k, ctypes.pointer(d))
     io.chunk_blocks = int(chunk)
@@ -657,10 +721,28 @@ class DistSolver:
         self._fac = None
         self.timings = {}
 
-    def solve(self):
+    def solve(self, host_in=None, host_out=None):
+        """One distributed solve.  ``host_in`` = (a, b) full-size pinned host
+        BtaMatrix: this rank's partition streams in behind its forward sweep
+        (plus the separators and tip every rank needs for the replicated
+        reduced system); ``host_out`` = (x_a, x_b) full-size host BtaMatrix:
+        the blocks this rank owns stream out behind its backward sweep."""
+        chunk = int(os.environ.get("BSEL_STREAM_CHUNK", "8"))
+        fused = self.B is not None
+        io_in = io_out = None
+        if host_in is not None:
+            io_in = _host_io(chunk, a=host_in[0], b=host_in[1] if fused else None, copy_tip=True)
+            self._copy_separators(host_in)
+        if host_out is not None:
+            io_out = _host_io(chunk, x_a=host_out[0], x_b=host_out[1] if fused else None)
         tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
         tm.start("forward")
-        pay, delta, self._fac = local_forward(self.A, self.B, self.plan, self.rank, _factors=self._fac)
+        if self._fac is None:
+            lo, hi = self.plan.ranges[self.rank]
+            self._fac = _alloc_factors(self.plan.kinds[self.rank], lo, hi, fused, self.A.b, self.A.a,
+                                       self.A.device)
+        pay, delta, self._fac = local_forward(self.A, self.B, self.plan, self.rank, _factors=self._fac,
+                                              _sync=io_in)
         tm.stop("forward")
         tm.start("communication")
         reduced = assemble_reduced(self.coll, self.A, self.B, self.plan, pay, delta)
@@ -669,10 +751,30 @@ class DistSolver:
         red_sol = solve_reduced(reduced, self.mode)
         tm.stop("reduced")
         tm.start("backward")
-        local_backward(self.A, self.B, self.plan, self.rank, self._fac, reduced, red_sol, out=self.out)
+        local_backward(self.A, self.B, self.plan, self.rank, self._fac, reduced, red_sol, out=self.out,
+                       _sync=io_out)
         tm.stop("backward")
         self._tm = tm
         return self.out
+
+    def _copy_separators(self, host_in):
+        """Couplings at the other partitions' boundaries (the reduced system
+        is assembled on every rank)."""
+        lo, hi = self.plan.ranges[self.rank]
+        for p in range(self.plan.num_parts - 1):
+            g = self.plan.ranges[p][1] - 1
+            if lo <= g < hi:
+                continue  # streamed with this rank's own chunks
+            for hm, D in zip(host_in, (self.A, self.B)):
+                if hm is None or D is None:
+                    continue
+                if isinstance(hm, HostWindow):
+                    lw, up = hm.separator(g)
+                else:
+                    h = hm.stacked()
+                    lw, up = torch.from_numpy(h["lower"][g]), torch.from_numpy(h["upper"][g])
+                D.lower[g].copy_(lw, non_blocking=True)
+                D.upper[g].copy_(up, non_blocking=True)
 
     def phase_seconds(self):
         return self._tm.seconds()

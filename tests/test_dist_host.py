@@ -161,26 +161,30 @@ def test_partition_counts_match_reference(name):
 
 
 @pytest.mark.parametrize("n,parts", [(1024, 8), (1024, 4), (12, 3), (8, 4), (20, 2)])
-def test_bench_rank_slices_cover_pattern(n, parts):
-    """bench.py's N>1 end-to-end copies: the owned output blocks of all ranks
-    partition the pattern exactly; every rank's inputs include its partition,
-    its neighbouring separators and all partition separators."""
-    import bench
-    from paper_2601_04904_b200 import plan_partitions
+def test_host_windows_cover_pattern(n, parts):
+    """HostWindow (per-rank pinned host storage of the N>1 end-to-end path):
+    the blocks the ranks own partition the pattern exactly, every window
+    holds its partition's couplings plus every partition separator, and the
+    descriptor addresses blocks by global index."""
+    from paper_2601_04904_b200 import HostWindow, plan_partitions
     plan = plan_partitions(n, parts, "siq")
-    owned = {k: [] for k in ("diag", "arrow_row", "arrow_col", "lower", "upper")}
+    b, a = 2, 1
     seps = [plan.ranges[p][1] - 1 for p in range(parts - 1)]
+    owned = {"diag": [], "lower": []}
     for r in range(parts):
-        ins, outs = bench.rank_slices(plan, r, n)
-        for k, rs in outs.items():
-            for s, e in rs:
-                owned[k].extend(range(s, e))
         lo, hi = plan.ranges[r]
-        need_off = set(range(max(lo - 1, 0), min(hi, n - 1))) | set(seps)
-        have_off = {g for s, e in ins["lower"] for g in range(s, e)}
-        assert need_off <= have_off
-        assert {g for s, e in ins["diag"] for g in range(s, e)} == set(range(lo, hi))
-    for k in ("diag", "arrow_row", "arrow_col"):
-        assert sorted(owned[k]) == list(range(n))
-    for k in ("lower", "upper"):
-        assert sorted(owned[k]) == list(range(n - 1))
+        w = HostWindow(n, b, a, lo, hi, seps)
+        owned["diag"].extend(range(lo, hi))
+        owned["lower"].extend(range(lo, min(hi, n - 1)))
+        for g in seps:
+            lw, up = w.separator(g)
+            assert lw.shape == (b, b) and up.shape == (b, b)
+        d = w.desc()
+        per = b * b * 16
+        assert d.n == n and d.diag + lo * per == w.diag.data_ptr()
+        if min(hi, n - 1) > lo:
+            assert d.lower + lo * per == w.lower.data_ptr()
+            assert d.upper + (min(hi, n - 1) - 1) * per == w.upper[-1].data_ptr()
+        assert d.arrow_row + (hi - 1) * a * b * 16 == w.arrow_row[-1].data_ptr()
+    assert sorted(owned["diag"]) == list(range(n))
+    assert sorted(owned["lower"]) == list(range(n - 1))

@@ -47,7 +47,26 @@ def _rank(rank, world, port, n, b, a, q):
         dB = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=1))
         s = bs.DistSolver(dA, dB, "siq", world, rank, torch.device("cuda", rank))
         s.solve()
-        s.solve()
+        XA, XB = s.solve()
+        # end-to-end path: host windows streamed behind the sweeps, bit-identical
+        lo, hi = s.plan.ranges[rank]
+        c = min(hi, n - 1)
+        ref = [(X.diag[lo:hi].cpu(), X.arrow_row[lo:hi].cpu(), X.lower[lo:c].cpu(), X.upper[lo:c].cpu(),
+                X.tip.cpu()) for X in (XA, XB)]
+        seps = [s.plan.ranges[p][1] - 1 for p in range(world - 1)]
+        win = tuple(bs.HostWindow(n, b, a, lo, hi, seps).fill_from(M) for M in (dA, dB))
+        hout = (bs.HostWindow(n, b, a, lo, hi), bs.HostWindow(n, b, a, lo, hi))
+        dA.diag.zero_()  # prove the streamed path does not read the device inputs' blocks
+        dA.lower.zero_()
+        os.environ["BSEL_STREAM_CHUNK"] = "3"
+        for _ in range(2):
+            s.solve(host_in=win, host_out=hout)
+            torch.cuda.synchronize()
+            for R, H in zip(ref, hout):
+                assert torch.equal(H.diag, R[0]) and torch.equal(H.arrow_row, R[1])
+                assert torch.equal(H.lower, R[2]) and torch.equal(H.upper, R[3])
+                if rank == 0:
+                    assert torch.equal(H.tip, R[4])
         dist.barrier()
         q.put((rank, err, kinds, None))
         dist.destroy_process_group()
