@@ -10,6 +10,8 @@ Public API mirrors btasel/__init__.py for the hot path:
 * distributed solver: dist_solve, local_forward, assemble_reduced,
   solve_reduced, local_backward, plan_partitions, Collectives
 * kernels: OpCounter, block_multiply_acc, mm, block_inverse
+* BTA1 files: read_bta, write_bta, read_bta_header (+ read_bta_device)
+* dense GPU oracle: dense_solve (baselines.py)
 * errors: the reference's exception hierarchy
 
 Every numerical call runs in libbtasel_b200.so (sm_100a); there is no CPU
@@ -17,12 +19,16 @@ fallback.
 """
 
 from .errors import (
+    BadMagicError,
     BtaselError,
     DenseGuardError,
+    FormatError,
     NativeUnavailableError,
     ProtocolError,
     ShapeMismatchError,
+    ShapeInconsistencyError,
     SingularBlockError,
+    TruncatedPayloadError,
     WorkerError,
 )
 from .matrix import BtaMatrix, SelectedSolution, generate_dd_bta, hermitianize, mask_to_pattern, to_dense
@@ -32,9 +38,10 @@ from .device import DeviceBta, generate_dd_bta_device, hermitianize_device, kern
 from .rgf import (RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, default_partitions,
                   release_caches, solve_selected)
 from .collectives import Collectives, LocalHub, TorchCollectives, TraceEvent
-from .dist import (BoundaryPayload, DistSolver, HostWindow, InGpuPartitions, LocalFactors, ReducedSystem, assemble_reduced,
-                   dist_solve,
-                   local_backward, local_forward, solve_reduced)
+from .dist import (BoundaryPayload, DistSolver, HostWindow, InGpuPartitions, LocalFactors, ReducedSystem,
+                   assemble_reduced, dist_solve, local_backward, local_forward, solve_reduced)
+from .fileio import read_bta, read_bta_device, read_bta_header, write_bta
+from .dense import dense_solve
 
 __version__ = "0.1.0"
 
@@ -48,5 +55,6 @@ __all__ = [
     "BoundaryPayload", "LocalFactors", "ReducedSystem", "DistSolver", "HostWindow", "Collectives", "TorchCollectives",
     "LocalHub", "TraceEvent", "generate_dd_bta_device", "hermitianize_device", "kernel_launches",
     "BtaselError", "ShapeMismatchError", "SingularBlockError", "DenseGuardError", "ProtocolError",
-    "WorkerError", "NativeUnavailableError",
+    "WorkerError", "NativeUnavailableError", "FormatError", "BadMagicError", "TruncatedPayloadError",
+    "ShapeInconsistencyError", "read_bta", "write_bta", "read_bta_header", "read_bta_device", "dense_solve",
 ]

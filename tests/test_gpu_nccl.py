@@ -75,7 +75,7 @@ def _rank(rank, world, port, n, b, a, q):
         q.put((rank, None, None, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world,n,b,a", [(2, 16, 64, 16), (2, 9, 40, 0)])
+@pytest.mark.parametrize("world,n,b,a", [(2, 16, 64, 16), (2, 9, 40, 0), (4, 24, 48, 8)])
 def test_nccl_dist_solve_matches_oracle(world, n, b, a):
     world = min(world, torch.cuda.device_count())
     ctx = mp.get_context("spawn")

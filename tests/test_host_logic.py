@@ -177,3 +177,20 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_dense_expansion_and_mask_roundtrip():
+    """dense.py expansion / masking (plain tensor indexing, runs on CPU
+    tensors too) agree with the host to_dense / mask_to_pattern."""
+    import torch
+    from paper_2601_04904_b200 import DeviceBta, generate_dd_bta
+    from paper_2601_04904_b200.dense import dense_device, mask_device
+    from paper_2601_04904_b200.matrix import to_dense
+    for shape in [(4, 3, 2), (1, 2, 0), (3, 1, 4), (2, 5, 0)]:
+        m = generate_dd_bta(*shape, seed=1)
+        d = DeviceBta(*shape, {k: torch.from_numpy(v) for k, v in m.stacked().items()})
+        dd = dense_device(d)
+        assert np.array_equal(dd.numpy(), to_dense(m))
+        back = mask_device(dd, shape)
+        for k, v in m.stacked().items():
+            assert np.array_equal(getattr(back, k).numpy(), v)
