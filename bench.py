@@ -209,6 +209,75 @@ def dist_e2e(args, solver, A, B, n, world, rank, dev, dist):
                     "solution blocks streamed out behind the backward; max over ranks"}
 
 
+def run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist):
+    """Config 5: energy-point sweep, energy parallel across ranks (weak
+    scaling: ``--energies-per-gpu`` energies per GPU per step, no
+    collective).  A step = every rank solves its energies; value = the
+    step's device time (max over ranks) / all energies of the step."""
+    import torch
+
+    import paper_2601_04904_b200 as bs
+
+    E = args.energies_per_gpu
+    sweep = bs.EnergySweep(n, b, a, "siq", device=dev)
+    mine = list(range(rank * E, (rank + 1) * E))  # energies of this rank (round robin over 64 = same set)
+
+    def step():
+        sweep.run(mine)
+
+    t0 = time.perf_counter()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    warm_s = time.perf_counter() - t0
+    launches0 = bs.kernel_launches()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            step()
+        end.record()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    ms = start.elapsed_time(end) / args.steps
+    launches = (bs.kernel_launches() - launches0) // args.steps
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        total_e = E * world
+        per = ms / total_e
+        F = flops_seq(n, b, a)
+        peak, peak_src = fp64_peak_tflops()
+        tf = F * total_e / (ms * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": per, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (device splitmix64 generator; energy e = seeds (2e, 2e+1))",
+            "config": {"workload": f"cfg5: BASELINE.json configs[{cfg_idx}]", "n_blocks": n, "block": b, "tip": a,
+                       "mode": "siq", "energies_per_gpu": E, "energies_per_step": total_e,
+                       "parallelism": f"energy parallel over {world} GPU(s), 2 in-GPU partitions per energy",
+                       "l2": "inputs 28 GiB per energy >> L2"},
+            "fp64_tflops_step": tf, "pct_fp64_peak_step": 100.0 * tf / (peak * world), "flops_per_energy": F,
+            "roofline": {"bound": "tensor", "kernel": "whole step (DMMA GEMMs + inverses)",
+                         "achieved": tf / world, "peak": peak, "unit": "TFLOP/s", "frac": tf / world / peak,
+                         "traffic": None, "peak_source": peak_src},
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "e2e": None, "e2e_note": "cfg5 inputs are generated on the device per energy (28 GiB each); "
+                                    "host-resident energy sets are out of scope of this mode",
+            "cpu_baseline": None, "warmup_s": warm_s,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -223,6 +292,8 @@ def main():
     ap.add_argument("--partitions", type=int, default=None,
                     help="N=1: in-GPU partitions of solve_selected (default: library default)")
     ap.add_argument("--no-seq", action="store_true", help="skip the extra sequential-RGF measurement")
+    ap.add_argument("--energies-per-gpu", type=int, default=8,
+                    help="cfg5: energy points per GPU per step (64 energies on 8 GPUs)")
     args = ap.parse_args()
     n, b, a, cfg_idx = WORKLOADS[args.workload]
     if args.n:
@@ -246,6 +317,9 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
         from paper_2601_04904_b200 import dist as bdist
+
+    if args.workload == "cfg5":
+        return run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist)
 
     # ---- inputs, generated on device --------------------------------------
     t_gen = time.perf_counter()

@@ -93,17 +93,23 @@ def to_host(d: DeviceBta, *, pinned=False) -> BtaMatrix:
     return out
 
 
-def generate_dd_bta_device(n, b, a, seed, dominance=1.5, device=None) -> DeviceBta:
+def generate_dd_bta_device(n, b, a, seed, dominance=1.5, device=None, *, out=None) -> DeviceBta:
     """generate_dd_bta (matrix.py:224-284) computed on the GPU: the same
     splitmix64 stream bit for bit; the dominance shift's |row| sums are
     accumulated sequentially (host: numpy pairwise), so shifted diagonal
-    entries may differ from the host generator in the last bit."""
+    entries may differ from the host generator in the last bit.  ``out``:
+    an existing DeviceBta of the shape to overwrite (on the current stream)."""
     import ctypes
 
     if n < 1 or b < 1 or a < 0:
         raise ValueError(f"invalid shape parameters (n={n}, b={b}, a={a})")
+    if out is not None:
+        if out.shape_params != (n, b, a):
+            raise ShapeMismatchError("out has a different shape")
+        device = out.device
     ctx = _native.Context.get(None if device is None else torch.device(device).index)
-    out = DeviceBta.empty(n, b, a, torch.device("cuda", ctx.device), zero=False)
+    if out is None:
+        out = DeviceBta.empty(n, b, a, torch.device("cuda", ctx.device), zero=False)
     d = out.desc()
     ctx.bind_stream()
     ctx.call("bsel_generate_dd_bta", ctypes.byref(d), int(seed) & 0xFFFFFFFFFFFFFFFF, float(dominance))

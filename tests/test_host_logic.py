@@ -194,3 +194,12 @@ def test_dense_expansion_and_mask_roundtrip():
         back = mask_device(dd, shape)
         for k, v in m.stacked().items():
             assert np.array_equal(getattr(back, k).numpy(), v)
+
+
+def test_energy_assignment():
+    from paper_2601_04904_b200 import energy_seeds, rank_energies
+    assert energy_seeds(0) == (0, 1) and energy_seeds(5) == (10, 11)
+    es = list(range(64))
+    parts = [rank_energies(es, 8, r) for r in range(8)]
+    assert sorted(sum(parts, [])) == es and all(len(p) == 8 for p in parts)
+    assert rank_energies(range(3), 4, 3) == []
