@@ -29,77 +29,128 @@ __device__ __forceinline__ double2 crecip_fast(double2 z) {
   return make_double2(z.x * r, -z.y * r);
 }
 
-// 32 x 32 Gauss-Jordan with partial pivoting by 256 threads.  Thread t owns
-// row t/8, columns 4*(t%8) .. +3 IN REGISTERS for the whole elimination;
-// per pivot step only the pivot column (for the search and the row
-// multipliers) and the pivot row go through shared memory (the row buffer is
-// skewed so the 4 reads per thread are conflict-free broadcasts).  Pivot
-// search by every warp: redux.sync on the high word of |re|+|im| (monotone
-// for non-negative doubles), lowest row on ties; virtual row interchanges
-// tracked in a register bitmask.  Input in a (rows/cols < n); on return a
-// holds S with inv(A)[r][piv[k]] = S[piv[r]][k].
+// 32 x 32 Gauss-Jordan with partial pivoting by 256 threads, blocked in four
+// sub-panels of 8 columns.  Thread t owns row i = t/8 and the columns
+// t%8 + 8s (one per sub-panel s) IN REGISTERS for the whole elimination.
+// A pivot step only updates the current sub-panel (one complex FMA per
+// thread); the sub-panel is republished to shared memory after every step
+// (double buffered), so pivot column, pivot row and multipliers all come
+// from one buffer and a step needs a single __syncthreads.  After the 8
+// steps of a sub-panel the other 24 columns receive the whole sub-panel at
+// once: with G = G_8..G_1 the sub-panel's elementary transforms and P its
+// pivot rows, x' = zero_rows_P(x) + G[:, P] x[P], and G[:, p_j] is exactly
+// the sub-panel column j after its 8 steps.  Pivot search by every warp:
+// redux.sync on the high word of |re|+|im| (monotone for non-negative
+// doubles), lowest row on ties; virtual row interchanges tracked in a
+// register bitmask.  Input in a (rows/cols < n); on return a holds S with
+// inv(A)[r][piv[k]] = S[piv[r]][k].
+constexpr int kSub = 8;               // sub-panel width
+constexpr int kPanLd = kSub + 1;      // padded: column reads hit 8 distinct bank groups
 struct Leaf32 {
-  double2 a[32][33];  // input, then (after the elimination) the result S
-  double2 col[2][32];
-  double2 row[2][32];
+  double2 a[32][33];                  // input, then (after the elimination) the result S
+  double2 pan[2][32][kPanLd];         // current sub-panel, double buffered
+  double2 prow[kSub][3][kSub];        // pivot rows of the other three sub-panels
   int piv[32];
 };
 
-__device__ __forceinline__ int row_slot(int c) { return (c & 3) * 8 + (c >> 2); }
-
-__device__ bool gj_leaf32(Leaf32& L, int n) {
+__device__ bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
   const int t = threadIdx.x, lane = t & 31;
-  const int i = t >> 3, c0 = (t & 7) * 4;
+  const int i = t >> 3, cl = t & 7;
   double2 v[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    v[q] = (i < n && c0 + q < n) ? L.a[i][c0 + q] : make_double2(0.0, 0.0);
-  if ((t & 7) == 0) L.col[0][i] = v[0];
-  __syncthreads();
+  for (int s = 0; s < 4; ++s) {
+    const int c = cl + kSub * s;
+    v[s] = (i < n && c < n) ? L.a[i][c] : make_double2(0.0, 0.0);
+  }
   unsigned used = 0u;
   bool any_zero = false;
-  for (int k = 0; k < n; ++k) {
-    const int buf = k & 1;
-    const bool cand = lane < n && !((used >> lane) & 1u);
-    const unsigned key = cand ? (unsigned)__double2hiint(cabs1(L.col[buf][lane])) + 1u : 0u;
-    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
-    const unsigned ball = __ballot_sync(0xffffffffu, cand && key == kmax);
-    const int p = __ffs(ball) - 1;
-    const bool zero = kmax <= 1u;  // all candidates zero (or subnormal): let the exact path decide
-    any_zero |= zero;
-    used |= 1u << p;
-    if (t == 0) L.piv[k] = p;
-    if (i == p) {
+  int buf = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) L.row[buf][row_slot(c0 + q)] = v[q];
-    }
-    const double2 inv = zero ? make_double2(1.0, 0.0) : crecip_fast(L.col[buf][p]);
-    const double2 m = cmul(L.col[buf][i], inv);
+  for (int s = 0; s < 4; ++s) {
+    const int k0 = kSub * s;
+    if (k0 >= n) break;
+    if (trace && t == 0) trace[3 * s] = clock64();
+    L.pan[buf][i][cl] = v[s];
     __syncthreads();
-    // pivot row: a'[p][c] = inv * a[p][c]; other rows: a'[i][c] = a[i][c] - m a[p][c];
-    // column k: inv resp. -m.  One complex FMA per entry: a' = base + coef * a[p][c].
-    const bool prow = i == p;
-    const double2 coef = prow ? inv : make_double2(-m.x, -m.y);
+    const int steps = min(kSub, n - k0);
+    int jp = -1;  // this row's step within the sub-panel if it was chosen as a pivot row
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = c0 + q;
-      const double2 pr = L.row[buf][row_slot(c)];
-      const double bx = prow ? 0.0 : v[q].x, by = prow ? 0.0 : v[q].y;
+    for (int j = 0; j < kSub; ++j) {
+      if (j >= steps) break;
+      const int k = k0 + j;
+      const double2 cv = L.pan[buf][lane][j];  // column k, row `lane`
+      const bool cand = lane < n && !((used >> lane) & 1u);
+      const unsigned key = cand ? (unsigned)__double2hiint(cabs1(cv)) + 1u : 0u;
+      // Off the critical path: every lane inverts its own candidate while the
+      // search runs; the pivot's reciprocal is then one shuffle away.
+      const double2 rl = crecip_fast(cv);
+      const double2 ci = make_double2(__shfl_sync(0xffffffffu, cv.x, i), __shfl_sync(0xffffffffu, cv.y, i));
+      const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+      const unsigned ball = __ballot_sync(0xffffffffu, cand && key == kmax);
+      const int p = __ffs(ball) - 1;
+      const bool zero = kmax <= 1u;  // all candidates zero (or subnormal): let the exact path decide
+      any_zero |= zero;
+      used |= 1u << p;
+      if (p == i) jp = j;
+      if (t == 0) L.piv[k] = p;
+      const double2 pr = L.pan[buf][p][cl];
+      const double2 rp = make_double2(__shfl_sync(0xffffffffu, rl.x, p), __shfl_sync(0xffffffffu, rl.y, p));
+      const double2 inv = zero ? make_double2(1.0, 0.0) : rp;
+      const double2 m = cmul(ci, inv);
+      // pivot row: a'[p][c] = inv * a[p][c]; other rows: a'[i][c] = a[i][c] - m a[p][c];
+      // column k: inv resp. -m.  One complex FMA per entry: a' = base + coef * a[p][c].
+      const bool prow_ = i == p;
+      const double2 coef = prow_ ? inv : make_double2(-m.x, -m.y);
+      const double bx = prow_ ? 0.0 : v[s].x, by = prow_ ? 0.0 : v[s].y;
       double2 nv;
       nv.x = fma(coef.x, pr.x, fma(-coef.y, pr.y, bx));
       nv.y = fma(coef.x, pr.y, fma(coef.y, pr.x, by));
-      if (c == k) nv = coef;
-      if (c < n && i < n) v[q] = nv;
+      if (cl == j) nv = coef;
+      if (i < n && cl + k0 < n) v[s] = nv;
+      buf ^= 1;
+      L.pan[buf][i][cl] = v[s];
+      __syncthreads();
     }
-    const int q1 = k + 1 - c0;  // publish column k+1 (static selects keep v[] in registers)
-    if (q1 >= 0 && q1 < 4) L.col[buf ^ 1][i] = q1 == 0 ? v[0] : q1 == 1 ? v[1] : q1 == 2 ? v[2] : v[3];
+    if (trace && t == 0) trace[3 * s + 1] = clock64();
+    // Lazy update of the other sub-panels: x' = zero_rows_P(x) + W x[P].
+    // Unconditional 8-term sums (the loads pipeline): a short last
+    // sub-panel has zero columns in pan and zero-filled pivot rows here.
+    if (steps < kSub) {
+      double2* pf = &L.prow[0][0][0];
+      for (int e = t; e < kSub * 3 * kSub; e += blockDim.x)
+        if (e / (3 * kSub) >= steps) pf[e] = make_double2(0.0, 0.0);
+    }
+    if (jp >= 0) {
+#pragma unroll
+      for (int o = 0, s2 = 0; s2 < 4; ++s2)
+        if (s2 != s) L.prow[jp][o++][cl] = v[s2];
+    }
     __syncthreads();
+    double2 w[kSub];
+#pragma unroll
+    for (int j = 0; j < kSub; ++j) w[j] = L.pan[buf][i][j];
+#pragma unroll
+    for (int o = 0, s2 = 0; s2 < 4; ++s2) {
+      if (s2 == s) continue;
+      double2 acc = jp >= 0 ? make_double2(0.0, 0.0) : v[s2];
+#pragma unroll
+      for (int j = 0; j < kSub; ++j) {
+        const double2 x = L.prow[j][o][cl];
+        acc.x = fma(w[j].x, x.x, fma(-w[j].y, x.y, acc.x));
+        acc.y = fma(w[j].x, x.y, fma(w[j].y, x.x, acc.y));
+      }
+      if (i < n && cl + kSub * s2 < n) v[s2] = acc;
+      ++o;
+    }
+    buf ^= 1;  // next sub-panel starts in the other buffer (the lazy update still read this one)
+    if (trace && t == 0) trace[3 * s + 2] = clock64();
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) L.a[i][c0 + q] = v[q];
+  for (int s = 0; s < 4; ++s) L.a[i][cl + kSub * s] = v[s];
   __syncthreads();
   return any_zero;
 }
+
 
 // One CTA (256 threads) per matrix, n <= 32.
 __global__ void __launch_bounds__(256)
@@ -243,15 +294,35 @@ constexpr int kLeafThreads = 256;
 constexpr int kT = 32;
 constexpr int kTLD = kT + 2;  // 544-byte rows: conflict-free DMMA fragment loads
 
-struct PinvSmem;
+// Operand tiles double buffered: the next tile's loads fly while the
+// current one computes (3 buffers, or the addend tile via smem, measured
+// slower: 1 CTA/SM either way, more bytes in flight per SM).
 struct PinvSmem {
-  double2 d[kT][kTLD];  // Dinv
-  double2 x[kT][kTLD];  // row-panel tile W[J,K] -> R = Dinv W[J,K]
-  double2 c[kT][kTLD];  // column-panel tile W[I,J]
-  double2 r[kT][kTLD];
+  double2 d[kT][kTLD];     // Dinv
+  double2 x[2][kT][kTLD];  // row-panel tiles W[J,K]; R = Dinv W[J,K] is formed from them
+  double2 c[2][kT][kTLD];  // column-panel tiles W[I,J]
+  double2 r[kT][kTLD];     // R of the current column
 };
 
-static_assert(sizeof(Leaf32) <= 2 * sizeof(double2) * kT * kTLD, "leaf scratch must fit in PinvSmem::x and ::c");
+static_assert(sizeof(Leaf32) <= sizeof(PinvSmem::x), "leaf scratch must fit in PinvSmem::x");
+
+__device__ __forceinline__ void inv_cp16(void* smem, const void* gmem, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void inv_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void inv_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Asynchronous (L2, cp.async.cg) load of a kT x kT tile; zero-fill outside rows x cols.
+__device__ __forceinline__ void load_tile_async(double2 (*dst)[kTLD], const double2* src, int64_t ld, int rows,
+                                                int cols) {
+  for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+    const int i = e / kT, j = e % kT;
+    const bool ok = i < rows && j < cols;
+    inv_cp16(&dst[i][j], ok ? src + (int64_t)i * ld + j : src, ok);
+  }
+}
 
 __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 
@@ -338,16 +409,52 @@ struct TileCtx {
   double2* Wn;
   int64_t ldn;
   int r_tk;  // column tile whose R = Dinv W[J,K] is cached in S.r
+  unsigned long long* trace;  // debug (may be null)
 };
 
-// One 32 x 32 output tile of the Gauss-Jordan update of panel p.
-__device__ void gj_tile(PinvSmem& S, TileCtx& T, int t) {
+// Issue the asynchronous operand loads of output tile t into buffer `buf`:
+// the column-panel tile W[I,J] and, at the first tile of a new column K,
+// the row-panel tile W[J,K] that R = Dinv W[J,K] is formed from.
+struct TileIssue {
+  bool has_x;
+  double2 w[4];  // epilogue operands W[I,K] of this thread's outputs (in flight)
+};
+__device__ __forceinline__ TileIssue issue_tile(PinvSmem& S, const TileCtx& T, int t, int buf, int& issued_r_tk) {
   const int tk = t / T.nt, ti = t % T.nt, p = T.p;
   const int i0 = ti * kT, k0 = tk * kT;
   const int ib = min(kT, T.n - i0), kb = min(kT, T.n - k0);
-  double acc[4][2];
+  TileIssue is;
+  is.has_x = false;
+  // Epilogue operands first: their L2 latency overlaps everything until the
+  // tile's DMMA is done.
+  const bool addend = ti != p && tk != p;
+  const int orow = acc_row();
+#pragma unroll
+  for (int jn = 0; jn < 4; ++jn) {
+    const int oc = acc_col(jn);
+    is.w[jn] = (addend && orow < ib && oc < kb) ? ldcg2(T.Wc + (int64_t)(i0 + orow) * T.ldc + k0 + oc)
+                                                : make_double2(0.0, 0.0);
+  }
+  if (!(ti == p && tk == p)) {
+    if (tk != p && tk != issued_r_tk) {
+      load_tile_async(S.x[buf], T.Wc + (int64_t)T.j0 * T.ldc + k0, T.ldc, T.jb, kb);
+      is.has_x = true;
+      issued_r_tk = tk;
+    }
+    if (ti != p) load_tile_async(S.c[buf], T.Wc + (int64_t)i0 * T.ldc + T.j0, T.ldc, ib, T.jb);
+  }
+  inv_cp_commit();
+  return is;
+}
+
+// Compute output tile t from buffer `buf` (its loads have landed).
+__device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int buf, const TileIssue& is) {
+  const int tk = t / T.nt, ti = t % T.nt, p = T.p;
+  const int i0 = ti * kT, k0 = tk * kT;
+  const int ib = min(kT, T.n - i0), kb = min(kT, T.n - k0);
   double2* out = T.Wn + (int64_t)i0 * T.ldn + k0;
   const int orow = acc_row();
+  double acc[4][2];
   if (ti == p && tk == p) {
     for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
       const int i = e >> 5, j = e & 31;
@@ -355,11 +462,9 @@ __device__ void gj_tile(PinvSmem& S, TileCtx& T, int t) {
     }
     return;
   }
-  if (tk != p && T.r_tk != tk) {  // R = Dinv . W[J,K]
-    __syncthreads();
-    load_tile(S.x, T.Wc + (int64_t)T.j0 * T.ldc + k0, T.ldc, T.jb, kb);
-    __syncthreads();
-    tile_mma(acc, S.d, S.x);
+  if (is.has_x) {  // R = Dinv . W[J,K]
+    tile_mma(acc, S.d, S.x[buf]);
+    __syncthreads();  // previous readers of S.r are done
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) S.r[orow][acc_col(jn)] = make_double2(acc[jn][0], acc[jn][1]);
     __syncthreads();
@@ -372,22 +477,64 @@ __device__ void gj_tile(PinvSmem& S, TileCtx& T, int t) {
     }
     return;
   }
-  __syncthreads();
-  load_tile(S.c, T.Wc + (int64_t)i0 * T.ldc + T.j0, T.ldc, ib, T.jb);
-  __syncthreads();
-  tile_mma(acc, S.c, tk == p ? S.d : S.r);
+  tile_mma(acc, S.c[buf], tk == p ? S.d : S.r);
 #pragma unroll
   for (int jn = 0; jn < 4; ++jn) {
     const int oc = acc_col(jn);
-    if (orow < ib && oc < kb) {
-      double2 v = make_double2(-acc[jn][0], -acc[jn][1]);
-      if (tk != p) {
-        const double2 w = ldcg2(T.Wc + (int64_t)(i0 + orow) * T.ldc + k0 + oc);
-        v.x += w.x;
-        v.y += w.y;
-      }
-      out[(int64_t)orow * T.ldn + oc] = v;
-    }
+    if (orow < ib && oc < kb) out[(int64_t)orow * T.ldn + oc] = make_double2(is.w[jn].x - acc[jn][0], is.w[jn].y - acc[jn][1]);
+  }
+
+}
+
+// Output tiles [t0, t1) of the Gauss-Jordan update of panel p (tile `skip`
+// excluded), software pipelined: the operands of the next tile stream in
+// (cp.async, double buffered) while the current one computes.
+// One pipeline stage: wait for tile t's operands (slot B), start tile tn's
+// loads into slot B ^ 1, compute t.  B is a template constant so the two
+// in-flight TileIssue register sets never have to be copied (a copy would
+// wait for the in-flight epilogue loads).
+template <int B>
+__device__ __forceinline__ void gj_stage(PinvSmem& S, TileCtx& T, int t, int tn, int t1, int t0,
+                                         const TileIssue& cur, TileIssue& nxt, int& issued_r_tk) {
+  if (tn < t1) {
+    nxt = issue_tile(S, T, tn, B ^ 1, issued_r_tk);
+    inv_cp_wait<1>();
+  } else {
+    inv_cp_wait<0>();
+  }
+  __syncthreads();
+  const bool tr = T.trace && blockIdx.x == 1 && threadIdx.x == 0 && t == t0;  // debug stamps
+  unsigned long long g0 = 0, g1 = 0;
+  if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  compute_tile(S, T, t, B, cur);
+  __syncthreads();  // slot B is refilled by the next stage's issue
+  if (tr) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    T.trace[8 * T.p + 6] = g0, T.trace[8 * T.p + 7] = g1;
+  }
+}
+
+// Output tiles [t0, t1) of the Gauss-Jordan update of panel p (tile `skip`
+// excluded), software pipelined: the operands of the next tile stream in
+// (cp.async, double buffered) while the current one computes.
+__device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
+  auto next = [&](int t) { ++t; return t == skip ? t + 1 : t; };
+  int t = t0 == skip ? t0 + 1 : t0;
+  if (t >= t1) return;
+  int issued_r_tk = T.r_tk;
+  __syncthreads();  // smem buffers free (previous panel / leaf)
+  TileIssue a, b;
+  a = issue_tile(S, T, t, 0, issued_r_tk);
+  b.has_x = false;
+  while (true) {
+    int tn = next(t);
+    gj_stage<0>(S, T, t, tn, t1, t0, a, b, issued_r_tk);
+    if (tn >= t1) break;
+    t = tn;
+    tn = next(t);
+    gj_stage<1>(S, T, t, tn, t1, t0, b, a, issued_r_tk);
+    if (tn >= t1) break;
+    t = tn;
   }
 }
 
@@ -395,7 +542,10 @@ __device__ void gj_tile(PinvSmem& S, TileCtx& T, int t) {
 // W'[p+1,p+1], immediately factors it and publishes Dinv_{p+1} (double-
 // buffered gD) while the other CTAs update the rest -> one grid barrier per
 // panel, the leaf latency hidden behind the update.
-__global__ void __launch_bounds__(256, 1)
+// launch_bounds(256, 2): <= 128 registers, so an inverse CTA can share an SM
+// with a GEMM CTA of the concurrent sweeps (at 200 registers it needed an SM
+// of its own and the chain waited for GEMM tails to drain).
+__global__ void __launch_bounds__(256, 2)
     persistent_inverse_kernel(const double2* __restrict__ X, int64_t ldx, double2* Y, int64_t ldy, int n,
                               double2* work, double2* gD, unsigned* barrier, int* flag,
                               unsigned long long* trace) {
@@ -411,13 +561,14 @@ __global__ void __launch_bounds__(256, 1)
   };
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
-  Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0]);  // spans x and c
+  Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0][0]);  // spans x[0] and x[1]
   const int nt = (n + kT - 1) / kT, ntiles = nt * nt, G = gridDim.x;
   unsigned target = 0;
   if (blockIdx.x == 0) leaf_publish(L, X, ldx, 0, min(kT, n), gD, flag);
   target += G;
   grid_barrier(barrier, target);
   TileCtx T;
+  T.trace = trace;
   T.n = n;
   T.nt = nt;
   T.Wc = X;
@@ -435,7 +586,7 @@ __global__ void __launch_bounds__(256, 1)
     const int sp = (p + 1 < nt) ? (p + 1) * nt + (p + 1) : -1;
     if (blockIdx.x == 0) stamp(8 * p + 0);
     if (blockIdx.x == 0 && sp >= 0) {
-      gj_tile(S, T, sp);
+      gj_tiles(S, T, sp, sp + 1, -1);
       __syncthreads();
       stamp(8 * p + 1);
       leaf_publish(L, T.Wn, T.ldn, (p + 1) * kT, min(kT, n - (p + 1) * kT), gD + ((p + 1) & 1) * kT * kT, flag);
@@ -444,8 +595,7 @@ __global__ void __launch_bounds__(256, 1)
     if (G == 1 || blockIdx.x > 0) {
       const int chunk = (ntiles + workers - 1) / workers;
       const int t0 = wid * chunk, t1 = min(ntiles, t0 + chunk);
-      for (int t = t0; t < t1; ++t)
-        if (t != sp || G == 1) gj_tile(S, T, t);
+      gj_tiles(S, T, t0, t1, G == 1 ? -1 : sp);
     }
     if (blockIdx.x == 0) stamp(8 * p + 3);
     if (blockIdx.x == 1) stamp(8 * p + 4);

@@ -91,8 +91,8 @@ int main() {
       unsigned long long t0 = h[0];
       for (int p = 0; p < nt; ++p) {
         auto d = [&](int k) { return h[8 * p + k] ? (double)(h[8 * p + k] - t0) / 1e3 : -1.0; };
-        printf("panel %2d: cta0 start %7.2f  tile %7.2f  leaf %7.2f  atbar %7.2f | cta1 done %7.2f  past-bar %7.2f us\n",
-               p, d(0), d(1), d(2), d(3), d(4), d(5));
+        printf("panel %2d: cta0 start %7.2f  tile %7.2f  leaf %7.2f  atbar %7.2f | cta1 first-tile %7.2f..%7.2f done %7.2f  past-bar %7.2f us\n",
+               p, d(0), d(1), d(2), d(3), d(6), d(7), d(4), d(5));
       }
     }
     cudaFree(X); cudaFree(Y); cudaFree(W); cudaFree(flag);
