@@ -208,6 +208,10 @@ typedef struct {
   double inverse_ms;     /* sum of their CUDA-event durations              */
   double gemm_bytes;     /* compulsory bytes of the GEMM launches: every  */
                          /* operand read once, outputs written once       */
+  double gemm_busy_ms;   /* union of the GEMM launches' [start, end] spans */
+                         /* (launches on concurrent streams overlap)      */
+  double inverse_busy_ms;/* union of the inverses' spans                   */
+  double inverse_flops;  /* sum of 8*n^3 over the inverses                 */
 } bsel_profile_t;
 /* Bracket every launch with CUDA events on its stream until _end (which
  * synchronizes the device and returns the totals).                        */

@@ -135,6 +135,9 @@ class Profile(ctypes.Structure):
         ("inverse_calls", ctypes.c_int64),
         ("inverse_ms", ctypes.c_double),
         ("gemm_bytes", ctypes.c_double),
+        ("gemm_busy_ms", ctypes.c_double),
+        ("inverse_busy_ms", ctypes.c_double),
+        ("inverse_flops", ctypes.c_double),
     ]
 
 

@@ -546,6 +546,9 @@ int bsel_profile_end(bsel_profile_t* out) {
     out->inverse_calls = t.inverse_calls;
     out->inverse_ms = t.inverse_ms;
     out->gemm_bytes = t.gemm_bytes;
+    out->gemm_busy_ms = t.gemm_busy_ms;
+    out->inverse_busy_ms = t.inverse_busy_ms;
+    out->inverse_flops = t.inverse_flops;
   }
   return BSEL_OK;
 }

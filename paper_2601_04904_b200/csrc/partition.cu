@@ -249,9 +249,10 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
   const bool fused = F.fused;
   if (fused && (!B || !WB || !ZR || !XB)) throw ShapeError("fused factors require the right-hand side");
   const int mx = (int)std::max(a, b);
-  ctx.reserve_slots(64, (int64_t)mx * mx);
+  ctx.reserve_slots(back_sweep_slots(), (int64_t)mx * mx);
   cudaStream_t s = ctx.stream();
   cuda_check(cudaEventRecord(ctx.timer(2), s), "timer");
+  BackSweep sweep(ctx, kTileAutoWide);
   // End-to-end mode: move each chunk of finished outputs to the host on the
   // copy stream while the sweep continues.
   const bool streamed = io && io->hxa && io->chunk > 0;
@@ -260,6 +261,7 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
   int64_t sent = 0;  // chunks queued
   auto send = [&](int64_t steps, bool final) {  // backward steps [0, steps) are complete
     if (!streamed) return;
+    sweep.fence();
     while (sent < n_out && (final || (sent + 1) * C <= steps) && (final || sent < n_out - 1)) {
       cudaEvent_t ev = ctx.xfer_event((int)sent);
       cuda_check(cudaEventRecord(ev, s), "chunk record");
@@ -315,14 +317,13 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       seed(k_top, lo);
     }
     L.flush();
-    BackPipe pipe(ctx);
+    sweep.begin();
     for (int64_t t = 0; t < len - 1; ++t) {
       const int64_t i = down ? hi - 2 - t : lo + 1 + t;
       const int64_t p = down ? i + 1 : i - 1;  // previously solved neighbour
       const int64_t e = down ? i : i - 1;
       BackStep st;
       st.k = 2;
-      st.late[0][0] = true;
       st.g = F.SA(i - lo);
       st.rs[0] = down ? A.U(e) : A.L(e), st.rs[1] = el(WA, i, false);
       st.qs[0] = down ? A.L(e) : A.U(e), st.qs[1] = el(WA, i, true);
@@ -339,13 +340,8 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
         st.zcol[0] = down ? XB->L(e) : XB->U(e), st.zcol[1] = XB->AR(i);
         st.zdiag = XB->D(i);
       }
-      pipe.early(L, st, (int)(t & 1));
-      L.flush();
-      pipe.rest(L, st, (int)(t & 1));
-      if (streamed && (t + 1) % C == 0) {
-        L.flush();
-        send(t + 1, false);
-      }
+      sweep.step(st);
+      if (streamed && (t + 1) % C == 0) send(t + 1, false);
     }
   } else {
     seed(k_top, lo);
@@ -363,13 +359,11 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       }
     }
     L.flush();
-    BackPipe pipe(ctx);
+    sweep.begin();
     for (int64_t i = hi - 2; i > lo; --i) {
-      const int q = (int)((hi - 2 - i) & 1);
       const bool last_step = i == lo + 1;
       BackStep st;
       st.k = 3;
-      st.late[1][1] = true;
       st.g = F.SA(i - lo);
       st.rs[0] = F.FC(i - lo), st.rs[1] = A.U(i), st.rs[2] = el(WA, i, false);
       st.qs[0] = F.FR(i - lo), st.qs[1] = A.L(i), st.qs[2] = el(WA, i, true);
@@ -377,9 +371,8 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       st.ya[0][0] = y00, st.ya[0][1] = yfr, st.ya[0][2] = y0t;
       st.ya[1][0] = yfc, st.ya[1][1] = XA.D(i + 1), st.ya[1][2] = XA.AC(i + 1);
       st.ya[2][0] = yt0, st.ya[2][1] = XA.AR(i + 1), st.ya[2][2] = ytt;
-      // row[0] = X(i, lo), col[0] = X(lo, i): carried to the next step (ping-pong slots).
-      st.row[0] = last_step ? XA.L(lo) : ctx.tmp(2 * q + 1, (int)b, (int)b);
-      st.col[0] = last_step ? XA.U(lo) : ctx.tmp(2 * q, (int)b, (int)b);
+      // row[0] = X(i, lo), col[0] = X(lo, i): carried to the next step (ring-allocated).
+      if (last_step) st.row[0] = XA.L(lo), st.col[0] = XA.U(lo);
       st.row[1] = XA.U(i), st.row[2] = XA.AC(i);
       st.col[1] = XA.L(i), st.col[2] = XA.AR(i);
       st.diag = XA.D(i);
@@ -391,25 +384,20 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
         st.yb[0][0] = z00, st.yb[0][1] = zfr, st.yb[0][2] = z0t;
         st.yb[1][0] = zfc, st.yb[1][1] = XB->D(i + 1), st.yb[1][2] = XB->AC(i + 1);
         st.yb[2][0] = zt0, st.yb[2][1] = XB->AR(i + 1), st.yb[2][2] = ztt;
-        st.zrow[0] = last_step ? XB->L(lo) : ctx.tmp(4 + 2 * q + 1, (int)b, (int)b);
-        st.zcol[0] = last_step ? XB->U(lo) : ctx.tmp(4 + 2 * q, (int)b, (int)b);
+        if (last_step) st.zrow[0] = XB->L(lo), st.zcol[0] = XB->U(lo);
         st.zrow[1] = XB->U(i), st.zrow[2] = XB->AC(i);
         st.zcol[1] = XB->L(i), st.zcol[2] = XB->AR(i);
         st.zdiag = XB->D(i);
       }
-      pipe.early(L, st, q);
-      L.flush();
-      pipe.rest(L, st, q);
+      sweep.step(st);
       const int64_t t = hi - 2 - i;
-      if (streamed && (t + 1) % C == 0) {
-        L.flush();
-        send(t + 1, false);
-      }
+      if (streamed && (t + 1) % C == 0) send(t + 1, false);
       yfr = st.col[0], yfc = st.row[0];
       if (fused) zfr = st.zcol[0], zfc = st.zrow[0];
     }
   }
   L.flush();
+  sweep.end();
   send(len - 1, true);
   cuda_check(cudaEventRecord(ctx.timer(3), s), "timer");
 }

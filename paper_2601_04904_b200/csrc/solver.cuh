@@ -70,6 +70,9 @@ class Context {
   // inverse -> elimination factors -> next pivot); its CTAs are scheduled
   // ahead of the aux stream's throughput work as SMs free up.
   cudaStream_t chain() const { return chain_; }
+  // Low-priority stream for work that runs ahead of both chains (the
+  // backward sweep's per-step prologue).
+  cudaStream_t side() const { return side_; }
   int device() const { return device_; }
 
   // Scratch: `count` temporaries of (r x c) complex, grow-only.
@@ -88,7 +91,9 @@ class Context {
   // a pool of ordering events for them (created on first use).
   cudaStream_t xfer();
   cudaEvent_t xfer_event(int i);
-  // Events for cross-stream ordering.
+  // Events for cross-stream ordering: 0..15 fork/join and the forward ring,
+  // kBackEvents.. the backward sweep's ring.
+  static constexpr int kBackEvents = 16;
   cudaEvent_t event(int i);
   cudaEvent_t timer(int i);
 
@@ -99,6 +104,7 @@ class Context {
   cudaStream_t user_stream_ = nullptr;
   cudaStream_t aux_ = nullptr;
   cudaStream_t chain_ = nullptr;
+  cudaStream_t side_ = nullptr;
   double2* slots_ = nullptr;
   int64_t slot_elems_ = 0;
   int nslots_ = 0;

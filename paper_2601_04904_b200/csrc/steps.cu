@@ -73,7 +73,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     return;
   }
   Mat f = rt(ctx, slot, 0, b, b), g = rt(ctx, slot, 1, a, b), w = rt(ctx, slot, 2, b, b);
-  Mat p = rt(ctx, slot, 3, a, b), k = rt(ctx, slot, 4, b, a), q = rt(ctx, slot, 5, b, b);
+  Mat k = rt(ctx, slot, 4, b, a), q = rt(ctx, slot, 5, b, b);
   {
     Level L(sA);
     L.out(f).mm(+1, st.Lk, N, S, N);
@@ -82,26 +82,30 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     L.out(st.ad_j).add(+1, st.ad_j).mm(-1, f, N, st.Uk, N);
     L.flush();
   }
-  // Aux: A-side arrow/tip updates and the B side in three levels.  v Lk^H =
-  // Lk S_B Lk^H = f (Bd f^H) = f q removes the reference's serial chain
-  // w -> S_B -> v -> Bd (same product count).
+  // Aux: A-side arrow/tip updates and the B side in three levels.  The
+  // reference's quadratic updates (rgf.py:257-280) are re-associated so each
+  // output is two products: with q = Bd f^H - BU and k = Bd g^H - BC_i,
+  //   v Lk^H - BL f^H - f BU        = f q - BL f^H        (v = Lk S_B)
+  //   -g BU + p f^H - BR_i f^H      = g q - BR_i f^H      (p = g Bd)
+  //   -f BC_i - BL g^H + f (Bd g^H) = f k - BL g^H
+  //   -g BC_i - BR_i g^H + p g^H    = g k - BR_i g^H
+  // which also removes the reference's serial chain w -> S_B -> v -> Bd.
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
   Level L(sB);
   L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(w).mm(+1, S, N, st.bd_i, N);
-  L.out(q).mm(+1, st.bd_i, N, f, H);
+  L.out(q).add(-1, st.BU).mm(+1, st.bd_i, N, f, H);
   L.out(st.ac_j).add(+1, st.ac_j).mm(-1, f, N, st.ac_i, N);
   L.flush();
   L.out(st.ar_j).add(+1, st.ar_j).mm(-1, g, N, st.Uk, N);
   L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
-  L.out(p).mm(+1, g, N, st.bd_i, N);
-  L.out(k).mm(+1, st.bd_i, N, g, H);
+  L.out(k).add(-1, st.bc_i).mm(+1, st.bd_i, N, g, H);
   L.out(st.sb).mm(+1, w, N, S, H);
-  L.out(st.bd_j).add(+1, st.bd_j).mm(+1, f, N, q, N).mm(-1, st.BL, N, f, H).mm(-1, f, N, st.BU, N);
+  L.out(st.bd_j).add(+1, st.bd_j).mm(+1, f, N, q, N).mm(-1, st.BL, N, f, H);
+  L.out(st.br_j).add(+1, st.br_j).mm(+1, g, N, q, N).mm(-1, st.br_i, N, f, H);
   L.flush();
-  L.out(st.br_j).add(+1, st.br_j).mm(-1, g, N, st.BU, N).mm(+1, p, N, f, H).mm(-1, st.br_i, N, f, H);
-  L.out(st.bc_j).add(+1, st.bc_j).mm(-1, f, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, f, N, k, N);
-  L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
+  L.out(st.bc_j).add(+1, st.bc_j).mm(+1, f, N, k, N).mm(-1, st.BL, N, g, H);
+  L.out(st.tipB).add(+1, st.tipB).mm(+1, g, N, k, N).mm(-1, st.br_i, N, g, H);
   L.flush();
   cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
 }
@@ -128,14 +132,15 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(st.nfill_c).mm(-1, fn, N, st.fill_c, N);
   L.out(st.ac_n).add(+1, st.ac_n).mm(-1, fn, N, st.ac_i, N);
-  Mat w, qn, qr, p, kk;
+  Mat w, qn, qr, kk;
   if (fused) {
-    // v_n = L S_B, v_0 = fill_r S_B enter only as v_x y^H = f_x (Bd f_y^H):
-    // two levels instead of the reference's w -> S_B -> v -> update chain.
+    // Re-associated quadratic updates (see end_step): with
+    //   qn = Bd fn^H - BU, qr = Bd fr^H - BFC, kk = Bd g^H - BC_i
+    // every B-side output of dist.py:360-396 is two products.
     w = rt(ctx, slot, 3, b, b), qn = rt(ctx, slot, 4, b, b), qr = rt(ctx, slot, 5, b, b);
-    p = rt(ctx, slot, 6, a, b), kk = rt(ctx, slot, 7, b, a);
+    kk = rt(ctx, slot, 7, b, a);
     L.out(w).mm(+1, S, N, st.bd_i, N);
-    L.out(qn).mm(+1, st.bd_i, N, fn, H);
+    L.out(qn).add(-1, st.BU).mm(+1, st.bd_i, N, fn, H);
   }
   L.flush();
   L.out(st.nfill_r).mm(-1, fr, N, st.U, N);
@@ -149,138 +154,154 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
     return;
   }
-  L.out(p).mm(+1, g, N, st.bd_i, N);
-  L.out(qr).mm(+1, st.bd_i, N, fr, H);
-  L.out(kk).mm(+1, st.bd_i, N, g, H);
+  L.out(qr).add(-1, st.bfill_c).mm(+1, st.bd_i, N, fr, H);
+  L.out(kk).add(-1, st.bc_i).mm(+1, st.bd_i, N, g, H);
   L.out(st.sb).mm(+1, w, N, S, H);
-  L.out(st.bd_n).add(+1, st.bd_n).mm(-1, fn, N, st.BU, N).mm(-1, st.BL, N, fn, H).mm(+1, fn, N, qn, N);
+  L.out(st.bd_n).add(+1, st.bd_n).mm(+1, fn, N, qn, N).mm(-1, st.BL, N, fn, H);
+  L.out(st.br_n).add(+1, st.br_n).mm(+1, g, N, qn, N).mm(-1, st.br_i, N, fn, H);
+  L.out(st.nbfill_r).mm(+1, fr, N, qn, N).mm(-1, st.bfill_r, N, fn, H);
   L.flush();
-  L.out(st.br_n).add(+1, st.br_n).mm(-1, g, N, st.BU, N).mm(-1, st.br_i, N, fn, H).mm(+1, p, N, fn, H);
-  L.out(st.br_lo).add(+1, st.br_lo).mm(-1, g, N, st.bfill_c, N).mm(-1, st.br_i, N, fr, H).mm(+1, p, N, fr, H);
-  L.out(st.tipB).add(+1, st.tipB).mm(-1, g, N, st.bc_i, N).mm(-1, st.br_i, N, g, H).mm(+1, p, N, g, H);
-  L.out(st.nbfill_c).mm(-1, fn, N, st.bfill_c, N).mm(-1, st.BL, N, fr, H).mm(+1, fn, N, qr, N);
-  L.out(st.nbfill_r).mm(-1, fr, N, st.BU, N).mm(-1, st.bfill_r, N, fn, H).mm(+1, fr, N, qn, N);
-  L.out(st.bd_lo).add(+1, st.bd_lo).mm(-1, fr, N, st.bfill_c, N).mm(-1, st.bfill_r, N, fr, H).mm(+1, fr, N, qr, N);
-  L.out(st.bc_n).add(+1, st.bc_n).mm(-1, fn, N, st.bc_i, N).mm(-1, st.BL, N, g, H).mm(+1, fn, N, kk, N);
-  L.out(st.bc_lo).add(+1, st.bc_lo).mm(-1, fr, N, st.bc_i, N).mm(-1, st.bfill_r, N, g, H).mm(+1, fr, N, kk, N);
+  L.out(st.br_lo).add(+1, st.br_lo).mm(+1, g, N, qr, N).mm(-1, st.br_i, N, fr, H);
+  L.out(st.tipB).add(+1, st.tipB).mm(+1, g, N, kk, N).mm(-1, st.br_i, N, g, H);
+  L.out(st.nbfill_c).mm(+1, fn, N, qr, N).mm(-1, st.BL, N, fr, H);
+  L.out(st.bd_lo).add(+1, st.bd_lo).mm(+1, fr, N, qr, N).mm(-1, st.bfill_r, N, fr, H);
+  L.out(st.bc_n).add(+1, st.bc_n).mm(+1, fn, N, kk, N).mm(-1, st.BL, N, g, H);
+  L.out(st.bc_lo).add(+1, st.bc_lo).mm(+1, fr, N, kk, N).mm(-1, st.bfill_r, N, g, H);
   L.flush();
   cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
 }
 
+// ---------------------------------------------------------------------------
+// Backward sweep engine (see steps.cuh for the re-associated step).
+// Ring slot r = t % kBackDepth holds step t's prologue temporaries and the
+// outputs the caller left empty; its events: pre done, X_A level 1 done,
+// X_B done.  The prologue of step t (side stream) reuses the slot of step
+// t - kBackDepth, whose blocks are last read by X_B(t - kBackDepth + 1)
+// (carried couplings of a middle partition), so it waits for that step.
+// ---------------------------------------------------------------------------
 namespace {
-constexpr int kBackSlots = 24;  // per parity half
-bool any_late_col(const BackStep& st, int j) {  // ya[l][j] for some l
-  for (int l = 0; l < st.k; ++l)
-    if (st.late[l][j]) return true;
-  return false;
+constexpr int kBackRingBase = 16;  // slots 0..15 stay free for the callers' prologues
+constexpr int kBackPerStep = 16;   // h, c, e, f (3 each) + 4 ring-allocated outputs
+cudaEvent_t ev_pre(Context& ctx, int64_t t) { return ctx.event(Context::kBackEvents + (int)(t % kBackDepth)); }
+cudaEvent_t ev_a1(Context& ctx, int64_t t) {
+  return ctx.event(Context::kBackEvents + kBackDepth + (int)(t % kBackDepth));
 }
-bool any_late_row(const BackStep& st, int j) {  // ya[j][l] for some l
-  for (int l = 0; l < st.k; ++l)
-    if (st.late[j][l]) return true;
-  return false;
+cudaEvent_t ev_b(Context& ctx, int64_t t) {
+  return ctx.event(Context::kBackEvents + 2 * kBackDepth + (int)(t % kBackDepth));
 }
+cudaEvent_t ev_fork(Context& ctx) { return ctx.event(Context::kBackEvents + 3 * kBackDepth); }
+cudaEvent_t ev_join(Context& ctx, int i) { return ctx.event(Context::kBackEvents + 3 * kBackDepth + 1 + i); }
+static_assert(Context::kBackEvents + 3 * kBackDepth + 3 <= 64, "event pool");
 }  // namespace
 
-// L1 of one step: the problems that only read inputs and trailing blocks.
-// `late_pass` selects which half is emitted.
-static void back_l1(Context& ctx, Level& L, const BackStep& st, int parity, bool late_pass, Mat* RA, Mat* CA,
-                    Mat* RZ, Mat* CZ, Mat* e, Mat* f) {
+int back_sweep_slots() { return kBackRingBase + kBackPerStep * kBackDepth; }
+
+BackSweep::BackSweep(Context& ctx, int tile_cfg) : ctx_(ctx), cfg_(tile_cfg) {}
+
+Mat BackSweep::ring(int64_t t, int k, int r, int c) {
+  return ctx_.tmp(kBackRingBase + (int)(t % kBackDepth) * kBackPerStep + k, r, c);
+}
+
+void BackSweep::begin() {
+  cuda_check(cudaEventRecord(ev_fork(ctx_), ctx_.stream()), "back fork");
+  for (cudaStream_t s : {ctx_.side(), ctx_.chain(), ctx_.aux()})
+    cuda_check(cudaStreamWaitEvent(s, ev_fork(ctx_), 0), "back fork wait");
+}
+
+void BackSweep::fence() {
+  // X_B(t) follows X_A level 1 (t), the prologue precedes both; the chain's
+  // last diagonal block is joined separately.
+  cuda_check(cudaEventRecord(ev_join(ctx_, 0), ctx_.aux()), "back join");
+  cuda_check(cudaEventRecord(ev_join(ctx_, 1), ctx_.chain()), "back join");
+  cuda_check(cudaStreamWaitEvent(ctx_.stream(), ev_join(ctx_, 0), 0), "back join wait");
+  cuda_check(cudaStreamWaitEvent(ctx_.stream(), ev_join(ctx_, 1), 0), "back join wait");
+}
+
+void BackSweep::step(BackStep& st) {
+  const int64_t t = t_++;
   const int k = st.k, b = st.g.r;
   const bool fused = st.sc.p != nullptr;
-  const int base = kBackBase + parity * kBackSlots;
+  if (k < 1 || k > 3) throw ShapeError("back step needs 1..3 couplings");
+  // Ring-allocate the outputs the caller left empty.
+  int spare = 12;
+  auto own = [&](Mat& m, int r, int c) {
+    if (m.p) return;
+    if (spare == kBackPerStep) throw ShapeError("too many ring-allocated back-step outputs");
+    m = ring(t, spare++, r, c);
+  };
   for (int j = 0; j < k; ++j) {
     const int dj = st.rs[j].c;
-    RA[j] = ctx.tmp(base + 6 * j + 0, b, dj);
-    CA[j] = ctx.tmp(base + 6 * j + 1, dj, b);
-    if (any_late_col(st, j) == late_pass) {
-      L.out(RA[j]);
-      for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, st.ya[l][j], N);
-    }
-    if (any_late_row(st, j) == late_pass) {
-      L.out(CA[j]);
-      for (int l = 0; l < k; ++l) L.mm(+1, st.ya[j][l], N, st.qs[l], N);
-    }
-    if (!fused) continue;
-    RZ[j] = ctx.tmp(base + 6 * j + 2, b, dj);
-    CZ[j] = ctx.tmp(base + 6 * j + 3, dj, b);
-    e[j] = ctx.tmp(base + 6 * j + 4, b, dj);
-    f[j] = ctx.tmp(base + 6 * j + 5, dj, b);
-    if (any_late_col(st, j) == late_pass) {
-      L.out(RZ[j]);
-      for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, st.yb[l][j], N);
-    }
-    if (any_late_row(st, j) == late_pass) {
-      L.out(CZ[j]);
-      for (int l = 0; l < k; ++l) L.mm(+1, st.yb[j][l], N, st.rs[l], H);
-    }
-    if (!late_pass) {
-      L.out(e[j]).mm(+1, st.g, N, st.ss[j], N).mm(-1, st.sc, N, st.qs[j], H);
-      L.out(f[j]).mm(+1, st.ws[j], N, st.g, H).mm(-1, st.qs[j], N, st.sc, N);
-    }
-  }
-}
-
-void BackPipe::early(Level& L, const BackStep& st, int parity) {
-  back_l1(ctx_, L, st, parity, false, RA, CA, RZ, CZ, e, f);
-}
-
-void BackPipe::rest(Level& L, const BackStep& st, int parity) {
-  const int k = st.k, b = st.g.r;
-  const bool fused = st.sc.p != nullptr;
-  back_l1(ctx_, L, st, parity, true, RA, CA, RZ, CZ, e, f);
-  L.flush();
-  // L2: row/column blocks of X_A and X_B, and the quadratic coupling.
-  const int base = kBackBase + parity * kBackSlots + 18;
-  Mat quad = ctx_.tmp(base + 0, b, b);
-  for (int j = 0; j < k; ++j) {
-    L.out(st.row[j]).mm(-1, st.g, N, RA[j], N);
-    L.out(st.col[j]).mm(-1, CA[j], N, st.g, N);
+    own(st.row[j], b, dj);
+    own(st.col[j], dj, b);
     if (fused) {
-      L.out(st.zrow[j]);
-      for (int l = 0; l < k; ++l) L.mm(+1, e[l], N, st.ya[j][l], H);
-      L.mm(-1, st.g, N, RZ[j], N);
-      L.out(st.zcol[j]);
-      for (int l = 0; l < k; ++l) L.mm(+1, st.ya[j][l], N, f[l], N);
-      L.mm(-1, CZ[j], N, st.g, H);
+      own(st.zrow[j], b, dj);
+      own(st.zcol[j], dj, b);
     }
   }
-  if (fused) {
-    L.out(quad);
-    for (int l = 0; l < k; ++l) L.mm(+1, st.rs[l], N, CZ[l], N);
+  Mat h[3], c[3], e[3], f[3];
+  for (int l = 0; l < k; ++l) {
+    const int dl = st.rs[l].c;
+    h[l] = ring(t, l, b, dl);
+    c[l] = ring(t, 3 + l, dl, b);
+    if (fused) e[l] = ring(t, 6 + l, b, dl), f[l] = ring(t, 9 + l, dl, b);
   }
-  L.flush();
-  // L3
-  Mat phi = ctx_.tmp(base + 1, b, b), acc1 = ctx_.tmp(base + 2, b, b), acc2 = ctx_.tmp(base + 3, b, b);
-  Mat gq = ctx_.tmp(base + 4, b, b);
-  L.out(phi);
-  for (int l = 0; l < k; ++l) L.mm(-1, st.row[l], N, st.qs[l], N);
-  if (fused) {
-    L.out(acc1);
-    for (int l = 0; l < k; ++l) L.mm(+1, st.ss[l], N, st.row[l], H);
-    L.out(acc2);
-    for (int l = 0; l < k; ++l) L.mm(+1, st.row[l], N, st.ws[l], N);
-    L.out(gq).mm(+1, st.g, N, quad, N);
+  // Prologue (side stream): forward factors and couplings only.
+  {
+    cudaStream_t sp = ctx_.side();
+    if (t >= kBackDepth - 1) cuda_check(cudaStreamWaitEvent(sp, ev_b(ctx_, t - kBackDepth + 1), 0), "ring wait");
+    Level P(sp, cfg_);
+    for (int l = 0; l < k; ++l) {
+      P.out(h[l]).mm(+1, st.g, N, st.rs[l], N);
+      P.out(c[l]).mm(+1, st.qs[l], N, st.g, N);
+      if (fused) {
+        P.out(e[l]).mm(+1, st.g, N, st.ss[l], N).mm(-1, st.sc, N, st.qs[l], H);
+        P.out(f[l]).mm(+1, st.ws[l], N, st.g, H).mm(-1, st.qs[l], N, st.sc, N);
+      }
+    }
+    P.flush();
+    cuda_check(cudaEventRecord(ev_pre(ctx_, t), sp), "pre record");
   }
-  L.flush();
-  // L4 (left pending: the caller adds the next step's early L1 before flushing)
-  L.out(st.diag).add(+1, st.g).mm(+1, phi, N, st.g, N);
-  if (fused) {
-    L.out(st.zdiag)
-        .add(+1, st.sc)
-        .mm(+1, phi, N, st.sc, N)
-        .mm(+1, st.sc, N, phi, H)
-        .mm(+1, st.g, N, acc1, N)
-        .mm(+1, acc2, N, st.g, H)
-        .mm(+1, gq, N, st.g, H);
+  // X_A chain (chain stream): row / col, then the diagonal block.
+  {
+    cudaStream_t sa = ctx_.chain();
+    cuda_check(cudaStreamWaitEvent(sa, ev_pre(ctx_, t), 0), "pre wait");
+    Level A(sa, cfg_);
+    for (int j = 0; j < k; ++j) {
+      A.out(st.row[j]);
+      for (int l = 0; l < k; ++l) A.mm(-1, h[l], N, st.ya[l][j], N);
+      A.out(st.col[j]);
+      for (int l = 0; l < k; ++l) A.mm(-1, st.ya[j][l], N, c[l], N);
+    }
+    A.flush();
+    cuda_check(cudaEventRecord(ev_a1(ctx_, t), sa), "a1 record");
+    A.out(st.diag).add(+1, st.g);
+    for (int l = 0; l < k; ++l) A.mm(-1, st.row[l], N, c[l], N);
+    A.flush();
   }
-}
-
-void back_step(Context& ctx, cudaStream_t s, const BackStep& st) {
-  BackPipe pipe(ctx);
-  Level L(s);
-  pipe.early(L, st, 0);
-  pipe.rest(L, st, 0);
-  L.flush();
+  if (!fused) {
+    cuda_check(cudaEventRecord(ev_b(ctx_, t), ctx_.chain()), "b record");
+    return;
+  }
+  // X_B chain (aux stream), one step behind at most kBackDepth - 1.
+  {
+    cudaStream_t sb = ctx_.aux();
+    cuda_check(cudaStreamWaitEvent(sb, ev_a1(ctx_, t), 0), "a1 wait");
+    Level B(sb, cfg_);
+    for (int j = 0; j < k; ++j) {
+      B.out(st.zrow[j]);
+      for (int l = 0; l < k; ++l) B.mm(+1, e[l], N, st.ya[j][l], H);
+      for (int l = 0; l < k; ++l) B.mm(-1, h[l], N, st.yb[l][j], N);
+      B.out(st.zcol[j]);
+      for (int l = 0; l < k; ++l) B.mm(+1, st.ya[j][l], N, f[l], N);
+      for (int l = 0; l < k; ++l) B.mm(-1, st.yb[j][l], N, h[l], H);
+    }
+    B.flush();
+    B.out(st.zdiag).add(+1, st.sc);
+    for (int l = 0; l < k; ++l) B.mm(+1, st.row[l], N, f[l], N);
+    for (int l = 0; l < k; ++l) B.mm(-1, st.zrow[l], N, h[l], H);
+    B.flush();
+    cuda_check(cudaEventRecord(ev_b(ctx_, t), sb), "b record");
+  }
 }
 
 }  // namespace bsel

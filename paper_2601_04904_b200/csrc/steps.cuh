@@ -46,35 +46,52 @@ void streams_join(Context& ctx);
 
 // Generic Takahashi back-substitution step with k <= 3 trailing couplings
 // (rgf.py:322-398).  sc.p == nullptr -> selected inversion only.
-// late[l][j]: ya/yb[l][j] is produced by the PREVIOUS step's last level (its
-// diagonal block); all other trailing blocks are available one level earlier.
+// Outputs left empty (p == nullptr) are allocated by BackSweep in its ring
+// (diagonal_only drops, carried middle-partition couplings); step() fills
+// them in so the caller can read the block back.
 struct BackStep {
   int k = 0;
   Mat g, sc;
   Mat rs[3], qs[3], ss[3], ws[3];
   Mat ya[3][3], yb[3][3];
-  bool late[3][3] = {};
   // outputs
   Mat row[3], col[3], diag;
   Mat zrow[3], zcol[3], zdiag;
 };
 
-// Software-pipelined form used by the sweeps:
-//   back_step_early(L, st_t)  queues step t's L1 products that do not read a
-//                              late block (they join step t-1's pending L4);
-//   L.flush();
-//   back_step_rest(L, st_t)   late L1 -> L2 -> L3, and queues L4 (pending).
-// Temporaries of step t live in slot half `parity` (t & 1).
-class BackPipe {
+// Backward sweep engine.  The reference's _backstep is re-associated so that
+// every product involving the trailing solution is ONE level deep:
+//   h_l = g rs_l,  c_l = qs_l g,  e_l = g ss_l - sc qs_l^H,  f_l = ws_l g^H - qs_l sc
+//   row_j = -sum_l h_l ya[l][j]             col_j = -sum_l ya[j][l] c_l
+//   diag  = g - sum_l row_l c_l
+//   zrow_j = sum_l e_l ya[j][l]^H - sum_l h_l yb[l][j]
+//   zcol_j = sum_l ya[j][l] f_l - sum_l yb[j][l] h_l^H
+//   zdiag = sc + sum_l (row_l f_l - zrow_l h_l^H)
+// (algebraically identical to rgf.py:342-397: phi g = -sum row_l c_l, and
+// g quad g^H + g acc1 + sc phi^H fold into -sum zrow_l h_l^H).
+// Three streams: the per-step prologue (h, c, e, f: forward factors only)
+// runs ahead on the side stream, the X_A chain (2 levels per step) on the
+// high-priority chain stream, the X_B chain (2 levels per step, lagging) on
+// the aux stream; a ring of kBackDepth steps bounds the lag.
+constexpr int kBackDepth = 4;
+// Slots of the context pool a backward sweep uses (reserve before begin()).
+int back_sweep_slots();
+class BackSweep {
  public:
-  explicit BackPipe(Context& ctx) : ctx_(ctx) {}
-  void early(Level& L, const BackStep& st, int parity);
-  void rest(Level& L, const BackStep& st, int parity);
+  explicit BackSweep(Context& ctx, int tile_cfg = kTileAuto);
+  // Fork the three streams from ctx.stream() (everything queued there so far
+  // precedes the sweep).
+  void begin();
+  void step(BackStep& st);
+  // Make ctx.stream() wait for every step issued so far (outputs complete).
+  void fence();
+  void end() { fence(); }
 
  private:
   Context& ctx_;
-  Mat RA[3], CA[3], RZ[3], CZ[3], e[3], f[3];
+  int cfg_;
+  int64_t t_ = 0;
+  Mat ring(int64_t t, int k, int r, int c);
 };
-void back_step(Context& ctx, cudaStream_t s, const BackStep& st);
 
 }  // namespace bsel

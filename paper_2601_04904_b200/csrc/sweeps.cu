@@ -26,9 +26,10 @@ Context::Context(int device) : device_(device) {
   cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
   cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, least), "aux stream");
   cuda_check(cudaStreamCreateWithPriority(&chain_, cudaStreamNonBlocking, greatest), "chain stream");
+  cuda_check(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, least), "side stream");
   cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "flag");
   cuda_check(cudaMalloc(&d_status_, sizeof(unsigned long long)), "status");
-  events_.resize(16);
+  events_.resize(64);
   for (auto& e : events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& t : timers_) cuda_check(cudaEventCreate(&t), "timer");
   reset_status();
@@ -48,6 +49,7 @@ Context::~Context() {
   if (xfer_) cudaStreamDestroy(xfer_);
   if (aux_) cudaStreamDestroy(aux_);
   if (chain_) cudaStreamDestroy(chain_);
+  if (side_) cudaStreamDestroy(side_);
 }
 
 cudaStream_t Context::xfer() {
@@ -69,6 +71,7 @@ void Context::reserve_slots(int nslots, int64_t slot_elems) {
   cuda_check(cudaStreamSynchronize(user_stream_), "sync before realloc");
   cuda_check(cudaStreamSynchronize(aux_), "sync before realloc");
   cuda_check(cudaStreamSynchronize(chain_), "sync before realloc");
+  cuda_check(cudaStreamSynchronize(side_), "sync before realloc");
   if (slots_) cudaFree(slots_);
   nslots_ = std::max(nslots, nslots_);
   slot_elems_ = std::max(slot_elems, slot_elems_);
@@ -160,18 +163,15 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
     }
     if (fused) {
       cuda_check(cudaStreamWaitEvent(sB, ctx.event(i & 1), 0), "wait A");
-      // v L^H = L S_B L^H = t1 (Bd t1^H): two levels (same product count).
+      // v L^H - t1 BU = L S_B L^H - t1 BU = t1 (Bd t1^H - BU): two levels,
+      // one product fewer than rgf.py:113-118.
       Mat w = ctx.tmp(r + 1, b, b), q = ctx.tmp(r + 2, b, b), sb = F.SB(i);
       Level L(sB);
       L.out(w).mm(+1, S, N, B->D(i), N);
-      L.out(q).mm(+1, B->D(i), N, t1, H);
+      L.out(q).add(-1, B->U(i)).mm(+1, B->D(i), N, t1, H);
       L.flush();
       L.out(sb).mm(+1, w, N, S, H);
-      L.out(B->D(i + 1))
-          .add(+1, B->D(i + 1))
-          .mm(+1, t1, N, q, N)
-          .mm(-1, B->L(i), N, t1, H)
-          .mm(-1, t1, N, B->U(i), N);
+      L.out(B->D(i + 1)).add(+1, B->D(i + 1)).mm(+1, t1, N, q, N).mm(-1, B->L(i), N, t1, H);
       L.flush();
       cuda_check(cudaEventRecord(ctx.event(2 + (i & 1)), sB), "record B");
     }
@@ -251,13 +251,15 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
 // Backward sweeps
 // ---------------------------------------------------------------------------
 
-// rgf.py:127-199 (Alg. 2), BT.
+// rgf.py:127-199 (Alg. 2), BT: the generic back step with k = 1 (rs = U,
+// qs = L), i.e. X_up = -(S U) X+, X_lo = -X+ (L S), X_dd = S - X_up (L S)
+// and the same re-association of the quadratic terms (steps.cuh).
 void bt_backward(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDev* B, const BtaDev& XA,
                  const BtaDev* XB, bool diag_only) {
   const int n = (int)A.n, b = (int)A.b;
   cudaStream_t s = ctx.stream();
   const bool fused = B != nullptr;
-  ctx.reserve_slots(16, (int64_t)b * b);
+  ctx.reserve_slots(back_sweep_slots(), (int64_t)b * b);
   Level L(s);
   copy_block(L, XA.D(n - 1), F.SA(n - 1));
   if (fused) {
@@ -267,53 +269,29 @@ void bt_backward(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDe
     L.out(XB->D(n - 1)).mm(+1, w, N, F.SA(n - 1), H);
   }
   L.flush();
+  BackSweep sweep(ctx);
+  sweep.begin();
   for (int i = n - 2; i >= 0; --i) {
-    Mat S = F.SA(i), Xp = XA.D(i + 1);
-    Mat tA1 = ctx.tmp(0, b, b), tA2 = ctx.tmp(1, b, b);
-    Mat xlo = diag_only ? ctx.tmp(2, b, b) : XA.L(i);
-    Mat xup = diag_only ? ctx.tmp(3, b, b) : XA.U(i);
-    L.out(tA1).mm(+1, S, N, A.U(i), N);
-    L.out(tA2).mm(+1, Xp, N, A.L(i), N);
-    Mat sbu = ctx.tmp(4, b, b), xbl = ctx.tmp(5, b, b);
+    BackStep st;
+    st.k = 1;
+    st.g = F.SA(i);
+    st.rs[0] = A.U(i), st.qs[0] = A.L(i);
+    st.ya[0][0] = XA.D(i + 1);
+    if (!diag_only) st.row[0] = XA.U(i), st.col[0] = XA.L(i);
+    st.diag = XA.D(i);
     if (fused) {
-      L.out(sbu).mm(+1, S, N, B->U(i), N);
-      L.out(xbl).mm(+1, Xp, N, B->L(i), N);
+      st.sc = F.SB(i);
+      st.ss[0] = B->U(i), st.ws[0] = B->L(i);
+      st.yb[0][0] = XB->D(i + 1);
+      if (!diag_only) st.zrow[0] = XB->U(i), st.zcol[0] = XB->L(i);
+      st.zdiag = XB->D(i);
     }
-    L.flush();
-    L.out(xlo).mm(-1, tA2, N, S, N);
-    L.out(xup).mm(-1, tA1, N, Xp, N);
-    Mat tB1 = ctx.tmp(6, b, b), tB2 = ctx.tmp(7, b, b), tB3 = ctx.tmp(8, b, b);
-    Mat tB4 = ctx.tmp(9, b, b), tB5 = ctx.tmp(10, b, b);
-    Mat Zp, sb;
-    if (fused) {
-      Zp = XB->D(i + 1);
-      sb = F.SB(i);
-      L.out(tB1).mm(+1, Zp, N, tA1, H);
-      L.out(tB2).mm(+1, sb, N, tA2, H);
-      L.out(tB3).mm(+1, tA2, N, sb, N);
-      L.out(tB4).mm(+1, sbu, N, Xp, H);
-      L.out(tB5).mm(+1, xbl, N, S, H);
-    }
-    L.flush();
-    L.out(XA.D(i)).add(+1, S).mm(-1, tA1, N, xlo, N);
-    if (fused) {
-      Mat xbup = diag_only ? ctx.tmp(11, b, b) : XB->U(i);
-      Mat xblo = diag_only ? ctx.tmp(12, b, b) : XB->L(i);
-      L.out(xbup).add(+1, tB4).add(-1, tB2).mm(-1, tA1, N, Zp, N);
-      L.out(xblo).add(-1, tB1).add(-1, tB3).add(+1, tB5);
-      L.out(XB->D(i))
-          .add(+1, sb)
-          .mm(+1, tA1, N, tB1, N)
-          .mm(+1, tA1, N, tB3, N)
-          .mm(+1, tB2, N, tA1, H)
-          .mm(-1, tA1, N, tB5, N)
-          .mm(-1, tB4, N, tA1, H);
-    }
-    L.flush();
+    sweep.step(st);
   }
+  sweep.end();
 }
 
-// rgf.py:401-489: generic _backstep (steps.cu back_step) with k = 1 at the
+// rgf.py:401-489: generic _backstep (steps.cu BackSweep) with k = 1 at the
 // last block (tip coupling only) and k = 2 elsewhere (next block, tip).
 void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDev* B,
                         const BtaDev& XA, const BtaDev* XB, bool diag_only) {
@@ -321,22 +299,25 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
   cudaStream_t s = ctx.stream();
   const bool fused = B != nullptr;
   const int mx = std::max(a, b);
-  ctx.reserve_slots(64, (int64_t)mx * mx);
+  ctx.reserve_slots(back_sweep_slots(), (int64_t)mx * mx);
   Mat Xtt = cm(F.tip_inv, a, a);
-  Mat Ztt;
+  Mat Ztt, sc_last;
   Level L(s);
   copy_block(L, XA.T(), Xtt);
   if (fused) {
-    Mat w = ctx.tmp(0, a, a);
+    Mat w = ctx.tmp(0, a, a), sct = ctx.tmp(1, b, b);
+    sc_last = ctx.tmp(2, b, b);
     L.out(w).mm(+1, Xtt, N, cm(F.b_tip, a, a), N);
+    L.out(sct).mm(+1, F.SA(n - 1), N, cm(F.b_diag_last, b, b), N);
     L.flush();
     L.out(XB->T()).mm(+1, w, N, Xtt, H);
+    L.out(sc_last).mm(+1, sct, N, F.SA(n - 1), H);
     Ztt = XB->T();
   }
   L.flush();
-  BackPipe pipe(ctx);
+  BackSweep sweep(ctx);
+  sweep.begin();
   for (int i = n - 1; i >= 0; --i) {
-    const int parity = (n - 1 - i) & 1;
     BackStep st;
     st.g = F.SA(i);
     if (i == n - 1) {
@@ -344,40 +325,32 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
       st.rs[0] = F.ACe(i), st.qs[0] = F.ARe(i), st.ya[0][0] = Xtt;
       st.row[0] = XA.AC(i), st.col[0] = XA.AR(i);
       if (fused) {
-        Mat sct = ctx.tmp(1, b, b), sc = ctx.tmp(2, b, b);
-        L.out(sct).mm(+1, st.g, N, cm(F.b_diag_last, b, b), N);
-        L.flush();
-        L.out(sc).mm(+1, sct, N, st.g, H);
-        L.flush();
-        st.sc = sc;
+        st.sc = sc_last;
         st.ss[0] = F.BCe(i), st.ws[0] = F.BRe(i), st.yb[0][0] = Ztt;
         st.zrow[0] = XB->AC(i), st.zcol[0] = XB->AR(i);
       }
     } else {
       st.k = 2;
-      st.late[0][0] = true;  // X(i+1,i+1) comes from the previous step's last level
       st.rs[0] = A.U(i), st.rs[1] = F.ACe(i);
       st.qs[0] = A.L(i), st.qs[1] = F.ARe(i);
       st.ya[0][0] = XA.D(i + 1), st.ya[0][1] = XA.AC(i + 1), st.ya[1][0] = XA.AR(i + 1), st.ya[1][1] = Xtt;
-      st.row[0] = diag_only ? ctx.tmp(3, b, b) : XA.U(i), st.row[1] = XA.AC(i);
-      st.col[0] = diag_only ? ctx.tmp(4, b, b) : XA.L(i), st.col[1] = XA.AR(i);
+      if (!diag_only) st.row[0] = XA.U(i), st.col[0] = XA.L(i);
+      st.row[1] = XA.AC(i), st.col[1] = XA.AR(i);
       if (fused) {
         st.sc = F.SB(i);
         st.ss[0] = B->U(i), st.ss[1] = F.BCe(i);
         st.ws[0] = B->L(i), st.ws[1] = F.BRe(i);
         st.yb[0][0] = XB->D(i + 1), st.yb[0][1] = XB->AC(i + 1), st.yb[1][0] = XB->AR(i + 1);
         st.yb[1][1] = Ztt;
-        st.zrow[0] = diag_only ? ctx.tmp(5, b, b) : XB->U(i), st.zrow[1] = XB->AC(i);
-        st.zcol[0] = diag_only ? ctx.tmp(6, b, b) : XB->L(i), st.zcol[1] = XB->AR(i);
+        if (!diag_only) st.zrow[0] = XB->U(i), st.zcol[0] = XB->L(i);
+        st.zrow[1] = XB->AC(i), st.zcol[1] = XB->AR(i);
       }
     }
     st.diag = XA.D(i);
     if (fused) st.zdiag = XB->D(i);
-    pipe.early(L, st, parity);
-    L.flush();
-    pipe.rest(L, st, parity);
+    sweep.step(st);
   }
-  L.flush();
+  sweep.end();
 }
 
 }  // namespace

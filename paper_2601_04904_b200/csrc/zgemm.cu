@@ -16,6 +16,7 @@
 #include "zgemm.cuh"
 
 #include <algorithm>
+#include <vector>
 #include <atomic>
 #include <cstdio>
 #include <deque>
@@ -335,7 +336,11 @@ size_t g_prof_used = 0;
 std::mutex g_prof_mu;
 }  // namespace
 
+cudaEvent_t g_prof_base = nullptr;
 void profile_begin() {
+  cudaDeviceSynchronize();
+  if (!g_prof_base) cudaEventCreate(&g_prof_base);
+  cudaEventRecord(g_prof_base, 0);
   g_prof_on = true;
   g_prof_used = 0;
 }
@@ -366,10 +371,17 @@ ProfileTotals profile_end() {
   ProfileTotals t{};
   cudaDeviceSynchronize();
   std::lock_guard<std::mutex> lock(g_prof_mu);
+  // Spans relative to the base event; busy time = union of the spans of one
+  // kind (launches of concurrent streams overlap).
+  std::vector<std::pair<float, float>> spans[2];
   for (size_t i = 0; i < g_prof_used; ++i) {
-    float ms = 0.f;
+    float ms = 0.f, s0 = 0.f, s1 = 0.f;
     cudaEventElapsedTime(&ms, g_prof[i].t0, g_prof[i].t1);
-    if (g_prof[i].kind == 0) {
+    cudaEventElapsedTime(&s0, g_prof_base, g_prof[i].t0);
+    cudaEventElapsedTime(&s1, g_prof_base, g_prof[i].t1);
+    const int kind = g_prof[i].kind == 0 ? 0 : 1;
+    spans[kind].emplace_back(s0, s1);
+    if (kind == 0) {
       ++t.gemm_launches;
       t.gemm_flops += g_prof[i].flops;
       t.gemm_bytes += g_prof[i].bytes;
@@ -377,8 +389,26 @@ ProfileTotals profile_end() {
     } else {
       ++t.inverse_calls;
       t.inverse_ms += ms;
+      t.inverse_flops += g_prof[i].flops;
     }
   }
+  double busy[2] = {0.0, 0.0};
+  for (int k = 0; k < 2; ++k) {
+    auto& v = spans[k];
+    std::sort(v.begin(), v.end());
+    double cur0 = -1.0, cur1 = -1.0;
+    for (auto& sp : v) {
+      if (sp.first > cur1) {
+        if (cur1 > cur0) busy[k] += cur1 - cur0;
+        cur0 = sp.first, cur1 = sp.second;
+      } else if (sp.second > cur1) {
+        cur1 = sp.second;
+      }
+    }
+    if (cur1 > cur0) busy[k] += cur1 - cur0;
+  }
+  t.gemm_busy_ms = busy[0];
+  t.inverse_busy_ms = busy[1];
   g_prof_on = false;
   g_prof_used = 0;
   return t;

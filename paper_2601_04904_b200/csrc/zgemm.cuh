@@ -92,6 +92,7 @@ struct ProfileTotals {
   int64_t inverse_calls;
   double inverse_ms;
   double gemm_bytes;
+  double gemm_busy_ms, inverse_busy_ms, inverse_flops;
 };
 void profile_begin();
 ProfileTotals profile_end();
