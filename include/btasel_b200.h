@@ -88,6 +88,16 @@ int bsel_context_set_stream(bsel_context_t* ctx, void* cuda_stream);
  * BSEL_INV_GRID).  Contexts sweeping concurrently on one GPU (in-GPU
  * partitions) use fewer so the chains leave SMs to each other's GEMMs.    */
 int bsel_context_set_inverse_grid(bsel_context_t* ctx, int ctas);
+/* Symmetry of the right-hand side B.  Every forward entry point checks B
+ * EXACTLY on its pattern (B = B^H, B = -B^H) while staging it; when B = s B^H
+ * the backward sweep uses X_B = s X_B^H (fewer products, same result to
+ * rounding).  mode: +1 / -1 force that path, 0 forces the general path,
+ * 2 (default) = from this context's own last check.  A partitioned solve
+ * must decide for the WHOLE B: OR the partitions' flags and force the mode.
+ * flags: bit 0 = B is not Hermitian, bit 1 = B is not anti-Hermitian
+ * (3 if nothing was checked since the last forward began).               */
+int bsel_context_set_b_symmetry(bsel_context_t* ctx, int mode);
+int bsel_context_b_symmetry(bsel_context_t* ctx, int* flags, int* mode);
 /* Synchronizes; reports deferred device errors (singular pivots). */
 int bsel_synchronize(bsel_context_t* ctx, bsel_status_t* st);
 /* Device time of the last forward / backward sweep in ms (synchronizes). */

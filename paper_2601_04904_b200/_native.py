@@ -26,6 +26,8 @@ EXPORTS = (
     "bsel_context_destroy",
     "bsel_context_set_stream",
     "bsel_context_set_inverse_grid",
+    "bsel_context_set_b_symmetry",
+    "bsel_context_b_symmetry",
     "bsel_synchronize",
     "bsel_last_timings",
     "bsel_block_multiply_acc",
@@ -166,6 +168,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             "bsel_context_destroy": ([vp], i32),
             "bsel_context_set_stream": ([vp, vp], i32),
             "bsel_context_set_inverse_grid": ([vp, i32], i32),
+            "bsel_context_set_b_symmetry": ([vp, i32], i32),
+            "bsel_context_b_symmetry": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
             "bsel_synchronize": ([vp, st], i32),
             "bsel_last_timings": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], i32),
             "bsel_block_multiply_acc": (
@@ -260,6 +264,20 @@ class Context:
         """CTAs of the persistent block inverse on this context (0 = default)."""
         if self.lib.bsel_context_set_inverse_grid(self.handle, int(ctas)) != 0:
             raise ValueError(f"invalid inverse grid {ctas}")
+
+    SYM_AUTO = 2
+
+    def set_b_symmetry(self, mode: int) -> None:
+        """Backward path for the quadratic solve: +1 / -1 (B = +-B^H), 0
+        (general) or SYM_AUTO (this context's own check of B)."""
+        if self.lib.bsel_context_set_b_symmetry(self.handle, int(mode)) != 0:
+            raise ValueError(f"invalid symmetry mode {mode}")
+
+    def b_symmetry(self) -> tuple[int, int]:
+        """(flags of the last check of B, path the backward would take)."""
+        flags, mode = ctypes.c_int32(), ctypes.c_int32()
+        self.lib.bsel_context_b_symmetry(self.handle, ctypes.byref(flags), ctypes.byref(mode))
+        return flags.value, mode.value
 
     def call(self, name: str, *args) -> None:
         st = Status()

@@ -210,6 +210,19 @@ int bsel_context_set_inverse_grid(bsel_context_t* ctx, int ctas) {
   return BSEL_OK;
 }
 
+int bsel_context_set_b_symmetry(bsel_context_t* ctx, int mode) {
+  if (!ctx || mode < -1 || mode > Context::kSymAuto) return BSEL_ERR_ARG;
+  ctx->impl->set_b_symmetry(mode);
+  return BSEL_OK;
+}
+
+int bsel_context_b_symmetry(bsel_context_t* ctx, int* flags, int* mode) {
+  if (!ctx) return BSEL_ERR_ARG;
+  if (flags) *flags = ctx->impl->sym_flags();
+  if (mode) *mode = ctx->impl->b_symmetry();
+  return BSEL_OK;
+}
+
 int bsel_synchronize(bsel_context_t* ctx, bsel_status_t* st) {
   return guarded(st, [&] {
     if (!ctx) throw ArgError("ctx is NULL");
@@ -308,8 +321,15 @@ int bsel_bta_forward(bsel_context_t* ctx, const bsel_bta_t* a_work, const bsel_b
     if (b_work) check_same(a_work, b_work);
     if ((f->fused != 0) != (b_work != nullptr)) throw ArgError("factors mode disagrees with right-hand side");
     BtaDev A = to_dev(*a_work), B;
-    if (b_work) B = to_dev(*b_work);
-    bta_forward(*ctx->impl, A, b_work ? &B : nullptr, to_dev(*f));
+    Context& cx = *ctx->impl;
+    if (b_work) {
+      B = to_dev(*b_work);
+      cx.sym_reset(cx.stream());
+      sym_check_strips(cx, B, 0, 0, B.n, nullptr, 0, cx.stream());
+      sym_check_couplings(cx, B, 0, B.n - 1, cx.stream());
+      sym_check_tip(cx, B, nullptr, cx.stream());
+    }
+    bta_forward(cx, A, b_work ? &B : nullptr, to_dev(*f));
     raise_if_singular(*ctx->impl, a_work->n);
   });
 }
@@ -400,10 +420,12 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
       B.arrow_row = at(7);
       B.arrow_col = at(8);
       B.tip = at(9);
-      cp(B.diag, b->diag, n * bs * bs);
-      cp(B.arrow_row, b->arrow_row, n * as * bs);
-      cp(B.arrow_col, b->arrow_col, n * bs * as);
-      cp(B.tip, b->tip, as * as);
+      // Working copies of B, staged by the symmetry check (one pass).
+      const BtaDev Bin = to_dev(*b);
+      cx.sym_reset(s);
+      sym_check_strips(cx, Bin, 0, 0, n, &B, 0, s);
+      sym_check_couplings(cx, Bin, 0, n - 1, s);
+      sym_check_tip(cx, Bin, B.tip, s);
       F.s_b = at(10);
       F.b_diag_last = at(11);
       F.b_tip = at(12);

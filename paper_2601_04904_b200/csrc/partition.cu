@@ -90,11 +90,21 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
   const int mx = (int)std::max(a, b);
   ctx.reserve_slots(64, (int64_t)mx * mx);
   ctx.reset_status();
+  ctx.sym_reset(ctx.stream());
   // Working copies of the partition (dist.py:194-202) and zeroed tip deltas.
-  auto stage = [&](const BtaDev& src, const BtaDev& w) {
-    copy_blocks(ctx, w.diag, src.diag + lo * b * b, len * b * b);
-    copy_blocks(ctx, w.arrow_row, src.arrow_row + lo * a * b, len * a * b);
-    copy_blocks(ctx, w.arrow_col, src.arrow_col + lo * b * a, len * b * a);
+  // B's strips are staged by the symmetry check (one pass), which also checks
+  // this partition's couplings and the tip (the partitions' flags are OR-ed
+  // by the host layer: together they cover every pattern block of B).
+  auto stage = [&](const BtaDev& src, const BtaDev& w, bool check) {
+    if (check) {
+      sym_check_strips(ctx, src, 0, lo, hi, &w, lo, ctx.stream());
+      sym_check_couplings(ctx, src, lo, std::min(hi, A.n - 1), ctx.stream());
+      sym_check_tip(ctx, src, nullptr, ctx.stream());
+    } else {
+      copy_blocks(ctx, w.diag, src.diag + lo * b * b, len * b * b);
+      copy_blocks(ctx, w.arrow_row, src.arrow_row + lo * a * b, len * a * b);
+      copy_blocks(ctx, w.arrow_col, src.arrow_col + lo * b * a, len * b * a);
+    }
     if (a > 0) cuda_check(cudaMemsetAsync(w.tip, 0, (size_t)(a * a) * sizeof(double2), ctx.stream()), "tip");
   };
   // End-to-end mode: input chunks are queued on the copy stream a few
@@ -127,10 +137,16 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
       if (fused) {
         copy_chunk(xs, *WB, *io->hb, r, lo, true, false);
         copy_chunk(xs, *B, *io->hb, r, 0, false, true);
+        // symmetry of the chunk as it lands (before the sweep mutates it)
+        sym_check_strips(ctx, *WB, lo, r.g0, r.g1, nullptr, 0, xs);
+        sym_check_couplings(ctx, *B, r.e0, r.e1, xs);
       }
       if (c == 0 && io->copy_tip && a > 0) {
         copy_async(xs, A.tip, io->ha->tip, a * a);
-        if (fused) copy_async(xs, B->tip, io->hb->tip, a * a);
+        if (fused) {
+          copy_async(xs, B->tip, io->hb->tip, a * a);
+          sym_check_tip(ctx, *B, nullptr, xs);
+        }
       }
       cuda_check(cudaEventRecord(ctx.xfer_event((int)c), xs), "chunk record");
       if (trace) tev(tin, xs);
@@ -151,8 +167,8 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
     for (auto* w : {&WA, WB})
       if (w && a > 0) cuda_check(cudaMemsetAsync(w->tip, 0, (size_t)(a * a) * sizeof(double2), ctx.stream()), "tip");
   } else {
-    stage(A, WA);
-    if (fused) stage(*B, *WB);
+    stage(A, WA, false);
+    if (fused) stage(*B, *WB, true);
   }
   cuda_check(cudaEventRecord(ctx.timer(0), ctx.stream()), "timer");
   auto d = [&](const BtaDev& w, int64_t i) { return w.D(i - lo); };

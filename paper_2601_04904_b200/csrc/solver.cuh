@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "level.cuh"
+#include "symmetry.cuh"
 
 namespace bsel {
 
@@ -82,6 +83,19 @@ class Context {
   void reserve_slots(int nslots, int64_t slot_elems);
   double2* inv_work(int64_t elems);
 
+  // Symmetry of the right-hand side B (symmetry.cuh).  sym_reset() clears
+  // the device flags, sym_check() ORs a block-pair check into them (stream
+  // ordered), read_status() brings them to the host.  b_symmetry(): the
+  // backward path to take, +1 / -1 (B = +-B^H exactly), 0 = general; forced
+  // by set_b_symmetry(+1 / -1 / 0) (the partitioned solves decide globally),
+  // or kSymAuto = from this context's own last check.
+  static constexpr int kSymAuto = 2;
+  void sym_reset(cudaStream_t s);
+  void sym_check(const SymJob& j, cudaStream_t s);
+  void set_b_symmetry(int mode) { sym_mode_ = mode; }
+  int b_symmetry() const;
+  int sym_flags() const { return sym_checked_ ? sym_flags_ : 3; }
+
   // Singularity bookkeeping (device side, checked at synchronize()).
   void reset_status();
   void invert(Mat X, Mat Y, uint64_t order, int64_t index, cudaStream_t s);
@@ -111,6 +125,9 @@ class Context {
   double2* inv_work_ = nullptr;
   int64_t inv_work_elems_ = 0;
   int* d_flag_ = nullptr;
+  int* d_sym_ = nullptr;
+  int sym_flags_ = 3, sym_mode_ = kSymAuto;
+  bool sym_checked_ = false;
   unsigned long long* d_status_ = nullptr;
   std::vector<cudaEvent_t> events_;
   std::vector<cudaEvent_t> xfer_events_;
@@ -118,6 +135,15 @@ class Context {
   int inv_grid_ = 0;
   cudaEvent_t timers_[4] = {nullptr, nullptr, nullptr, nullptr};
 };
+
+// Symmetry checks of a right-hand side (Context::sym_check).  Strips: diag
+// blocks and arrow pairs of global blocks [g0, g1) of `src` (whose block 0 is
+// global block src_lo), optionally copied to `dst` (block 0 = dst_lo);
+// couplings: lower/upper pairs [e0, e1); tip: optionally copied to dst_tip.
+void sym_check_strips(Context& ctx, const BtaDev& src, int64_t src_lo, int64_t g0, int64_t g1, const BtaDev* dst,
+                      int64_t dst_lo, cudaStream_t s);
+void sym_check_couplings(Context& ctx, const BtaDev& src, int64_t e0, int64_t e1, cudaStream_t s);
+void sym_check_tip(Context& ctx, const BtaDev& src, double2* dst_tip, cudaStream_t s);
 
 // rgf.py:79 bt_forward / rgf.py:207 bta_forward.  `A`, `B` are working
 // copies mutated in place (diag, arrow strips, tip); B may be null (SI).

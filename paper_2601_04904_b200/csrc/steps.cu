@@ -196,7 +196,7 @@ static_assert(Context::kBackEvents + 3 * kBackDepth + 3 <= 64, "event pool");
 
 int back_sweep_slots() { return kBackRingBase + kBackPerStep * kBackDepth; }
 
-BackSweep::BackSweep(Context& ctx, int tile_cfg) : ctx_(ctx), cfg_(tile_cfg) {}
+BackSweep::BackSweep(Context& ctx, int tile_cfg) : ctx_(ctx), cfg_(tile_cfg), sym_(ctx.b_symmetry()) {}
 
 Mat BackSweep::ring(int64_t t, int k, int r, int c) {
   return ctx_.tmp(kBackRingBase + (int)(t % kBackDepth) * kBackPerStep + k, r, c);
@@ -221,6 +221,7 @@ void BackSweep::step(BackStep& st) {
   const int64_t t = t_++;
   const int k = st.k, b = st.g.r;
   const bool fused = st.sc.p != nullptr;
+  const int sym = fused ? sym_ : 0;
   if (k < 1 || k > 3) throw ShapeError("back step needs 1..3 couplings");
   // Ring-allocate the outputs the caller left empty.
   int spare = 12;
@@ -243,7 +244,7 @@ void BackSweep::step(BackStep& st) {
     const int dl = st.rs[l].c;
     h[l] = ring(t, l, b, dl);
     c[l] = ring(t, 3 + l, dl, b);
-    if (fused) e[l] = ring(t, 6 + l, b, dl), f[l] = ring(t, 9 + l, dl, b);
+    if (fused) e[l] = ring(t, 6 + l, b, dl), f[l] = sym ? Mat{} : ring(t, 9 + l, dl, b);
   }
   // Prologue (side stream): forward factors and couplings only.
   {
@@ -255,7 +256,7 @@ void BackSweep::step(BackStep& st) {
       P.out(c[l]).mm(+1, st.qs[l], N, st.g, N);
       if (fused) {
         P.out(e[l]).mm(+1, st.g, N, st.ss[l], N).mm(-1, st.sc, N, st.qs[l], H);
-        P.out(f[l]).mm(+1, st.ws[l], N, st.g, H).mm(-1, st.qs[l], N, st.sc, N);
+        if (!sym) P.out(f[l]).mm(+1, st.ws[l], N, st.g, H).mm(-1, st.qs[l], N, st.sc, N);
       }
     }
     P.flush();
@@ -291,15 +292,28 @@ void BackSweep::step(BackStep& st) {
       B.out(st.zrow[j]);
       for (int l = 0; l < k; ++l) B.mm(+1, e[l], N, st.ya[j][l], H);
       for (int l = 0; l < k; ++l) B.mm(-1, h[l], N, st.yb[l][j], N);
+      if (sym) continue;
       B.out(st.zcol[j]);
       for (int l = 0; l < k; ++l) B.mm(+1, st.ya[j][l], N, f[l], N);
       for (int l = 0; l < k; ++l) B.mm(-1, st.yb[j][l], N, h[l], H);
     }
     B.flush();
     B.out(st.zdiag).add(+1, st.sc);
-    for (int l = 0; l < k; ++l) B.mm(+1, st.row[l], N, f[l], N);
+    for (int l = 0; l < k; ++l) {
+      if (sym) B.mm(sym, st.row[l], N, e[l], H);  // f_l = s e_l^H
+      else B.mm(+1, st.row[l], N, f[l], N);
+    }
     for (int l = 0; l < k; ++l) B.mm(-1, st.zrow[l], N, h[l], H);
     B.flush();
+    if (sym) {  // zcol_j = X_B(trail_j, i) = s X_B(i, trail_j)^H
+      TransJob tj[3];
+      for (int j = 0; j < k; ++j) {
+        tj[j].src = st.zrow[j].p, tj[j].lds = st.zrow[j].ld, tj[j].r = st.zrow[j].r, tj[j].c = st.zrow[j].c;
+        tj[j].dst = st.zcol[j].p, tj[j].ldd = st.zcol[j].ld;
+        if (st.zcol[j].r != st.zrow[j].c || st.zcol[j].c != st.zrow[j].r) throw ShapeError("zcol shape");
+      }
+      cuda_check(launch_conj_transpose(tj, k, sym, sb), "conjugate transpose");
+    }
     cuda_check(cudaEventRecord(ev_b(ctx_, t), sb), "b record");
   }
 }

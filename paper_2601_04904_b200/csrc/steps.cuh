@@ -69,6 +69,9 @@ struct BackStep {
 //   zdiag = sc + sum_l (row_l f_l - zrow_l h_l^H)
 // (algebraically identical to rgf.py:342-397: phi g = -sum row_l c_l, and
 // g quad g^H + g acc1 + sc phi^H fold into -sum zrow_l h_l^H).
+// When B = s B^H exactly (s = +-1, Context::b_symmetry()), X_B = s X_B^H and
+// f_l = s e_l^H: the prologue skips f, zcol_j = s zrow_j^H is a transposed
+// copy and zdiag uses s row_l e_l^H (a quarter fewer products per step).
 // Three streams: the per-step prologue (h, c, e, f: forward factors only)
 // runs ahead on the side stream, the X_A chain (2 levels per step) on the
 // high-priority chain stream, the X_B chain (2 levels per step, lagging) on
@@ -90,6 +93,7 @@ class BackSweep {
  private:
   Context& ctx_;
   int cfg_;
+  int sym_;  // b_symmetry() at construction: +1 / -1 / 0
   int64_t t_ = 0;
   Mat ring(int64_t t, int k, int r, int c);
 };

@@ -13,6 +13,7 @@
 #include "inverse.cuh"
 #include "solver.cuh"
 #include "steps.cuh"
+#include "symmetry.cuh"
 
 namespace bsel {
 
@@ -29,6 +30,7 @@ Context::Context(int device) : device_(device) {
   cuda_check(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, least), "side stream");
   cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "flag");
   cuda_check(cudaMalloc(&d_status_, sizeof(unsigned long long)), "status");
+  cuda_check(cudaMalloc(&d_sym_, sizeof(int)), "symmetry flags");
   events_.resize(64);
   for (auto& e : events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& t : timers_) cuda_check(cudaEventCreate(&t), "timer");
@@ -43,6 +45,7 @@ Context::~Context() {
   if (inv_work_) cudaFree(inv_work_);
   if (d_flag_) cudaFree(d_flag_);
   if (d_status_) cudaFree(d_status_);
+  if (d_sym_) cudaFree(d_sym_);
   for (auto& e : events_) cudaEventDestroy(e);
   for (auto& t : timers_) cudaEventDestroy(t);
   for (auto& e : xfer_events_) cudaEventDestroy(e);
@@ -113,16 +116,83 @@ void Context::invert(Mat X, Mat Y, uint64_t order, int64_t index, cudaStream_t s
   cuda_check(e, "block inverse");
 }
 
+void Context::sym_reset(cudaStream_t s) {
+  cuda_check(cudaMemsetAsync(d_sym_, 0, sizeof(int), s), "memset symmetry flags");
+  sym_checked_ = false;
+}
+
+void Context::sym_check(const SymJob& j, cudaStream_t s) {
+  cuda_check(launch_sym_check(j, d_sym_, s), "symmetry check");
+  sym_checked_ = true;
+}
+
+int Context::b_symmetry() const {
+  if (sym_mode_ != kSymAuto) return sym_mode_;
+  if (!sym_checked_) return 0;
+  if (!(sym_flags_ & kNotHermitian)) return +1;
+  if (!(sym_flags_ & kNotSkew)) return -1;
+  return 0;
+}
+
 SingularInfo Context::read_status() {
   unsigned long long st = 0;
   cuda_check(cudaMemcpyAsync(&st, d_status_, sizeof(st), cudaMemcpyDeviceToHost, user_stream_), "status d2h");
+  int sym = 3;
+  cuda_check(cudaMemcpyAsync(&sym, d_sym_, sizeof(sym), cudaMemcpyDeviceToHost, user_stream_), "symmetry d2h");
   cuda_check(cudaStreamSynchronize(user_stream_), "status sync");
+  sym_flags_ = sym;
   SingularInfo info;
   if (st != ~0ull) {
     info.singular = true;
     info.index = (int64_t)(uint32_t)(st & 0xffffffffu);
   }
   return info;
+}
+
+void sym_check_strips(Context& ctx, const BtaDev& src, int64_t src_lo, int64_t g0, int64_t g1, const BtaDev* dst,
+                      int64_t dst_lo, cudaStream_t s) {
+  if (g1 <= g0) return;
+  const int64_t b = src.b, a = src.a, o = g0 - src_lo, od = g0 - dst_lo;
+  SymJob d;
+  d.X = d.Y = src.diag + o * b * b;
+  d.r = d.c = (int)b;
+  d.sx = d.sy = b * b;
+  d.count = g1 - g0;
+  d.same = true;
+  if (dst) d.dX = d.dY = dst->diag + od * b * b;
+  ctx.sym_check(d, s);
+  if (a == 0) return;
+  SymJob r;
+  r.X = src.arrow_row + o * a * b;
+  r.Y = src.arrow_col + o * b * a;
+  r.r = (int)a, r.c = (int)b;
+  r.sx = r.sy = a * b;
+  r.count = g1 - g0;
+  if (dst) r.dX = dst->arrow_row + od * a * b, r.dY = dst->arrow_col + od * b * a;
+  ctx.sym_check(r, s);
+}
+
+void sym_check_couplings(Context& ctx, const BtaDev& src, int64_t e0, int64_t e1, cudaStream_t s) {
+  if (e1 <= e0) return;
+  const int64_t b = src.b;
+  SymJob j;
+  j.X = src.lower + e0 * b * b;
+  j.Y = src.upper + e0 * b * b;
+  j.r = j.c = (int)b;
+  j.sx = j.sy = b * b;
+  j.count = e1 - e0;
+  ctx.sym_check(j, s);
+}
+
+void sym_check_tip(Context& ctx, const BtaDev& src, double2* dst_tip, cudaStream_t s) {
+  if (src.a == 0) return;
+  SymJob j;
+  j.X = j.Y = src.tip;
+  j.r = j.c = (int)src.a;
+  j.count = 1;
+  j.same = true;
+  j.dX = j.dY = dst_tip;
+  ctx.sym_check(j, s);
 }
 
 cudaEvent_t Context::event(int i) { return events_.at(i); }

@@ -97,6 +97,10 @@ class BoundaryPayload:
     b_coupling: list = field(default_factory=list)
     b_arrow_row: list = field(default_factory=list)
     b_arrow_col: list = field(default_factory=list)
+    # symmetry flags of this rank's check of B (Context.b_symmetry; 3 = none),
+    # carried in the slot header: the reduced solve and every local backward
+    # take the symmetric path only if ALL of B is (anti-)Hermitian
+    sym_flags: int = 3
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for f in _FIELDS for t in getattr(self, f))
@@ -117,7 +121,8 @@ class BoundaryPayload:
     def pack(self) -> torch.Tensor:
         dev = self.diag[0].device
         out = torch.zeros(self.slot_elems(), dtype=torch.float64, device=dev)
-        out[0], out[1], out[2], out[3] = float(self.rank), float(_KIND_CODES[self.kind]), len(self.diag), 0.0
+        out[0], out[1], out[2] = float(self.rank), float(_KIND_CODES[self.kind]), len(self.diag)
+        out[3] = float(self.sym_flags)
         off = 4
         for name, (r, c) in self._layout():
             for t in getattr(self, name):
@@ -132,7 +137,7 @@ class BoundaryPayload:
         if kind is None or int(hdr[0]) != rank:
             raise ProtocolError(f"payload {rank} carries rank {int(hdr[0])} kind code {int(hdr[1])}")
         nbnd = int(hdr[2])
-        p = BoundaryPayload(rank=rank, kind=kind, b=self.b, a=self.a, fused=self.fused)
+        p = BoundaryPayload(rank=rank, kind=kind, b=self.b, a=self.a, fused=self.fused, sym_flags=int(hdr[3]))
         off = 4
         for name, (r, c) in self._layout():
             count = nbnd if not name.endswith("coupling") else (2 if kind == "middle" else 0)
@@ -174,6 +179,9 @@ class ReducedSystem:
     matrix_b: DeviceBta | None
     provenance: list
     index: dict
+    # backward path for the quadratic solve decided from every rank's check of
+    # B: +1 / -1 when B = +-B^H exactly, 0 otherwise (Context.set_b_symmetry)
+    b_symmetry: int = 0
 
 
 class _Strips:
@@ -248,7 +256,8 @@ def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | Non
              ctypes.byref(wbd) if fused else None, ctypes.byref(fd), ctypes.byref(_sync) if _sync else None)
     record_partition(counter, kind, length, bs, asz, fac.mode, "forward")
     bnd = {"first": [hi - 1], "last": [lo], "middle": [lo, hi - 1]}[kind]
-    pay = BoundaryPayload(rank=rank, kind=kind, b=bs, a=asz, fused=fused)
+    pay = BoundaryPayload(rank=rank, kind=kind, b=bs, a=asz, fused=fused,
+                          sym_flags=ctx.b_symmetry()[0] if fused else 3)
     pay.diag = [WA.diag[g - lo] for g in bnd]
     pay.arrow_row = [WA.arrow_row[g - lo] for g in bnd]
     pay.arrow_col = [WA.arrow_col[g - lo] for g in bnd]
@@ -313,6 +322,10 @@ def _assemble(gathered, a, b, plan: PartitionPlan, tip_sum) -> ReducedSystem:
             return torch.stack([x.to(dev) for x in lst]).contiguous()
         return torch.empty((0,) + shape, dtype=torch.complex128, device=dev)
 
+    flags = 0
+    for pay in gathered:
+        flags |= int(pay.sym_flags)
+    sym = 0 if not fused else (1 if not flags & 1 else -1 if not flags & 2 else 0)
     tip = (a.tip.to(dev) + tip_sum[0]) if asz else torch.empty((0, 0), dtype=torch.complex128, device=dev)
     ra = DeviceBta(nr, bs, asz, {"diag": stack(d, (bs, bs)), "lower": stack(lw, (bs, bs)),
                                  "upper": stack(up, (bs, bs)), "arrow_row": stack(r, (asz, bs)),
@@ -323,7 +336,8 @@ def _assemble(gathered, a, b, plan: PartitionPlan, tip_sum) -> ReducedSystem:
         rb = DeviceBta(nr, bs, asz, {"diag": stack(bd, (bs, bs)), "lower": stack(blw, (bs, bs)),
                                      "upper": stack(bup, (bs, bs)), "arrow_row": stack(br, (asz, bs)),
                                      "arrow_col": stack(bc, (bs, asz)), "tip": btip.contiguous()})
-    return ReducedSystem(matrix_a=ra, matrix_b=rb, provenance=prov, index={key: k for k, key in enumerate(prov)})
+    return ReducedSystem(matrix_a=ra, matrix_b=rb, provenance=prov, index={key: k for k, key in enumerate(prov)},
+                         b_symmetry=sym)
 
 
 def assemble_reduced(coll: Collectives, a, b, plan: PartitionPlan, payload: BoundaryPayload,
@@ -339,7 +353,8 @@ def solve_reduced(reduced: ReducedSystem, mode: str, counter=None, recursive_par
     """Solve the replicated reduced system (dist.py:507-523) on the GPU."""
     if recursive_parts and reduced.matrix_a.n >= 2 * recursive_parts:
         return dist_solve(reduced.matrix_a, reduced.matrix_b, num_parts=recursive_parts, mode=mode)
-    return solve_selected(reduced.matrix_a, reduced.matrix_b if mode == "siq" else None, mode, counter=counter)
+    return solve_selected(reduced.matrix_a, reduced.matrix_b if mode == "siq" else None, mode, counter=counter,
+                          _b_symmetry=reduced.b_symmetry)
 
 
 def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, reduced: ReducedSystem,
@@ -372,8 +387,12 @@ def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, 
     xbd = XB.desc() if fused else None
     ref = lambda x: ctypes.byref(x) if x is not None else None  # noqa: E731
     ctx.bind_stream()
-    ctx.call("bsel_local_backward", ref(ad), ref(bd), ref(fd), ref(wad), ref(wbd), ref(xrd), ref(zrd),
-             k_top, k_bot, int(rank == 0), ref(xad), ref(xbd), ref(_sync))
+    ctx.set_b_symmetry(reduced.b_symmetry)
+    try:
+        ctx.call("bsel_local_backward", ref(ad), ref(bd), ref(fd), ref(wad), ref(wbd), ref(xrd), ref(zrd),
+                 k_top, k_bot, int(rank == 0), ref(xad), ref(xbd), ref(_sync))
+    finally:
+        ctx.set_b_symmetry(ctx.SYM_AUTO)
     record_partition(counter, kind, hi - lo, bs, asz, factors.mode, "backward")
     return out
 

@@ -258,7 +258,7 @@ def release_caches() -> None:
 
 
 def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal_only=False,
-                   out=None, workspace=None, partitions=None) -> SelectedSolution:
+                   out=None, workspace=None, partitions=None, _b_symmetry=None) -> SelectedSolution:
     """Selected inverse of ``a`` and, in fused mode, the selected quadratic
     solution for ``b`` (rgf.py:497-531).  Never mutates its inputs.
 
@@ -308,9 +308,17 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
     bd = B.desc() if fused else None
     xbd = XB.desc() if fused else None
     ctx.bind_stream()
-    ctx.call("bsel_solve_selected", ctypes.byref(ad), ctypes.byref(bd) if fused else None, ctypes.byref(xad),
-             ctypes.byref(xbd) if fused else None, int(bool(diagonal_only)),
-             ctypes.c_void_p(workspace.data_ptr()), workspace.numel())
+    # _b_symmetry (internal): the partitioned solves force the backward path
+    # decided for the whole B; by default the solve uses its own check of B.
+    if _b_symmetry is not None:
+        ctx.set_b_symmetry(_b_symmetry)
+    try:
+        ctx.call("bsel_solve_selected", ctypes.byref(ad), ctypes.byref(bd) if fused else None, ctypes.byref(xad),
+                 ctypes.byref(xbd) if fused else None, int(bool(diagonal_only)),
+                 ctypes.c_void_p(workspace.data_ptr()), workspace.numel())
+    finally:
+        if _b_symmetry is not None:
+            ctx.set_b_symmetry(ctx.SYM_AUTO)
     record_sweep(counter, n, bs, asz, mode, "forward")
     record_sweep(counter, n, bs, asz, mode, "backward")
     if timings is not None:
