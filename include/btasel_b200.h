@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BSEL_ABI_VERSION 2
+#define BSEL_ABI_VERSION 3
 
 typedef enum {
   BSEL_OK = 0,
@@ -74,6 +74,15 @@ typedef struct {
   double* arrow_col_elim;   /* [n][b][a]                                    */
   double* b_arrow_row_elim; /* [n][a][b]   (fused)                          */
   double* b_arrow_col_elim; /* [n][b][a]   (fused)                          */
+  /* Optional (NULL = recomputed by the backward): elimination products the
+   * forward step of block i forms anyway, retained for the backward step of
+   * block i (no reference counterpart):
+   *   elim_f = A(j,i) S_i, elim_g = AR_i S_i,
+   *   elim_q = Bd_i elim_f^H - B(i,j), elim_k = Bd_i elim_g^H - BC_i.        */
+  double* elim_f;           /* [n][b][b]                                    */
+  double* elim_g;           /* [n][a][b]                                    */
+  double* elim_q;           /* [n][b][b]   (fused)                          */
+  double* elim_k;           /* [n][b][a]   (fused)                          */
 } bsel_factors_t;
 
 typedef struct bsel_context bsel_context_t;
@@ -153,6 +162,14 @@ typedef struct {
   double* fill_col;   /* [len][b][b]  (middle)                           */
   double* b_fill_row; /* [len][b][b]  (middle, fused)                    */
   double* b_fill_col; /* [len][b][b]  (middle, fused)                    */
+  /* Optional elimination products (see bsel_factors_t); middle partitions
+   * also elim_fr = fill_row S_i and elim_qr = Bd_i elim_fr^H - b_fill_col.  */
+  double* elim_f;     /* [len][b][b]                                     */
+  double* elim_g;     /* [len][a][b]                                     */
+  double* elim_q;     /* [len][b][b]  (fused)                            */
+  double* elim_k;     /* [len][b][a]  (fused)                            */
+  double* elim_fr;    /* [len][b][b]  (middle)                           */
+  double* elim_qr;    /* [len][b][b]  (middle, fused)                    */
 } bsel_local_factors_t;
 /* Optional end-to-end mode (no reference counterpart; the reference moves
  * whole matrices with cupy before/after its sweeps): the full-size matrices

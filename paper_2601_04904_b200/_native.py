@@ -85,6 +85,10 @@ class Factors(ctypes.Structure):
         ("arrow_col_elim", ctypes.c_void_p),
         ("b_arrow_row_elim", ctypes.c_void_p),
         ("b_arrow_col_elim", ctypes.c_void_p),
+        ("elim_f", ctypes.c_void_p),
+        ("elim_g", ctypes.c_void_p),
+        ("elim_q", ctypes.c_void_p),
+        ("elim_k", ctypes.c_void_p),
     ]
 
 
@@ -126,6 +130,12 @@ class LocalFactors(ctypes.Structure):
         ("fill_col", ctypes.c_void_p),
         ("b_fill_row", ctypes.c_void_p),
         ("b_fill_col", ctypes.c_void_p),
+        ("elim_f", ctypes.c_void_p),
+        ("elim_g", ctypes.c_void_p),
+        ("elim_q", ctypes.c_void_p),
+        ("elim_k", ctypes.c_void_p),
+        ("elim_fr", ctypes.c_void_p),
+        ("elim_qr", ctypes.c_void_p),
     ]
 
 
@@ -197,7 +207,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res
-        if lib.bsel_abi_version() != 2:
+        if lib.bsel_abi_version() != 3:
             raise NativeUnavailableError("ABI version mismatch")
         if path is None:
             _lib = lib

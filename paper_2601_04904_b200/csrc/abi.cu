@@ -95,6 +95,10 @@ FactorsDev to_dev(const bsel_factors_t& f) {
   d.arrow_col_elim = dp(f.arrow_col_elim);
   d.b_arrow_row_elim = dp(f.b_arrow_row_elim);
   d.b_arrow_col_elim = dp(f.b_arrow_col_elim);
+  d.elim_f = dp(f.elim_f);
+  d.elim_g = dp(f.elim_g);
+  d.elim_q = dp(f.elim_q);
+  d.elim_k = dp(f.elim_k);
   return d;
 }
 
@@ -137,7 +141,7 @@ __global__ void axpby_kernel(double2* d, int64_t ldd, const double2* x, int64_t 
 }
 
 struct SolveLayout {
-  size_t off[16];
+  size_t off[17];
   size_t total;
 };
 
@@ -165,7 +169,11 @@ SolveLayout solve_layout(int64_t n, int64_t b, int64_t a, bool fused) {
     take(10, (n - 1) * b * b); // s_b
     take(11, b * b);           // b_diag_last
     take(12, a * a);           // b_tip
+    take(15, n * b * b);       // elim_q
+    take(16, n * b * a);       // elim_k
   }
+  take(13, n * b * b);  // elim_f
+  take(14, n * a * b);  // elim_g
   L.total = cur + 256;
   return L;
 }
@@ -413,6 +421,8 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
     F.tip_inv = at(5);
     F.arrow_row_elim = A.arrow_row;
     F.arrow_col_elim = A.arrow_col;
+    F.elim_f = at(13);
+    F.elim_g = as > 0 ? at(14) : nullptr;
     BtaDev B;
     if (fused) {
       B = to_dev(*b);
@@ -431,6 +441,8 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
       F.b_tip = at(12);
       F.b_arrow_row_elim = B.arrow_row;
       F.b_arrow_col_elim = B.arrow_col;
+      F.elim_q = at(15);
+      F.elim_k = as > 0 ? at(16) : nullptr;
     }
     bta_forward(cx, A, fused ? &B : nullptr, F);
     raise_if_singular(cx, n);
@@ -456,6 +468,12 @@ static LocalFactorsDev to_dev(const bsel_local_factors_t& f, int64_t b, int64_t 
   d.fill_col = dp(f.fill_col);
   d.b_fill_row = dp(f.b_fill_row);
   d.b_fill_col = dp(f.b_fill_col);
+  d.elim_f = dp(f.elim_f);
+  d.elim_g = dp(f.elim_g);
+  d.elim_q = dp(f.elim_q);
+  d.elim_k = dp(f.elim_k);
+  d.elim_fr = dp(f.elim_fr);
+  d.elim_qr = dp(f.elim_qr);
   return d;
 }
 

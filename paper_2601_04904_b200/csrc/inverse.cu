@@ -769,10 +769,28 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     const int cap = grid_req > 0 ? grid_req : inverse_grid_cap();
     if (grid > cap) grid = cap;
     unsigned long long* trace = g_inverse_trace;
-    void* args[] = {(void*)&X, (void*)&ldx, (void*)&Y, (void*)&ldy, (void*)&n,
-                    (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag, (void*)&trace};
-    err = cudaLaunchCooperativeKernel((const void*)persistent_inverse_kernel, grid, 256, args, sizeof(PinvSmem),
-                                      stream);
+    // A plain launch with the kernel's own grid barrier: cooperative launches
+    // from different streams are serialized by the driver, which made the
+    // inverses of concurrent partitions (lanes) wait for each other (SI, 2
+    // lanes: 666 us per inverse vs 284 us alone).  Co-residency still holds:
+    // grid <= the occupancy limit, and every other kernel that can hold the
+    // SMs (GEMM levels) finishes without waiting on the inverse, so all CTAs
+    // of the inverse become resident.  BSEL_INV_COOP=1 restores the
+    // cooperative launch.
+    static const bool coop = [] {
+      const char* e = getenv("BSEL_INV_COOP");
+      return e && atoi(e) != 0;
+    }();
+    if (coop) {
+      void* args[] = {(void*)&X, (void*)&ldx, (void*)&Y, (void*)&ldy, (void*)&n,
+                      (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag, (void*)&trace};
+      err = cudaLaunchCooperativeKernel((const void*)persistent_inverse_kernel, grid, 256, args, sizeof(PinvSmem),
+                                        stream);
+    } else {
+      persistent_inverse_kernel<<<grid, 256, sizeof(PinvSmem), stream>>>(X, ldx, Y, ldy, n, work, gD, barrier, flag,
+                                                                          trace);
+      err = cudaGetLastError();
+    }
     count_launch();
   } else {
     err = levels_inverse(X, ldx, Y, ldy, n, work, flag, stream);

@@ -39,7 +39,10 @@ enum : char { N = 'N', H = 'H' };
 
 class Level {
  public:
-  explicit Level(cudaStream_t s, int tile_cfg = kTileAuto) : s_(s), cfg_(tile_cfg) { b_.nproblems = 0; }
+  explicit Level(cudaStream_t s, int tile_cfg = kTileAuto, int max_ctas = 0) : s_(s), cfg_(tile_cfg) {
+    b_.nproblems = 0;
+    b_.max_ctas = max_ctas;
+  }
   ~Level() noexcept(false) {}
 
   // Start a new output D = (addends) + (terms).

@@ -20,6 +20,19 @@ struct LocalFactorsDev {
   double2* fill_col = nullptr;    // [len][b][b]   (middle)
   double2* b_fill_row = nullptr;  // [len][b][b]   (middle, fused)
   double2* b_fill_col = nullptr;  // [len][b][b]   (middle, fused)
+  // optional retained elimination products (bsel_local_factors_t elim_*)
+  double2* elim_f = nullptr;
+  double2* elim_g = nullptr;
+  double2* elim_q = nullptr;
+  double2* elim_k = nullptr;
+  double2* elim_fr = nullptr;
+  double2* elim_qr = nullptr;
+  Mat EF(int64_t k) const { return elim_f ? blk(elim_f, k, (int)b, (int)b) : Mat{}; }
+  Mat EG(int64_t k) const { return elim_g ? blk(elim_g, k, (int)a, (int)b) : Mat{}; }
+  Mat EQ(int64_t k) const { return elim_q ? blk(elim_q, k, (int)b, (int)b) : Mat{}; }
+  Mat EK(int64_t k) const { return elim_k ? blk(elim_k, k, (int)b, (int)a) : Mat{}; }
+  Mat EFR(int64_t k) const { return elim_fr ? blk(elim_fr, k, (int)b, (int)b) : Mat{}; }
+  Mat EQR(int64_t k) const { return elim_qr ? blk(elim_qr, k, (int)b, (int)b) : Mat{}; }
   Mat SA(int64_t k) const { return blk(s_a, k, (int)b, (int)b); }
   Mat SB(int64_t k) const { return blk(s_b, k, (int)b, (int)b); }
   Mat FR(int64_t k) const { return blk(fill_row, k, (int)b, (int)b); }

@@ -41,6 +41,15 @@ struct FactorsDev {
   double2* arrow_col_elim = nullptr;  // [n][b][a]
   double2* b_arrow_row_elim = nullptr;
   double2* b_arrow_col_elim = nullptr;
+  // optional retained elimination products (bsel_factors_t elim_*)
+  double2* elim_f = nullptr;  // [n][b][b]  A(j,i) S_i
+  double2* elim_g = nullptr;  // [n][a][b]  AR_i S_i
+  double2* elim_q = nullptr;  // [n][b][b]  Bd_i f^H - B(i,j)
+  double2* elim_k = nullptr;  // [n][b][a]  Bd_i g^H - BC_i
+  Mat EF(int64_t i) const { return elim_f ? blk(elim_f, i, (int)b, (int)b) : Mat{}; }
+  Mat EG(int64_t i) const { return elim_g ? blk(elim_g, i, (int)a, (int)b) : Mat{}; }
+  Mat EQ(int64_t i) const { return elim_q ? blk(elim_q, i, (int)b, (int)b) : Mat{}; }
+  Mat EK(int64_t i) const { return elim_k ? blk(elim_k, i, (int)b, (int)a) : Mat{}; }
   Mat SA(int64_t i) const { return blk(s_a, i, (int)b, (int)b); }
   Mat SB(int64_t i) const { return blk(s_b, i, (int)b, (int)b); }
   Mat ARe(int64_t i) const { return blk(arrow_row_elim, i, (int)a, (int)b); }

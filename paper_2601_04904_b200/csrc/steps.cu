@@ -8,6 +8,8 @@
 // (ring_wait), so the B side may lag the A chain by kFwdDepth - 1 steps: the
 // latency-bound chain runs ahead and the B-side GEMM levels fill the SMs it
 // leaves idle.
+#include <cstdlib>
+
 #include "steps.cuh"
 
 namespace bsel {
@@ -19,6 +21,15 @@ constexpr int kBackBase = 16;   // first slot used by back_step (2 x kBackSlots)
 // forward and backward never run concurrently on one context.
 static_assert(kFwdDepth * kRing <= 64, "forward ring exceeds the slot pool");
 Mat rt(Context& ctx, int slot, int k, int r, int c) { return ctx.tmp(slot * kRing + k, r, c); }
+// CTA cap of the forward's aux-stream levels (BSEL_AUX_CTAS, 0 = none): a
+// capped level loops its tiles over fewer CTAs and leaves SMs to the chain.
+int aux_ctas() {
+  static const int cap = [] {
+    const char* e = getenv("BSEL_AUX_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  return cap;
+}
 }  // namespace
 
 cudaEvent_t ring_a_event(Context& ctx, int slot) { return ctx.event(8 + slot); }
@@ -62,7 +73,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     L.out(st.ad_j).add(+1, st.ad_j).mm(-1, st.Lk, N, t1, N);
     L.flush();
     cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
-    Level LB(sB);
+    Level LB(sB, kTileAuto, aux_ctas());
     LB.out(t2).mm(+1, S, N, st.ac_i, N);
     LB.out(st.ar_j).add(+1, st.ar_j).mm(-1, st.ar_i, N, t1, N);
     LB.flush();
@@ -72,8 +83,9 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
     return;
   }
-  Mat f = rt(ctx, slot, 0, b, b), g = rt(ctx, slot, 1, a, b), w = rt(ctx, slot, 2, b, b);
-  Mat k = rt(ctx, slot, 4, b, a), q = rt(ctx, slot, 5, b, b);
+  auto keep = [&](const Mat& m, int k_, int r, int c) { return m.p ? m : rt(ctx, slot, k_, r, c); };
+  Mat f = keep(st.f_out, 0, b, b), g = keep(st.g_out, 1, a, b), w = rt(ctx, slot, 2, b, b);
+  Mat k = keep(st.k_out, 4, b, a), q = keep(st.q_out, 5, b, b);
   {
     Level L(sA);
     L.out(f).mm(+1, st.Lk, N, S, N);
@@ -91,7 +103,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   //   -g BC_i - BR_i g^H + p g^H    = g k - BR_i g^H
   // which also removes the reference's serial chain w -> S_B -> v -> Bd.
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
-  Level L(sB);
+  Level L(sB, kTileAuto, aux_ctas());
   L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(w).mm(+1, S, N, st.bd_i, N);
   L.out(q).add(-1, st.BU).mm(+1, st.bd_i, N, f, H);
@@ -117,7 +129,8 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   const int b = st.ad_i.r, a = st.ar_i.r;
   ctx.invert(st.ad_i, st.S, order, index, sA);
   const Mat& S = st.S;
-  Mat fn = rt(ctx, slot, 0, b, b), fr = rt(ctx, slot, 1, b, b), g = rt(ctx, slot, 2, a, b);
+  auto keep = [&](const Mat& m, int k_, int r, int c) { return m.p ? m : rt(ctx, slot, k_, r, c); };
+  Mat fn = keep(st.fn_out, 0, b, b), fr = keep(st.fr_out, 1, b, b), g = keep(st.g_out, 2, a, b);
   {
     Level L(sA);
     L.out(fn).mm(+1, st.L, N, S, N);
@@ -127,7 +140,7 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     L.flush();
   }
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
-  Level L(sB);
+  Level L(sB, kTileAuto, aux_ctas());
   L.out(fr).mm(+1, st.fill_r, N, S, N);
   L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(st.nfill_c).mm(-1, fn, N, st.fill_c, N);
@@ -137,8 +150,8 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     // Re-associated quadratic updates (see end_step): with
     //   qn = Bd fn^H - BU, qr = Bd fr^H - BFC, kk = Bd g^H - BC_i
     // every B-side output of dist.py:360-396 is two products.
-    w = rt(ctx, slot, 3, b, b), qn = rt(ctx, slot, 4, b, b), qr = rt(ctx, slot, 5, b, b);
-    kk = rt(ctx, slot, 7, b, a);
+    w = rt(ctx, slot, 3, b, b), qn = keep(st.qn_out, 4, b, b), qr = keep(st.qr_out, 5, b, b);
+    kk = keep(st.kk_out, 7, b, a);
     L.out(w).mm(+1, S, N, st.bd_i, N);
     L.out(qn).add(-1, st.BU).mm(+1, st.bd_i, N, fn, H);
   }
@@ -253,9 +266,12 @@ void BackSweep::step(BackStep& st) {
     Level P(sp, cfg_);
     for (int l = 0; l < k; ++l) {
       P.out(h[l]).mm(+1, st.g, N, st.rs[l], N);
-      P.out(c[l]).mm(+1, st.qs[l], N, st.g, N);
+      if (st.cpre[l].p) c[l] = st.cpre[l];
+      else P.out(c[l]).mm(+1, st.qs[l], N, st.g, N);
       if (fused) {
-        P.out(e[l]).mm(+1, st.g, N, st.ss[l], N).mm(-1, st.sc, N, st.qs[l], H);
+        // e_l = g ss_l - sc qs_l^H = -g (Bd c_l^H - ss_l)  (sc = g Bd g^H)
+        if (st.qpre[l].p) P.out(e[l]).mm(-1, st.g, N, st.qpre[l], N);
+        else P.out(e[l]).mm(+1, st.g, N, st.ss[l], N).mm(-1, st.sc, N, st.qs[l], H);
         if (!sym) P.out(f[l]).mm(+1, st.ws[l], N, st.g, H).mm(-1, st.qs[l], N, st.sc, N);
       }
     }

@@ -16,6 +16,9 @@ struct EndStep {
   Mat ad_i, ad_j, ar_i, ar_j, ac_i, ac_j, tipA;
   Mat bd_i, bd_j, br_i, br_j, bc_i, bc_j, tipB;
   Mat S, sb;
+  // optional: retain f = Lk S, g = AR_i S, q = Bd_i f^H - BU, k = Bd_i g^H - BC_i
+  // here (the backward step of block i reuses them) instead of ring slots
+  Mat f_out, g_out, q_out, k_out;
 };
 // Forward ring: temporaries of step k live in ring slot fwd_slot(k); the
 // B side (aux stream) may lag the A chain by up to kFwdDepth - 1 steps.
@@ -35,6 +38,9 @@ struct MiddleStep {
   Mat fill_r, fill_c, bfill_r, bfill_c;
   Mat nfill_r, nfill_c, nbfill_r, nbfill_c;
   Mat S, sb;
+  // optional retained products (see EndStep): fn = L S, fr = fill_r S,
+  // g = AR_i S, qn = Bd fn^H - BU, qr = Bd fr^H - bfill_c, kk = Bd g^H - BC_i
+  Mat fn_out, fr_out, g_out, qn_out, qr_out, kk_out;
 };
 void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int slot);
 
@@ -54,6 +60,9 @@ struct BackStep {
   Mat g, sc;
   Mat rs[3], qs[3], ss[3], ws[3];
   Mat ya[3][3], yb[3][3];
+  // optional products retained by the forward step of this block:
+  // cpre[l] = qs_l g, qpre[l] = Bd (qs_l g)^H - ss_l  (then e_l = -g qpre[l])
+  Mat cpre[3], qpre[3];
   // outputs
   Mat row[3], col[3], diag;
   Mat zrow[3], zcol[3], zdiag;

@@ -217,7 +217,7 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
   ctx.reserve_slots(8, (int64_t)b * b);
   for (int i = 0; i < n - 1; ++i) {
     const int r = (i & 1) * 4;
-    Mat S = F.SA(i), t1 = ctx.tmp(r + 0, b, b);
+    Mat S = F.SA(i), t1 = F.elim_f ? F.EF(i) : ctx.tmp(r + 0, b, b);
     ctx.invert(A.D(i), S, i, i, sA);
     if (fused && i >= 2) cuda_check(cudaStreamWaitEvent(sA, ctx.event(2 + (i & 1)), 0), "wait B");
     {
@@ -235,7 +235,7 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
       cuda_check(cudaStreamWaitEvent(sB, ctx.event(i & 1), 0), "wait A");
       // v L^H - t1 BU = L S_B L^H - t1 BU = t1 (Bd t1^H - BU): two levels,
       // one product fewer than rgf.py:113-118.
-      Mat w = ctx.tmp(r + 1, b, b), q = ctx.tmp(r + 2, b, b), sb = F.SB(i);
+      Mat w = ctx.tmp(r + 1, b, b), q = F.elim_q ? F.EQ(i) : ctx.tmp(r + 2, b, b), sb = F.SB(i);
       Level L(sB);
       L.out(w).mm(+1, S, N, B->D(i), N);
       L.out(q).add(-1, B->U(i)).mm(+1, B->D(i), N, t1, H);
@@ -274,6 +274,7 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
       st.bd_i = B->D(i), st.bd_j = B->D(i + 1), st.br_i = B->AR(i), st.br_j = B->AR(i + 1);
       st.bc_i = B->AC(i), st.bc_j = B->AC(i + 1), st.tipB = B->T();
       st.sb = F.SB(i);
+      st.f_out = F.EF(i), st.g_out = F.EG(i), st.q_out = F.EQ(i), st.k_out = F.EK(i);
     }
     end_step(ctx, st, fused, i, i, fwd_slot(i));
   }
@@ -352,6 +353,7 @@ void bt_backward(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDe
     if (fused) {
       st.sc = F.SB(i);
       st.ss[0] = B->U(i), st.ws[0] = B->L(i);
+      st.cpre[0] = F.EF(i), st.qpre[0] = F.EQ(i);
       st.yb[0][0] = XB->D(i + 1);
       if (!diag_only) st.zrow[0] = XB->U(i), st.zcol[0] = XB->L(i);
       st.zdiag = XB->D(i);
@@ -408,6 +410,7 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
       st.row[1] = XA.AC(i), st.col[1] = XA.AR(i);
       if (fused) {
         st.sc = F.SB(i);
+        st.cpre[0] = F.EF(i), st.cpre[1] = F.EG(i), st.qpre[0] = F.EQ(i), st.qpre[1] = F.EK(i);
         st.ss[0] = B->U(i), st.ss[1] = F.BCe(i);
         st.ws[0] = B->L(i), st.ws[1] = F.BRe(i);
         st.yb[0][0] = XB->D(i + 1), st.yb[0][1] = XB->AC(i + 1), st.yb[1][0] = XB->AR(i + 1);

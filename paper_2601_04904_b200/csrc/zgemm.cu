@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const int wm = warp / C::WN;
   const int wn = warp % C::WN;
 
+  for (int bid = blockIdx.x; bid < batch.total_tiles; bid += gridDim.x) {
+  if (bid != (int)blockIdx.x) __syncthreads();  // previous tile's readers of the stages are done
   // Locate the problem / tile of this CTA.
-  const int bid = blockIdx.x;
   int pi = 0;
   while (pi + 1 < batch.nproblems && bid >= batch.p[pi + 1].tile_begin) ++pi;
   const GemmProblem& P = batch.p[pi];
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       P.D[(int64_t)m * P.ldd + n] = make_double2(re, imv);
     }
   }
+  }  // tile loop
 }
 
 template <class C>
@@ -304,7 +306,8 @@ cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
     }
     prof = profile_open(stream);
   }
-  zgemm_grouped_kernel<C><<<tiles, C::THREADS, C::SMEM, stream>>>(batch);
+  const int grid = batch.max_ctas > 0 && batch.max_ctas < tiles ? batch.max_ctas : tiles;
+  zgemm_grouped_kernel<C><<<grid, C::THREADS, C::SMEM, stream>>>(batch);
   count_launch();
   profile_close(prof, stream, 0, flops, bytes);
   return cudaGetLastError();
@@ -322,6 +325,7 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 struct ProfRec {
   cudaEvent_t t0, t1;
+  cudaStream_t stream;
   int kind;
   double flops;
   double bytes;
@@ -356,6 +360,7 @@ int profile_open(cudaStream_t s) {
     g_prof.push_back(r);
   }
   const int id = (int)g_prof_used++;
+  g_prof[id].stream = s;
   cudaEventRecord(g_prof[id].t0, s);
   return id;
 }
@@ -374,6 +379,9 @@ ProfileTotals profile_end() {
   // Spans relative to the base event; busy time = union of the spans of one
   // kind (launches of concurrent streams overlap).
   std::vector<std::pair<float, float>> spans[2];
+  // BSEL_PROFILE_DUMP=path: every launch as "kind,stream,start_ms,end_ms,flops" (timeline analysis)
+  static const char* dump_path = getenv("BSEL_PROFILE_DUMP");
+  FILE* dump = dump_path ? fopen(dump_path, "w") : nullptr;
   for (size_t i = 0; i < g_prof_used; ++i) {
     float ms = 0.f, s0 = 0.f, s1 = 0.f;
     cudaEventElapsedTime(&ms, g_prof[i].t0, g_prof[i].t1);
@@ -381,6 +389,8 @@ ProfileTotals profile_end() {
     cudaEventElapsedTime(&s1, g_prof_base, g_prof[i].t1);
     const int kind = g_prof[i].kind == 0 ? 0 : 1;
     spans[kind].emplace_back(s0, s1);
+    if (dump)
+      fprintf(dump, "%d,%p,%.4f,%.4f,%.6g\n", kind, (void*)g_prof[i].stream, s0, s1, g_prof[i].flops);
     if (kind == 0) {
       ++t.gemm_launches;
       t.gemm_flops += g_prof[i].flops;
@@ -407,6 +417,7 @@ ProfileTotals profile_end() {
     }
     if (cur1 > cur0) busy[k] += cur1 - cur0;
   }
+  if (dump) fclose(dump);
   t.gemm_busy_ms = busy[0];
   t.inverse_busy_ms = busy[1];
   g_prof_on = false;

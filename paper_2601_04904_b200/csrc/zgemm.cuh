@@ -62,6 +62,10 @@ struct GemmProblem {
 struct GemmBatch {
   int32_t nproblems;
   int32_t total_tiles;
+  // > 0: launch at most max_ctas CTAs that loop over the tiles (leaves SMs
+  // free for a concurrent latency-critical chain); 0: one CTA per tile
+  int32_t max_ctas;
+  int32_t pad_;
   GemmProblem p[kMaxProblems];
 };
 

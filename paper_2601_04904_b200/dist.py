@@ -165,7 +165,8 @@ class LocalFactors:
     def desc(self) -> _native.LocalFactors:
         f = _native.LocalFactors()
         f.lo, f.hi, f.kind, f.fused = self.lo, self.hi, _KIND_CODES[self.kind], int(self.mode == "siq")
-        for k in ("s_a", "s_b", "fill_row", "fill_col", "b_fill_row", "b_fill_col"):
+        for k in ("s_a", "s_b", "fill_row", "fill_col", "b_fill_row", "b_fill_col", "elim_f", "elim_g", "elim_q",
+                  "elim_k", "elim_fr", "elim_qr"):
             t = self.tensors.get(k)
             setattr(f, k, t.data_ptr() if (t is not None and t.numel()) else None)
         return f
@@ -219,14 +220,21 @@ def _alloc_factors(kind, lo, hi, fused, bs, asz, dev) -> "LocalFactors":
     length = hi - lo
     c128 = dict(dtype=torch.complex128, device=dev)
     t = {"s_a": torch.empty((length, bs, bs), **c128)}
+    # elimination products retained for the backward (bsel_local_factors_t)
+    t["elim_f"] = torch.empty((length, bs, bs), **c128)
+    t["elim_g"] = torch.empty((length, asz, bs), **c128)
     if fused:
         t["s_b"] = torch.empty((length, bs, bs), **c128)
+        t["elim_q"] = torch.empty((length, bs, bs), **c128)
+        t["elim_k"] = torch.empty((length, bs, asz), **c128)
     if kind == "middle":
         t["fill_row"] = torch.empty((length, bs, bs), **c128)
         t["fill_col"] = torch.empty((length, bs, bs), **c128)
+        t["elim_fr"] = torch.empty((length, bs, bs), **c128)
         if fused:
             t["b_fill_row"] = torch.empty((length, bs, bs), **c128)
             t["b_fill_col"] = torch.empty((length, bs, bs), **c128)
+            t["elim_qr"] = torch.empty((length, bs, bs), **c128)
     return LocalFactors(kind=kind, lo=lo, hi=hi, mode="siq" if fused else "si", tensors=t,
                         work_a=_Strips(length, bs, asz, dev), work_b=_Strips(length, bs, asz, dev) if fused else None)
 

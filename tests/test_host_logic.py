@@ -129,7 +129,7 @@ def test_library_exports_every_header_symbol():
     assert set(declared) == set(_native.EXPORTS)
     for sym in declared:
         assert hasattr(lib, sym), sym
-    assert lib.bsel_abi_version() == 2
+    assert lib.bsel_abi_version() == 3
 
 
 def test_abi_struct_layouts():
