@@ -135,15 +135,37 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(n_s, b, a, threads=None):
-    """Time the CPU reference path (oracle port of btasel, NumPy/SciPy on the
-    host BLAS) on an n_s-block sample of the workload.  Returns seconds."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_impl():
+    """(module, kind): the unmodified reference btasel installed in
+    baseline/_ref (pip install --target, see DESIGN.md 5) -> "reference";
+    otherwise the oracle port (oracle/, same NumPy/SciPy arithmetic) ->
+    "port"."""
+    if os.path.isdir(os.path.join(REF_DIR, "btasel")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        try:
+            import btasel
+
+            return btasel, "reference"
+        except Exception:  # pragma: no cover - broken install
+            pass
     import oracle  # CPU baseline leg only
 
-    A = oracle.generate_dd_bta(n_s, b, a, seed=0)
-    B = oracle.hermitianize(oracle.generate_dd_bta(n_s, b, a, seed=1))
+    return oracle, "port"
+
+
+def cpu_sample(n_s, b, a, threads=None):
+    """Time the CPU reference path (btasel solve_selected, or its oracle port,
+    NumPy/SciPy on the host BLAS) on an n_s-block sample of the workload with
+    the reference bench protocol inputs (bench.py:202-203).  Returns seconds."""
+    ref, _ = reference_impl()
+    A = ref.generate_dd_bta(n_s, b, a, seed=0)
+    B = ref.hermitianize(ref.generate_dd_bta(n_s, b, a, seed=1))
     t0 = time.perf_counter()
-    oracle.solve_selected(A, B, "siq")
+    ref.solve_selected(A, B, "siq")
     return time.perf_counter() - t0
 
 
@@ -164,7 +186,9 @@ def run_reference(args, n, b, a):
         cpu_sample(n_s, b, a)
     times = [cpu_sample(n_s, b, a) for _ in range(args.steps)]
     per = statistics.mean(times) / n_s * n * 1e3
-    sample = (f"oracle port of btasel solve_selected (NumPy/SciPy, OpenBLAS default threads) on "
+    _, kind = reference_impl()
+    what = ("unmodified reference btasel (baseline/_ref)" if kind == "reference" else "oracle port of btasel")
+    sample = (f"{what} solve_selected (NumPy/SciPy, OpenBLAS default threads) on "
               f"n={n_s} of {n} blocks (b={b}, a={a}), extrapolated linearly in n (reference acceptance "
               f"criterion 7)")
     cores = host_cores()
@@ -173,7 +197,7 @@ def run_reference(args, n, b, a):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": args.workload, "n_blocks": n, "block": b, "tip": a, "mode": "siq"},
-        "cpu_baseline": {"value": per, "unit": "ms", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": per, "unit": "ms", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": per, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -467,8 +491,10 @@ def main():
     if not args.no_cpu and world == 1 and rank == 0:
         n_s = args.cpu_sample_n
         t_s = cpu_sample(n_s, b, a)
-        cpu = {"value": t_s / n_s * n * 1e3, "unit": "ms", "cores": host_cores(), "kind": "port",
-               "sample": f"oracle port (NumPy/SciPy, OpenBLAS default threads) solve_selected on n={n_s} of "
+        _, kind = reference_impl()
+        what = "reference btasel (baseline/_ref)" if kind == "reference" else "oracle port"
+        cpu = {"value": t_s / n_s * n * 1e3, "unit": "ms", "cores": host_cores(), "kind": kind,
+               "sample": f"{what} (NumPy/SciPy, OpenBLAS default threads) solve_selected on n={n_s} of "
                          f"{n} blocks (b={b}, a={a}) took {t_s:.2f} s; extrapolated linearly in n"}
 
     if rank == 0:

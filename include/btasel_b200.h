@@ -83,6 +83,7 @@ typedef struct {
   double* elim_g;           /* [n][a][b]                                    */
   double* elim_q;           /* [n][b][b]   (fused)                          */
   double* elim_k;           /* [n][b][a]   (fused)                          */
+  double* elim_h;           /* [n][b][b]   S_i A(i,j)                       */
 } bsel_factors_t;
 
 typedef struct bsel_context bsel_context_t;
@@ -170,6 +171,7 @@ typedef struct {
   double* elim_k;     /* [len][b][a]  (fused)                            */
   double* elim_fr;    /* [len][b][b]  (middle)                           */
   double* elim_qr;    /* [len][b][b]  (middle, fused)                    */
+  double* elim_h;     /* [len][b][b]  S_i U_i (U = the coupling eliminated along) */
 } bsel_local_factors_t;
 /* Optional end-to-end mode (no reference counterpart; the reference moves
  * whole matrices with cupy before/after its sweeps): the full-size matrices

@@ -89,6 +89,7 @@ class Factors(ctypes.Structure):
         ("elim_g", ctypes.c_void_p),
         ("elim_q", ctypes.c_void_p),
         ("elim_k", ctypes.c_void_p),
+        ("elim_h", ctypes.c_void_p),
     ]
 
 
@@ -136,6 +137,7 @@ class LocalFactors(ctypes.Structure):
         ("elim_k", ctypes.c_void_p),
         ("elim_fr", ctypes.c_void_p),
         ("elim_qr", ctypes.c_void_p),
+        ("elim_h", ctypes.c_void_p),
     ]
 
 

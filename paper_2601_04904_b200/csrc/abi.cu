@@ -99,6 +99,7 @@ FactorsDev to_dev(const bsel_factors_t& f) {
   d.elim_g = dp(f.elim_g);
   d.elim_q = dp(f.elim_q);
   d.elim_k = dp(f.elim_k);
+  d.elim_h = dp(f.elim_h);
   return d;
 }
 
@@ -141,7 +142,7 @@ __global__ void axpby_kernel(double2* d, int64_t ldd, const double2* x, int64_t 
 }
 
 struct SolveLayout {
-  size_t off[17];
+  size_t off[18];
   size_t total;
 };
 
@@ -174,6 +175,7 @@ SolveLayout solve_layout(int64_t n, int64_t b, int64_t a, bool fused) {
   }
   take(13, n * b * b);  // elim_f
   take(14, n * a * b);  // elim_g
+  take(17, n * b * b);  // elim_h
   L.total = cur + 256;
   return L;
 }
@@ -423,6 +425,7 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
     F.arrow_col_elim = A.arrow_col;
     F.elim_f = at(13);
     F.elim_g = as > 0 ? at(14) : nullptr;
+    F.elim_h = at(17);
     BtaDev B;
     if (fused) {
       B = to_dev(*b);
@@ -474,6 +477,7 @@ static LocalFactorsDev to_dev(const bsel_local_factors_t& f, int64_t b, int64_t 
   d.elim_k = dp(f.elim_k);
   d.elim_fr = dp(f.elim_fr);
   d.elim_qr = dp(f.elim_qr);
+  d.elim_h = dp(f.elim_h);
   return d;
 }
 

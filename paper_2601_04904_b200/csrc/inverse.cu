@@ -1,4 +1,5 @@
 // Complex128 block inverse (see inverse.cuh).
+#include <algorithm>
 #include <cstdlib>
 
 #include "inverse.cuh"
@@ -177,11 +178,10 @@ __global__ void __launch_bounds__(256)
 
 // Exact fallback: full-column partial-pivoting Gauss-Jordan in global memory
 // (one CTA).  Runs only when the fast path flagged a zero leaf pivot.
-__global__ void __launch_bounds__(1024)
-    exact_inverse_kernel(const double2* __restrict__ X, int64_t ldx, double2* __restrict__ Y, int64_t ldy,
+// Returns false (flag = 2 + row, status updated) if exactly singular.
+__device__ bool exact_gj(const double2* __restrict__ X, int64_t ldx, double2* __restrict__ Y, int64_t ldy,
                          int n, double2* __restrict__ S, int* flag, unsigned long long* status,
                          unsigned long long key) {
-  if (*flag != 1) return;  // only after a fast-path zero pivot
   extern __shared__ unsigned char smem_raw[];
   double2* fcol = reinterpret_cast<double2*>(smem_raw);
   double2* prow = fcol + n;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(1024)
         *flag = 2 + k;
         if (status) atomicMin(status, key);
       }
-      return;
+      return false;
     }
     const int p = s_p;
     const double2 inv = s_inv;
@@ -273,7 +273,54 @@ __global__ void __launch_bounds__(1024)
     int r = (int)(e / n), k = (int)(e % n);
     Y[(int64_t)r * ldy + piv[k]] = S[(int64_t)piv[r] * n + k];
   }
-  if (tid == 0) *flag = 0;  // fast path failed, exact path succeeded
+  __syncthreads();
+  return true;
+}
+
+__global__ void __launch_bounds__(1024)
+    exact_inverse_kernel(const double2* __restrict__ X, int64_t ldx, double2* __restrict__ Y, int64_t ldy,
+                         int n, double2* __restrict__ S, int* flag, unsigned long long* status,
+                         unsigned long long key) {
+  if (*flag != 1) return;  // only after a fast-path zero pivot
+  if (exact_gj(X, ldx, Y, ldy, n, S, flag, status, key) && threadIdx.x == 0) *flag = 0;
+}
+
+// Schur step fallback: exact inverse, then H = S U, F = L S, C -= F U by plain
+// loops (one CTA; only runs when a leaf met an exactly zero pivot, in which
+// case the fast kernel left C untouched).
+__global__ void __launch_bounds__(1024)
+    exact_schur_kernel(const double2* __restrict__ D, int64_t ldd, const double2* __restrict__ U, int64_t ldu,
+                       const double2* __restrict__ Lm, int64_t ldl, double2* C, int64_t ldc, double2* Sout,
+                       int64_t lds, double2* H, int64_t ldh, double2* F, int64_t ldf, int n, double2* scratch,
+                       int* flag, unsigned long long* status, unsigned long long key) {
+  if (*flag != 1) return;
+  if (!exact_gj(D, ldd, Sout, lds, n, scratch, flag, status, key)) return;
+  __threadfence_block();
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e % n);
+    double2 h = make_double2(0.0, 0.0), f = make_double2(0.0, 0.0);
+    for (int k = 0; k < n; ++k) {
+      const double2 s1 = Sout[(int64_t)r * lds + k], u = U[(int64_t)k * ldu + c];
+      const double2 l = Lm[(int64_t)r * ldl + k], s2 = Sout[(int64_t)k * lds + c];
+      h.x += s1.x * u.x - s1.y * u.y, h.y += s1.x * u.y + s1.y * u.x;
+      f.x += l.x * s2.x - l.y * s2.y, f.y += l.x * s2.y + l.y * s2.x;
+    }
+    H[(int64_t)r * ldh + c] = h;
+    F[(int64_t)r * ldf + c] = f;
+  }
+  __threadfence_block();
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e % n);
+    double2 v = C[(int64_t)r * ldc + c];
+    for (int k = 0; k < n; ++k) {
+      const double2 f = F[(int64_t)r * ldf + k], u = U[(int64_t)k * ldu + c];
+      v.x -= f.x * u.x - f.y * u.y, v.y -= f.x * u.y + f.y * u.x;
+    }
+    C[(int64_t)r * ldc + c] = v;
+  }
+  if (threadIdx.x == 0) *flag = 0;
 }
 
 constexpr int kLeafThreads = 256;
@@ -402,14 +449,30 @@ __device__ void leaf_publish(Leaf32& L, const double2* W, int64_t ld, int j0, in
   __syncthreads();
 }
 
+// A square matrix of 1 x 1 or 2 x 2 quadrants of b x b blocks at separate
+// addresses (quadrant (r, c) at index 2r + c).  Tile (ti, tk) of the tile grid
+// (nq*ntq x nq*ntq, ntq = ceil(b/32) tiles per quadrant side) never straddles
+// quadrants; edge tiles of each quadrant are partial.
+struct Quad {
+  double2* p[4];
+  int64_t ld[4];
+};
+
 struct TileCtx {
-  int n, nt, p, j0, jb;
-  const double2* Wc;
-  int64_t ldc;
-  double2* Wn;
-  int64_t ldn;
+  int b, ntq, nt, p, j0, jb;
+  const Quad* Wc;  // current (in the __grid_constant__ kernel parameters)
+  const Quad* Wn;  // next
+  bool final_;      // this panel writes the caller's outputs
+  bool skip_c;      // final: leave quadrant 3 untouched (fallback recomputes it)
   int r_tk;  // column tile whose R = Dinv W[J,K] is cached in S.r
   unsigned long long* trace;  // debug (may be null)
+  __device__ int quad(int ti, int tk) const { return 2 * (ti / ntq) + (tk / ntq); }
+  __device__ int ext(int t) const { return min(kT, b - (t % ntq) * kT); }  // valid rows / cols of tile t
+  __device__ double2* at(const Quad* Q, int ti, int tk) const {
+    const int q = quad(ti, tk);
+    return Q->p[q] + (int64_t)((ti % ntq) * kT) * Q->ld[q] + (tk % ntq) * kT;
+  }
+  __device__ int64_t ld(const Quad* Q, int ti, int tk) const { return Q->ld[quad(ti, tk)]; }
 };
 
 // Issue the asynchronous operand loads of output tile t into buffer `buf`:
@@ -421,27 +484,27 @@ struct TileIssue {
 };
 __device__ __forceinline__ TileIssue issue_tile(PinvSmem& S, const TileCtx& T, int t, int buf, int& issued_r_tk) {
   const int tk = t / T.nt, ti = t % T.nt, p = T.p;
-  const int i0 = ti * kT, k0 = tk * kT;
-  const int ib = min(kT, T.n - i0), kb = min(kT, T.n - k0);
+  const int ib = T.ext(ti), kb = T.ext(tk);
   TileIssue is;
   is.has_x = false;
   // Epilogue operands first: their L2 latency overlaps everything until the
   // tile's DMMA is done.
   const bool addend = ti != p && tk != p;
   const int orow = acc_row();
+  const double2* wik = T.at(T.Wc, ti, tk);
+  const int64_t ldik = T.ld(T.Wc, ti, tk);
 #pragma unroll
   for (int jn = 0; jn < 4; ++jn) {
     const int oc = acc_col(jn);
-    is.w[jn] = (addend && orow < ib && oc < kb) ? ldcg2(T.Wc + (int64_t)(i0 + orow) * T.ldc + k0 + oc)
-                                                : make_double2(0.0, 0.0);
+    is.w[jn] = (addend && orow < ib && oc < kb) ? ldcg2(wik + (int64_t)orow * ldik + oc) : make_double2(0.0, 0.0);
   }
   if (!(ti == p && tk == p)) {
     if (tk != p && tk != issued_r_tk) {
-      load_tile_async(S.x[buf], T.Wc + (int64_t)T.j0 * T.ldc + k0, T.ldc, T.jb, kb);
+      load_tile_async(S.x[buf], T.at(T.Wc, p, tk), T.ld(T.Wc, p, tk), T.jb, kb);
       is.has_x = true;
       issued_r_tk = tk;
     }
-    if (ti != p) load_tile_async(S.c[buf], T.Wc + (int64_t)i0 * T.ldc + T.j0, T.ldc, ib, T.jb);
+    if (ti != p) load_tile_async(S.c[buf], T.at(T.Wc, ti, p), T.ld(T.Wc, ti, p), ib, T.jb);
   }
   inv_cp_commit();
   return is;
@@ -450,15 +513,20 @@ __device__ __forceinline__ TileIssue issue_tile(PinvSmem& S, const TileCtx& T, i
 // Compute output tile t from buffer `buf` (its loads have landed).
 __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int buf, const TileIssue& is) {
   const int tk = t / T.nt, ti = t % T.nt, p = T.p;
-  const int i0 = ti * kT, k0 = tk * kT;
-  const int ib = min(kT, T.n - i0), kb = min(kT, T.n - k0);
-  double2* out = T.Wn + (int64_t)i0 * T.ldn + k0;
+  const int ib = T.ext(ti), kb = T.ext(tk);
+  const int q = T.quad(ti, tk);
+  double2* out = T.at(T.Wn, ti, tk);
+  const int64_t ldn = T.ld(T.Wn, ti, tk);
+  // final panel: quadrant 2 receives -(-L D^-1) = L D^-1; quadrant 3 is kept
+  // when the exact fallback will recompute it
+  const bool skip = T.final_ && T.skip_c && q == 3;
+  const double sg = (T.final_ && q == 2) ? -1.0 : 1.0;
   const int orow = acc_row();
   double acc[4][2];
   if (ti == p && tk == p) {
     for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
       const int i = e >> 5, j = e & 31;
-      if (i < ib && j < kb) out[(int64_t)i * T.ldn + j] = S.d[i][j];
+      if (i < ib && j < kb) out[(int64_t)i * ldn + j] = S.d[i][j];
     }
     return;
   }
@@ -473,22 +541,20 @@ __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int
   if (ti == p) {  // W'[J,K] = R
     for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
       const int i = e >> 5, j = e & 31;
-      if (i < ib && j < kb) out[(int64_t)i * T.ldn + j] = S.r[i][j];
+      if (i < ib && j < kb) out[(int64_t)i * ldn + j] = S.r[i][j];
     }
     return;
   }
   tile_mma(acc, S.c[buf], tk == p ? S.d : S.r);
+  if (skip) return;
 #pragma unroll
   for (int jn = 0; jn < 4; ++jn) {
     const int oc = acc_col(jn);
-    if (orow < ib && oc < kb) out[(int64_t)orow * T.ldn + oc] = make_double2(is.w[jn].x - acc[jn][0], is.w[jn].y - acc[jn][1]);
+    if (orow < ib && oc < kb)
+      out[(int64_t)orow * ldn + oc] = make_double2(sg * (is.w[jn].x - acc[jn][0]), sg * (is.w[jn].y - acc[jn][1]));
   }
-
 }
 
-// Output tiles [t0, t1) of the Gauss-Jordan update of panel p (tile `skip`
-// excluded), software pipelined: the operands of the next tile stream in
-// (cp.async, double buffered) while the current one computes.
 // One pipeline stage: wait for tile t's operands (slot B), start tile tn's
 // loads into slot B ^ 1, compute t.  B is a template constant so the two
 // in-flight TileIssue register sets never have to be copied (a copy would
@@ -538,58 +604,76 @@ __device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
   }
 }
 
+// Persistent blocked Gauss-Jordan over the pivot columns of quadrant 0:
+// nq = 1: Y = inv(X).  nq = 2: the Schur step of the forward sweep,
+//   [[D, U], [L, C]] -> [[D^-1, D^-1 U], [L D^-1, C - L D^-1 U]]
+// (pivot rows and columns only in D; the L rows and U columns are eliminated
+// along, so the chain's two GEMMs f = L S, C -= f U become part of the GJ
+// panel updates, which overlap the latency-bound leaf factorizations).
+// Buffers: panel 0 reads IN; the last panel writes OUT; the panels before it
+// alternate between B (last-but-one) and A.  A may share quadrants with OUT
+// except the one OUT shares with IN (C, updated in place).
 // Lookahead: during panel p, CTA 0 first computes the next diagonal tile
 // W'[p+1,p+1], immediately factors it and publishes Dinv_{p+1} (double-
 // buffered gD) while the other CTAs update the rest -> one grid barrier per
 // panel, the leaf latency hidden behind the update.
-// launch_bounds(256, 2): <= 128 registers, so an inverse CTA can share an SM
-// with a GEMM CTA of the concurrent sweeps (at 200 registers it needed an SM
-// of its own and the chain waited for GEMM tails to drain).
-__global__ void __launch_bounds__(256, 2)
-    persistent_inverse_kernel(const double2* __restrict__ X, int64_t ldx, double2* Y, int64_t ldy, int n,
-                              double2* work, double2* gD, unsigned* barrier, int* flag,
-                              unsigned long long* trace) {
+// launch_bounds(256, 2): <= 128 registers, so a CTA can share an SM with a
+// GEMM CTA of the concurrent sweeps.
+struct GjArgs {
+  Quad in, out, a, bq;
+  int b, nq;
+  double2* gD;
+  unsigned* barrier;
+  int* flag;
+  unsigned long long* trace;
+};
+
+__global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_constant__ GjArgs g) {
   // trace (debug, may be null): per panel p, [8p+0] CTA0 start, [+1] after the
   // lookahead tile, [+2] after the leaf, [+3] CTA0 at barrier, [+4] CTA1 done
   // with its tiles, [+5] CTA1 after barrier (globaltimer ns).
   auto stamp = [&](int slot) {
-    if (trace && threadIdx.x == 0) {
+    if (g.trace && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[slot] = t;
+      g.trace[slot] = t;
     }
   };
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
   Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0][0]);  // spans x[0] and x[1]
-  const int nt = (n + kT - 1) / kT, ntiles = nt * nt, G = gridDim.x;
+  const int b = g.b, ntq = (b + kT - 1) / kT, nt = g.nq * ntq, ntiles = nt * nt, G = gridDim.x;
   unsigned target = 0;
-  if (blockIdx.x == 0) leaf_publish(L, X, ldx, 0, min(kT, n), gD, flag);
+  if (blockIdx.x == 0) leaf_publish(L, g.in.p[0], g.in.ld[0], 0, min(kT, b), g.gD, g.flag);
   target += G;
-  grid_barrier(barrier, target);
+  grid_barrier(g.barrier, target);
   TileCtx T;
-  T.trace = trace;
-  T.n = n;
+  T.trace = g.trace;
+  T.b = b;
+  T.ntq = ntq;
   T.nt = nt;
-  T.Wc = X;
-  T.ldc = ldx;
+  T.Wc = &g.in;
   const int workers = G > 1 ? G - 1 : 1, wid = G > 1 ? (int)blockIdx.x - 1 : 0;
-  for (int p = 0; p < nt; ++p) {
+  for (int p = 0; p < ntq; ++p) {
     T.p = p;
     T.j0 = p * kT;
-    T.jb = min(kT, n - T.j0);
-    T.Wn = ((nt - 1 - p) % 2 == 0) ? Y : work;
-    T.ldn = (T.Wn == Y) ? ldy : n;
+    T.jb = min(kT, b - T.j0);
+    const int rem = ntq - 1 - p;  // panels after this one
+    T.final_ = rem == 0;
+    T.Wn = rem == 0 ? &g.out : (rem % 2 == 1 ? &g.bq : &g.a);
+    // every leaf (the last one was factored during panel ntq-2) has reported
+    T.skip_c = T.final_ && g.nq == 2 && *reinterpret_cast<volatile int*>(g.flag) != 0;
     T.r_tk = -1;
-    load_tile(S.d, gD + (p & 1) * kT * kT, kT, kT, kT);
+    load_tile(S.d, g.gD + (p & 1) * kT * kT, kT, kT, kT);
     __syncthreads();
-    const int sp = (p + 1 < nt) ? (p + 1) * nt + (p + 1) : -1;
+    const int sp = (p + 1 < ntq) ? (p + 1) * nt + (p + 1) : -1;
     if (blockIdx.x == 0) stamp(8 * p + 0);
     if (blockIdx.x == 0 && sp >= 0) {
       gj_tiles(S, T, sp, sp + 1, -1);
       __syncthreads();
       stamp(8 * p + 1);
-      leaf_publish(L, T.Wn, T.ldn, (p + 1) * kT, min(kT, n - (p + 1) * kT), gD + ((p + 1) & 1) * kT * kT, flag);
+      leaf_publish(L, T.at(T.Wn, p + 1, p + 1), T.ld(T.Wn, p + 1, p + 1), 0, min(kT, b - (p + 1) * kT),
+                   g.gD + ((p + 1) & 1) * kT * kT, g.flag);
       stamp(8 * p + 2);
     }
     if (G == 1 || blockIdx.x > 0) {
@@ -600,10 +684,9 @@ __global__ void __launch_bounds__(256, 2)
     if (blockIdx.x == 0) stamp(8 * p + 3);
     if (blockIdx.x == 1) stamp(8 * p + 4);
     target += G;
-    grid_barrier(barrier, target);
+    grid_barrier(g.barrier, target);
     if (blockIdx.x == 1) stamp(8 * p + 5);
     T.Wc = T.Wn;
-    T.ldc = T.ldn;
   }
 }
 
@@ -633,9 +716,9 @@ int coop_grid_limit() {
     int dev = 0, coop = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    if (cudaFuncSetAttribute(persistent_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(persistent_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(PinvSmem)) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persistent_inverse_kernel, 256,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persistent_gj_kernel, 256,
                                                       sizeof(PinvSmem)) != cudaSuccess)
       per_sm = 0;
     return coop ? per_sm * device_sm_count() : 0;
@@ -754,6 +837,57 @@ cudaError_t levels_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ld
 
 }  // namespace
 
+namespace {
+Quad quad1(const double2* p, int64_t ld) {
+  Quad q{};
+  q.p[0] = const_cast<double2*>(p);
+  q.ld[0] = ld;
+  return q;
+}
+
+cudaError_t launch_gj(GjArgs& g, int grid, cudaStream_t stream) {
+  if ((cudaError_t)cudaMemsetAsync(g.barrier, 0, sizeof(unsigned), stream) != cudaSuccess) return cudaGetLastError();
+  // A plain launch with the kernel's own grid barrier: cooperative launches
+  // from different streams are serialized by the driver, which made the
+  // inverses of concurrent partitions (lanes) wait for each other (SI, 2
+  // lanes: 666 us per inverse vs 284 us alone).  Co-residency still holds:
+  // grid <= the occupancy limit, and every other kernel that can hold the
+  // SMs (GEMM levels) finishes without waiting on this one, so all its CTAs
+  // become resident.  BSEL_INV_COOP=1 restores the cooperative launch.
+  static const bool coop = [] {
+    const char* e = getenv("BSEL_INV_COOP");
+    return e && atoi(e) != 0;
+  }();
+  // BSEL_INV_SMEM (bytes, experiment): request more shared memory per CTA
+  // than the kernel uses, so that no GEMM CTA can share an SM with it.
+  static const size_t smem = [] {
+    const char* e = getenv("BSEL_INV_SMEM");
+    size_t v = e ? (size_t)atoll(e) : 0;
+    if (v < sizeof(PinvSmem)) v = sizeof(PinvSmem);
+    if (v != sizeof(PinvSmem)) cudaFuncSetAttribute(persistent_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v);
+    return v;
+  }();
+  cudaError_t err;
+  if (coop) {
+    void* args[] = {(void*)&g};
+    err = cudaLaunchCooperativeKernel((const void*)persistent_gj_kernel, grid, 256, args, smem, stream);
+  } else {
+    persistent_gj_kernel<<<grid, 256, smem, stream>>>(g);
+    err = cudaGetLastError();
+  }
+  count_launch();
+  return err;
+}
+
+cudaError_t launch_exact_fallback_attr() {
+  static const cudaError_t a1 =  // thread-safe one-time init, sized for n <= 2048
+      cudaFuncSetAttribute(exact_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  static const cudaError_t a2 =
+      cudaFuncSetAttribute(exact_schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  return a1 != cudaSuccess ? a1 : a2;
+}
+}  // namespace
+
 cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n,
                                  double2* work, int* flag, unsigned long long* status,
                                  unsigned long long key, cudaStream_t stream, int grid_req) {
@@ -762,36 +896,20 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
   const int panels = (n + kLeaf - 1) / kLeaf;
   const int limit = coop_grid_limit();
   if (panels > 1 && limit > 0) {
-    double2* gD = work + (int64_t)n * n;
-    unsigned* barrier = reinterpret_cast<unsigned*>(gD + 2 * kT * kT);
-    if ((err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream)) != cudaSuccess) return err;
+    GjArgs g{};
+    g.in = quad1(X, ldx);
+    g.out = g.a = quad1(Y, ldy);
+    g.bq = quad1(work, n);
+    g.b = n;
+    g.nq = 1;
+    g.gD = work + (int64_t)n * n;
+    g.barrier = reinterpret_cast<unsigned*>(g.gD + 2 * kT * kT);
+    g.flag = flag;
+    g.trace = g_inverse_trace;
     int grid = panels * panels < limit ? panels * panels : limit;
     const int cap = grid_req > 0 ? grid_req : inverse_grid_cap();
     if (grid > cap) grid = cap;
-    unsigned long long* trace = g_inverse_trace;
-    // A plain launch with the kernel's own grid barrier: cooperative launches
-    // from different streams are serialized by the driver, which made the
-    // inverses of concurrent partitions (lanes) wait for each other (SI, 2
-    // lanes: 666 us per inverse vs 284 us alone).  Co-residency still holds:
-    // grid <= the occupancy limit, and every other kernel that can hold the
-    // SMs (GEMM levels) finishes without waiting on the inverse, so all CTAs
-    // of the inverse become resident.  BSEL_INV_COOP=1 restores the
-    // cooperative launch.
-    static const bool coop = [] {
-      const char* e = getenv("BSEL_INV_COOP");
-      return e && atoi(e) != 0;
-    }();
-    if (coop) {
-      void* args[] = {(void*)&X, (void*)&ldx, (void*)&Y, (void*)&ldy, (void*)&n,
-                      (void*)&work, (void*)&gD, (void*)&barrier, (void*)&flag, (void*)&trace};
-      err = cudaLaunchCooperativeKernel((const void*)persistent_inverse_kernel, grid, 256, args, sizeof(PinvSmem),
-                                        stream);
-    } else {
-      persistent_inverse_kernel<<<grid, 256, sizeof(PinvSmem), stream>>>(X, ldx, Y, ldy, n, work, gD, barrier, flag,
-                                                                          trace);
-      err = cudaGetLastError();
-    }
-    count_launch();
+    err = launch_gj(g, grid, stream);
   } else {
     err = levels_inverse(X, ldx, Y, ldy, n, work, flag, stream);
   }
@@ -799,10 +917,57 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
   // Exact fallback (no-op unless a leaf met an exactly zero pivot).
   const size_t smem = (size_t)n * (2 * sizeof(double2) + 2 * sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static const cudaError_t smem_attr =  // thread-safe one-time init, sized for n <= 2048
-      cudaFuncSetAttribute(exact_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  if (smem_attr != cudaSuccess) return smem_attr;
+  if ((err = launch_exact_fallback_attr()) != cudaSuccess) return err;
   exact_inverse_kernel<<<1, 1024, smem, stream>>>(X, ldx, Y, ldy, n, work, flag, status, key);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int64_t schur_step_workspace(int b) { return 6 * (int64_t)b * b + 2 * kT * kT + 1; }
+
+bool schur_step_supported(int b) { return b > kLeaf && coop_grid_limit() > 0; }
+
+cudaError_t launch_schur_step(const double2* D, int64_t ldd, const double2* U, int64_t ldu, const double2* Lm,
+                              int64_t ldl, double2* C, int64_t ldc, double2* Sout, int64_t lds, double2* H,
+                              int64_t ldh, double2* F, int64_t ldf, int b, double2* work, int* flag,
+                              unsigned long long* status, unsigned long long key, cudaStream_t stream,
+                              int grid_req) {
+  if (!schur_step_supported(b)) return cudaErrorInvalidValue;
+  const int64_t bb = (int64_t)b * b;
+  double2* w = work;  // w0..w3 (B buffer), wc (A's C quadrant), wh (H if none given)
+  if (!H) H = w + 5 * bb, ldh = b;
+  GjArgs g{};
+  const double2* inp[4] = {D, U, Lm, C};
+  const int64_t inl[4] = {ldd, ldu, ldl, ldc};
+  double2* outp[4] = {Sout, H, F, C};
+  const int64_t outl[4] = {lds, ldh, ldf, ldc};
+  for (int q = 0; q < 4; ++q) {
+    g.in.p[q] = const_cast<double2*>(inp[q]), g.in.ld[q] = inl[q];
+    g.out.p[q] = outp[q], g.out.ld[q] = outl[q];
+    g.a.p[q] = q == 3 ? w + 4 * bb : outp[q], g.a.ld[q] = q == 3 ? b : outl[q];
+    g.bq.p[q] = w + q * bb, g.bq.ld[q] = b;
+  }
+  g.b = b;
+  g.nq = 2;
+  g.gD = w + 6 * bb;
+  g.barrier = reinterpret_cast<unsigned*>(g.gD + 2 * kT * kT);
+  g.flag = flag;
+  g.trace = g_inverse_trace;
+  const int ntq = (b + kT - 1) / kT;
+  int grid = std::min(4 * ntq * ntq, coop_grid_limit());
+  static const int cap_env = [] {
+    const char* e = getenv("BSEL_SCHUR_GRID");
+    return e ? atoi(e) : 128;
+  }();
+  const int cap = grid_req > 0 ? grid_req : cap_env;
+  if (cap > 0 && grid > cap) grid = cap;
+  cudaError_t err = launch_gj(g, grid, stream);
+  if (err != cudaSuccess) return err;
+  const size_t smem = (size_t)b * (2 * sizeof(double2) + 2 * sizeof(int));
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if ((err = launch_exact_fallback_attr()) != cudaSuccess) return err;
+  exact_schur_kernel<<<1, 1024, smem, stream>>>(D, ldd, U, ldu, Lm, ldl, C, ldc, Sout, lds, H, ldh, F, ldf, b, w,
+                                                 flag, status, key);
   count_launch();
   return cudaGetLastError();
 }

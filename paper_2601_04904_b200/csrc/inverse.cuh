@@ -37,6 +37,20 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
                                  double2* work, int* flag, unsigned long long* status,
                                  unsigned long long key, cudaStream_t stream, int grid = 0);
 
+// Fused Schur step of the forward sweeps (one persistent launch):
+//   Sout = D^-1, H = D^-1 U, F = L D^-1, C <- C - L D^-1 U   (all b x b)
+// by Gauss-Jordan on [[D, U], [L, C]] with pivots in D only: the chain's two
+// GEMMs become part of the panel updates.  H may be null (not kept).  Same
+// singularity semantics as launch_block_inverse (exact fallback recomputes
+// everything from the untouched D, U, L, C).  b > kLeaf only.
+int64_t schur_step_workspace(int b);
+bool schur_step_supported(int b);
+cudaError_t launch_schur_step(const double2* D, int64_t ldd, const double2* U, int64_t ldu, const double2* L,
+                              int64_t ldl, double2* C, int64_t ldc, double2* S, int64_t lds, double2* H,
+                              int64_t ldh, double2* F, int64_t ldf, int b, double2* work, int* flag,
+                              unsigned long long* status, unsigned long long key, cudaStream_t stream,
+                              int grid = 0);
+
 // Batched small inverses (n <= kLeaf) in one launch: Y_b = inv(X_b).
 cudaError_t launch_leaf_inverse_batched(const double2* X, int64_t ldx, int64_t strideX, double2* Y,
                                         int64_t ldy, int64_t strideY, int n, int batch, int* flags,

@@ -210,6 +210,7 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.sb = F.SB(i - lo);
         st.f_out = F.EF(i - lo), st.g_out = F.EG(i - lo), st.q_out = F.EQ(i - lo), st.k_out = F.EK(i - lo);
       }
+      st.h_out = F.EH(i - lo);
       end_step(ctx, st, fused, (uint64_t)s, i, fwd_slot(s));
       if (trace && (s + 1) % C == 0) tev(tstep, ctx.chain());
     }
@@ -237,6 +238,7 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.fn_out = F.EF(i - lo), st.fr_out = F.EFR(i - lo), st.g_out = F.EG(i - lo);
         st.qn_out = F.EQ(i - lo), st.qr_out = F.EQR(i - lo), st.kk_out = F.EK(i - lo);
       }
+      st.h_out = F.EH(i - lo);
       middle_step(ctx, st, fused, (uint64_t)s, i, fwd_slot(s));
     }
   }
@@ -353,6 +355,7 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       if (fused) {
         st.sc = F.SB(i - lo);
         st.cpre[0] = F.EF(i - lo), st.cpre[1] = F.EG(i - lo), st.qpre[0] = F.EQ(i - lo), st.qpre[1] = F.EK(i - lo);
+        if (ctx.schur_ok((int)b)) st.hpre[0] = F.EH(i - lo);
         st.ss[0] = down ? B->U(e) : B->L(e), st.ss[1] = el(*WB, i, false);
         st.ws[0] = down ? B->L(e) : B->U(e), st.ws[1] = el(*WB, i, true);
         st.yb[0][0] = XB->D(p), st.yb[0][1] = XB->AC(p), st.yb[1][0] = XB->AR(p), st.yb[1][1] = ztt;
@@ -400,6 +403,7 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
         st.sc = F.SB(i - lo);
         st.cpre[0] = F.EFR(i - lo), st.cpre[1] = F.EF(i - lo), st.cpre[2] = F.EG(i - lo);
         st.qpre[0] = F.EQR(i - lo), st.qpre[1] = F.EQ(i - lo), st.qpre[2] = F.EK(i - lo);
+        if (ctx.schur_ok((int)b)) st.hpre[1] = F.EH(i - lo);
         st.ss[0] = F.BFC(i - lo), st.ss[1] = B->U(i), st.ss[2] = el(*WB, i, false);
         st.ws[0] = F.BFR(i - lo), st.ws[1] = B->L(i), st.ws[2] = el(*WB, i, true);
         const Mat z00 = XB->D(lo), z0t = XB->AC(lo), zt0 = XB->AR(lo);

@@ -27,6 +27,8 @@ struct LocalFactorsDev {
   double2* elim_k = nullptr;
   double2* elim_fr = nullptr;
   double2* elim_qr = nullptr;
+  double2* elim_h = nullptr;
+  Mat EH(int64_t k) const { return elim_h ? blk(elim_h, k, (int)b, (int)b) : Mat{}; }
   Mat EF(int64_t k) const { return elim_f ? blk(elim_f, k, (int)b, (int)b) : Mat{}; }
   Mat EG(int64_t k) const { return elim_g ? blk(elim_g, k, (int)a, (int)b) : Mat{}; }
   Mat EQ(int64_t k) const { return elim_q ? blk(elim_q, k, (int)b, (int)b) : Mat{}; }

@@ -46,6 +46,8 @@ struct FactorsDev {
   double2* elim_g = nullptr;  // [n][a][b]  AR_i S_i
   double2* elim_q = nullptr;  // [n][b][b]  Bd_i f^H - B(i,j)
   double2* elim_k = nullptr;  // [n][b][a]  Bd_i g^H - BC_i
+  double2* elim_h = nullptr;  // [n][b][b]  S_i A(i,j)
+  Mat EH(int64_t i) const { return elim_h ? blk(elim_h, i, (int)b, (int)b) : Mat{}; }
   Mat EF(int64_t i) const { return elim_f ? blk(elim_f, i, (int)b, (int)b) : Mat{}; }
   Mat EG(int64_t i) const { return elim_g ? blk(elim_g, i, (int)a, (int)b) : Mat{}; }
   Mat EQ(int64_t i) const { return elim_q ? blk(elim_q, i, (int)b, (int)b) : Mat{}; }
@@ -108,6 +110,10 @@ class Context {
   // Singularity bookkeeping (device side, checked at synchronize()).
   void reset_status();
   void invert(Mat X, Mat Y, uint64_t order, int64_t index, cudaStream_t s);
+  // Fused Schur step (inverse.cuh launch_schur_step): S = D^-1, H = D^-1 U
+  // (H.p may be null), F = L D^-1, C -= L D^-1 U.  schur_ok(b): available.
+  bool schur_ok(int b) const;
+  void schur(Mat D, Mat U, Mat L, Mat C, Mat S, Mat H, Mat F, uint64_t order, int64_t index, cudaStream_t s);
   SingularInfo read_status();  // synchronizes the user stream
 
   // Copy stream for host<->device transfers overlapped with the sweeps and

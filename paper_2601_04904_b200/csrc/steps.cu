@@ -61,17 +61,24 @@ void ring_wait(Context& ctx, int step) {
 void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64_t index, int slot) {
   cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
-  ctx.invert(st.ad_i, st.S, order, index, sA);
+  const bool schur = ctx.schur_ok(b);
   const Mat& S = st.S;
   if (!fused) {
     // rgf.py:283-288 / dist.py:252-257: right-hand temporaries.
-    Mat t1 = rt(ctx, slot, 0, b, b), t2 = rt(ctx, slot, 1, b, a);
-    Level L(sA);
-    L.out(t1).mm(+1, S, N, st.Uk, N);
-    L.flush();
-    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
-    L.out(st.ad_j).add(+1, st.ad_j).mm(-1, st.Lk, N, t1, N);
-    L.flush();
+    Mat t1 = st.h_out.p ? st.h_out : rt(ctx, slot, 0, b, b), t2 = rt(ctx, slot, 1, b, a);
+    if (schur) {  // S, t1 = S Uk and ad_j -= Lk t1 in one launch
+      ctx.schur(st.ad_i, st.Uk, st.Lk, st.ad_j, S, t1, st.f_out.p ? st.f_out : rt(ctx, slot, 2, b, b), order, index,
+                sA);
+      cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
+    } else {
+      ctx.invert(st.ad_i, st.S, order, index, sA);
+      Level L(sA);
+      L.out(t1).mm(+1, S, N, st.Uk, N);
+      L.flush();
+      cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
+      L.out(st.ad_j).add(+1, st.ad_j).mm(-1, st.Lk, N, t1, N);
+      L.flush();
+    }
     cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
     Level LB(sB, kTileAuto, aux_ctas());
     LB.out(t2).mm(+1, S, N, st.ac_i, N);
@@ -86,7 +93,11 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   auto keep = [&](const Mat& m, int k_, int r, int c) { return m.p ? m : rt(ctx, slot, k_, r, c); };
   Mat f = keep(st.f_out, 0, b, b), g = keep(st.g_out, 1, a, b), w = rt(ctx, slot, 2, b, b);
   Mat k = keep(st.k_out, 4, b, a), q = keep(st.q_out, 5, b, b);
-  {
+  if (schur) {  // S, f = Lk S and ad_j -= f Uk (and h = S Uk) in one launch
+    ctx.schur(st.ad_i, st.Uk, st.Lk, st.ad_j, S, st.h_out, f, order, index, sA);
+    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
+  } else {
+    ctx.invert(st.ad_i, st.S, order, index, sA);
     Level L(sA);
     L.out(f).mm(+1, st.Lk, N, S, N);
     L.flush();
@@ -127,11 +138,14 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
 void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int slot) {
   cudaStream_t sA = ctx.chain(), sB = ctx.aux();
   const int b = st.ad_i.r, a = st.ar_i.r;
-  ctx.invert(st.ad_i, st.S, order, index, sA);
   const Mat& S = st.S;
   auto keep = [&](const Mat& m, int k_, int r, int c) { return m.p ? m : rt(ctx, slot, k_, r, c); };
   Mat fn = keep(st.fn_out, 0, b, b), fr = keep(st.fr_out, 1, b, b), g = keep(st.g_out, 2, a, b);
-  {
+  if (ctx.schur_ok(b)) {  // S, fn = L S and ad_n -= fn U (and h = S U) in one launch
+    ctx.schur(st.ad_i, st.U, st.L, st.ad_n, S, st.h_out, fn, order, index, sA);
+    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
+  } else {
+    ctx.invert(st.ad_i, st.S, order, index, sA);
     Level L(sA);
     L.out(fn).mm(+1, st.L, N, S, N);
     L.flush();
@@ -265,7 +279,8 @@ void BackSweep::step(BackStep& st) {
     if (t >= kBackDepth - 1) cuda_check(cudaStreamWaitEvent(sp, ev_b(ctx_, t - kBackDepth + 1), 0), "ring wait");
     Level P(sp, cfg_);
     for (int l = 0; l < k; ++l) {
-      P.out(h[l]).mm(+1, st.g, N, st.rs[l], N);
+      if (st.hpre[l].p) h[l] = st.hpre[l];
+      else P.out(h[l]).mm(+1, st.g, N, st.rs[l], N);
       if (st.cpre[l].p) c[l] = st.cpre[l];
       else P.out(c[l]).mm(+1, st.qs[l], N, st.g, N);
       if (fused) {

@@ -19,6 +19,7 @@ struct EndStep {
   // optional: retain f = Lk S, g = AR_i S, q = Bd_i f^H - BU, k = Bd_i g^H - BC_i
   // here (the backward step of block i reuses them) instead of ring slots
   Mat f_out, g_out, q_out, k_out;
+  Mat h_out;  // optional: h = S Uk (the backward's h_0), free with the fused Schur step
 };
 // Forward ring: temporaries of step k live in ring slot fwd_slot(k); the
 // B side (aux stream) may lag the A chain by up to kFwdDepth - 1 steps.
@@ -41,6 +42,7 @@ struct MiddleStep {
   // optional retained products (see EndStep): fn = L S, fr = fill_r S,
   // g = AR_i S, qn = Bd fn^H - BU, qr = Bd fr^H - bfill_c, kk = Bd g^H - BC_i
   Mat fn_out, fr_out, g_out, qn_out, qr_out, kk_out;
+  Mat h_out;  // optional: h = S U
 };
 void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int slot);
 
@@ -63,6 +65,7 @@ struct BackStep {
   // optional products retained by the forward step of this block:
   // cpre[l] = qs_l g, qpre[l] = Bd (qs_l g)^H - ss_l  (then e_l = -g qpre[l])
   Mat cpre[3], qpre[3];
+  Mat hpre[3];  // optional: h_l = g rs_l (from the fused Schur step)
   // outputs
   Mat row[3], col[3], diag;
   Mat zrow[3], zcol[3], zdiag;

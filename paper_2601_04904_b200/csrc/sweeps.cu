@@ -8,6 +8,7 @@
 // so the latency-bound pivot inverse of step i+1 overlaps the quadratic
 // updates of step i.  Temporaries live in a double-buffered slot ring.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "inverse.cuh"
@@ -134,6 +135,31 @@ int Context::b_symmetry() const {
   return 0;
 }
 
+// The fused Schur step is opt-in (BSEL_SCHUR=1, read per call): alone it
+// beats inverse + 2 GEMMs (SI chain 422 vs 453 us per step at b=512), but its
+// 4x larger rank-32 panel updates lose more under the quadratic solve's
+// concurrent GEMM levels (cfg4, 2 lanes: forward 700 vs 565 ms).
+bool Context::schur_ok(int b) const {
+  const char* e = getenv("BSEL_SCHUR");
+  return e && atoi(e) != 0 && schur_step_supported(b);
+}
+
+void Context::schur(Mat D, Mat U, Mat L, Mat C, Mat S, Mat H, Mat F, uint64_t order, int64_t index,
+                    cudaStream_t s) {
+  const int b = D.r;
+  for (const Mat* m : {&D, &U, &L, &C, &S, &F})
+    if (m->r != b || m->c != b) throw ShapeError("Schur step needs square blocks of one size");
+  if (H.p && (H.r != b || H.c != b)) throw ShapeError("Schur step H shape");
+  const unsigned long long key = (order << 32) | (uint64_t)(uint32_t)index;
+  double2* work = inv_work(schur_step_workspace(b));
+  int id = profiling() ? profile_open(s) : -1;
+  // executed: the inverse and the three products it absorbs (L S, S U, (L S) U)
+  cudaError_t e = launch_schur_step(D.p, D.ld, U.p, U.ld, L.p, L.ld, C.p, C.ld, S.p, S.ld, H.p, H.ld, F.p, F.ld,
+                                    b, work, d_flag_, d_status_, key, s, inv_grid_ > 0 ? 2 * inv_grid_ : 0);
+  profile_close(id, s, 1, 32.0 * b * (double)b * b);
+  cuda_check(e, "Schur step");
+}
+
 SingularInfo Context::read_status() {
   unsigned long long st = 0;
   cuda_check(cudaMemcpyAsync(&st, d_status_, sizeof(st), cudaMemcpyDeviceToHost, user_stream_), "status d2h");
@@ -218,16 +244,17 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
   for (int i = 0; i < n - 1; ++i) {
     const int r = (i & 1) * 4;
     Mat S = F.SA(i), t1 = F.elim_f ? F.EF(i) : ctx.tmp(r + 0, b, b);
-    ctx.invert(A.D(i), S, i, i, sA);
     if (fused && i >= 2) cuda_check(cudaStreamWaitEvent(sA, ctx.event(2 + (i & 1)), 0), "wait B");
-    {
+    if (ctx.schur_ok(b)) {
+      // inverse, t1 = L S and D(i+1) -= t1 U in one persistent launch
+      ctx.schur(A.D(i), A.U(i), A.L(i), A.D(i + 1), S, F.EH(i), t1, i, i, sA);
+      if (fused) cuda_check(cudaEventRecord(ctx.event(i & 1), sA), "record A");
+    } else {
+      ctx.invert(A.D(i), S, i, i, sA);
       Level L(sA);
       L.out(t1).mm(+1, A.L(i), N, S, N);
       L.flush();
-    }
-    if (fused) cuda_check(cudaEventRecord(ctx.event(i & 1), sA), "record A");
-    {
-      Level L(sA);
+      if (fused) cuda_check(cudaEventRecord(ctx.event(i & 1), sA), "record A");
       L.out(A.D(i + 1)).add(+1, A.D(i + 1)).mm(-1, t1, N, A.U(i), N);
       L.flush();
     }
@@ -276,6 +303,7 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
       st.sb = F.SB(i);
       st.f_out = F.EF(i), st.g_out = F.EG(i), st.q_out = F.EQ(i), st.k_out = F.EK(i);
     }
+    st.h_out = F.EH(i);
     end_step(ctx, st, fused, i, i, fwd_slot(i));
   }
   // Epilogue (rgf.py:290-318).  The last block's arrow strips and the tip
@@ -354,6 +382,7 @@ void bt_backward(Context& ctx, const FactorsDev& F, const BtaDev& A, const BtaDe
       st.sc = F.SB(i);
       st.ss[0] = B->U(i), st.ws[0] = B->L(i);
       st.cpre[0] = F.EF(i), st.qpre[0] = F.EQ(i);
+      if (ctx.schur_ok(b)) st.hpre[0] = F.EH(i);
       st.yb[0][0] = XB->D(i + 1);
       if (!diag_only) st.zrow[0] = XB->U(i), st.zcol[0] = XB->L(i);
       st.zdiag = XB->D(i);
@@ -411,6 +440,7 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
       if (fused) {
         st.sc = F.SB(i);
         st.cpre[0] = F.EF(i), st.cpre[1] = F.EG(i), st.qpre[0] = F.EQ(i), st.qpre[1] = F.EK(i);
+        if (ctx.schur_ok(b)) st.hpre[0] = F.EH(i);
         st.ss[0] = B->U(i), st.ss[1] = F.BCe(i);
         st.ws[0] = B->L(i), st.ws[1] = F.BRe(i);
         st.yb[0][0] = XB->D(i + 1), st.yb[0][1] = XB->AC(i + 1), st.yb[1][0] = XB->AR(i + 1);

@@ -166,7 +166,7 @@ class LocalFactors:
         f = _native.LocalFactors()
         f.lo, f.hi, f.kind, f.fused = self.lo, self.hi, _KIND_CODES[self.kind], int(self.mode == "siq")
         for k in ("s_a", "s_b", "fill_row", "fill_col", "b_fill_row", "b_fill_col", "elim_f", "elim_g", "elim_q",
-                  "elim_k", "elim_fr", "elim_qr"):
+                  "elim_k", "elim_fr", "elim_qr", "elim_h"):
             t = self.tensors.get(k)
             setattr(f, k, t.data_ptr() if (t is not None and t.numel()) else None)
         return f
@@ -223,6 +223,7 @@ def _alloc_factors(kind, lo, hi, fused, bs, asz, dev) -> "LocalFactors":
     # elimination products retained for the backward (bsel_local_factors_t)
     t["elim_f"] = torch.empty((length, bs, bs), **c128)
     t["elim_g"] = torch.empty((length, asz, bs), **c128)
+    t["elim_h"] = torch.empty((length, bs, bs), **c128)
     if fused:
         t["s_b"] = torch.empty((length, bs, bs), **c128)
         t["elim_q"] = torch.empty((length, bs, bs), **c128)

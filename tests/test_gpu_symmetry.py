@@ -107,3 +107,47 @@ def test_forced_mode_roundtrip():
         ctx.set_b_symmetry(m)
     with pytest.raises(ValueError):
         ctx.set_b_symmetry(5)
+
+
+@pytest.fixture
+def fused_schur(monkeypatch):
+    monkeypatch.setenv("BSEL_SCHUR", "1")  # read by the library per step
+
+
+@pytest.mark.parametrize("kind", ["hermitian", "general"])
+@pytest.mark.parametrize("n,b,a,parts", [(9, 40, 12, 1), (12, 64, 16, 2), (16, 33, 8, 3), (6, 100, 0, 1)])
+def test_fused_schur_step_paths(fused_schur, kind, n, b, a, parts):
+    A = bs.generate_dd_bta(n, b, a, seed=13)
+    B = rhs(n, b, a, kind, seed=14)
+    got = bs.dist_solve(A, B, num_parts=parts, mode="siq") if parts > 1 else bs.solve_selected(A, B, "siq",
+                                                                                             partitions=1)
+    xa, xb = oracle.solve_selected(A, B, "siq")
+    assert max_block_rel_err(got.x_a, xa) <= TOL
+    assert max_block_rel_err(got.x_b, xb) <= TOL
+    got = bs.solve_selected(A, None, "si", partitions=1)
+    xa, _ = oracle.solve_selected(A, None, "si")
+    assert max_block_rel_err(got.x_a, xa) <= TOL
+
+
+@pytest.mark.parametrize("b", [40, 64, 96])
+@pytest.mark.parametrize("schur", [False, True])
+def test_zero_leaf_pivot_fallback(monkeypatch, b, schur):
+    """A leaf meeting an exactly zero pivot takes the exact fallback (the
+    reference's semantics); with the fused Schur step (inverse + L S +
+    C - L S U in one launch) the fallback recomputes S, F, H and the Schur
+    complement from the untouched inputs."""
+    if schur:
+        monkeypatch.setenv("BSEL_SCHUR", "1")
+    n, a = 5, 8
+    A = bs.generate_dd_bta(n, b, a, seed=11)
+    arr = {k: v.copy() for k, v in A.stacked().items()}
+    d = arr["diag"][0]
+    # first 32 rows of column 0 exactly zero, the block stays nonsingular
+    d[:32, 0] = 0.0
+    d[b - 1, 0] = 5.0 * b
+    A2 = bs.BtaMatrix.from_stacked(n, b, a, arr)
+    B = bs.hermitianize(bs.generate_dd_bta(n, b, a, seed=12))
+    sol = bs.solve_selected(A2, B, "siq", partitions=1)
+    xa, xb = oracle.solve_selected(A2, B, "siq")
+    assert max_block_rel_err(sol.x_a, xa) <= TOL
+    assert max_block_rel_err(sol.x_b, xb) <= TOL
