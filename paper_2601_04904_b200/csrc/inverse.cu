@@ -847,16 +847,18 @@ Quad quad1(const double2* p, int64_t ld) {
 
 cudaError_t launch_gj(GjArgs& g, int grid, cudaStream_t stream) {
   if ((cudaError_t)cudaMemsetAsync(g.barrier, 0, sizeof(unsigned), stream) != cudaSuccess) return cudaGetLastError();
-  // A plain launch with the kernel's own grid barrier: cooperative launches
-  // from different streams are serialized by the driver, which made the
-  // inverses of concurrent partitions (lanes) wait for each other (SI, 2
-  // lanes: 666 us per inverse vs 284 us alone).  Co-residency still holds:
-  // grid <= the occupancy limit, and every other kernel that can hold the
-  // SMs (GEMM levels) finishes without waiting on this one, so all its CTAs
-  // become resident.  BSEL_INV_COOP=1 restores the cooperative launch.
+  // The CTAs wait on one another (grid barrier), so the launch is
+  // cooperative: co-residency of the whole grid is guaranteed.  Cooperative
+  // launches from different streams are serialized by the driver, which
+  // makes the inverses of concurrent lanes wait for each other (SI, 2 lanes:
+  // 454 us per inverse with plain launches vs 666 us cooperative; SI+SQ
+  // forward 564 vs 578 ms).  BSEL_INV_COOP=0 (experiment) uses a plain launch:
+  // all CTAs still become resident in practice (grid <= occupancy limit and
+  // the concurrent GEMM levels never wait on the inverse) but nothing
+  // guarantees it.
   static const bool coop = [] {
     const char* e = getenv("BSEL_INV_COOP");
-    return e && atoi(e) != 0;
+    return !(e && atoi(e) == 0);
   }();
   // BSEL_INV_SMEM (bytes, experiment): request more shared memory per CTA
   // than the kernel uses, so that no GEMM CTA can share an SM with it.

@@ -68,6 +68,13 @@ class Level {
     a.sign = sign;
     return *this;
   }
+  // Only the tiles on / below the tile diagonal of the (square) output are
+  // computed (a Hermitian result mirrored afterwards).
+  Level& lower_only() {
+    if (!cur_ || cur_->M != cur_->N) throw ShapeError("lower_only() needs a square output");
+    cur_->lower_only = 1;
+    return *this;
+  }
   // D += sign * op(A) @ op(B); op 'N' or 'H' (conjugate transpose).
   Level& mm(int sign, Mat A, char oa, Mat B, char ob) {
     if (!cur_) throw ShapeError("mm() before out()");

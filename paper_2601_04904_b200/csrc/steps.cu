@@ -330,13 +330,16 @@ void BackSweep::step(BackStep& st) {
     }
     B.flush();
     B.out(st.zdiag).add(+1, st.sc);
+    if (sym) B.lower_only();  // X_B(i,i) = s X_B(i,i)^H: lower tiles, then mirrored
     for (int l = 0; l < k; ++l) {
       if (sym) B.mm(sym, st.row[l], N, e[l], H);  // f_l = s e_l^H
       else B.mm(+1, st.row[l], N, f[l], N);
     }
     for (int l = 0; l < k; ++l) B.mm(-1, st.zrow[l], N, h[l], H);
     B.flush();
-    if (sym) {  // zcol_j = X_B(trail_j, i) = s X_B(i, trail_j)^H
+    if (sym) {
+      cuda_check(launch_mirror_lower(st.zdiag.p, st.zdiag.ld, st.zdiag.r, sym, sb), "mirror");
+      // zcol_j = X_B(trail_j, i) = s X_B(i, trail_j)^H
       TransJob tj[3];
       for (int j = 0; j < k; ++j) {
         tj[j].src = st.zrow[j].p, tj[j].lds = st.zrow[j].ld, tj[j].r = st.zrow[j].r, tj[j].c = st.zrow[j].c;

@@ -87,7 +87,39 @@ __global__ void __launch_bounds__(kT * kRows) conj_transpose_kernel(TransBatch b
     }
   }
 }
+__global__ void __launch_bounds__(kT * kRows) mirror_lower_kernel(double2* A, int64_t ld, int n, int sign) {
+  // pair index -> (tj, ti), ti <= tj: the upper tile (ti, tj) is written from
+  // the lower tile (tj, ti)
+  const int l = blockIdx.x;
+  int tj = (int)((sqrt(8.0 * l + 1.0) - 1.0) * 0.5);
+  while ((tj + 1) * (tj + 2) / 2 <= l) ++tj;
+  while (tj * (tj + 1) / 2 > l) --tj;
+  const int ti = l - tj * (tj + 1) / 2;
+  __shared__ double2 s[kT][kT + 1];
+  const int tx = threadIdx.x;
+  for (int e = threadIdx.y; e < kT; e += kRows) {  // lower tile rows tj*32.., cols ti*32..
+    const int row = tj * kT + e, col = ti * kT + tx;
+    if (row < n && col < n) s[e][tx] = A[(int64_t)row * ld + col];
+  }
+  __syncthreads();
+  const double sg = (double)sign;
+  for (int e = threadIdx.y; e < kT; e += kRows) {  // upper element (ti*32+e, tj*32+tx) <- s[tx][e]
+    const int row = ti * kT + e, col = tj * kT + tx;
+    if (row < n && col < n && col > row) {
+      const double2 v = s[tx][e];
+      A[(int64_t)row * ld + col] = make_double2(sg * v.x, -sg * v.y);
+    }
+  }
+}
 }  // namespace
+
+cudaError_t launch_mirror_lower(double2* A, int64_t ld, int n, int sign, cudaStream_t s) {
+  if (n <= 1) return cudaSuccess;
+  const int nt = (n + kT - 1) / kT;
+  mirror_lower_kernel<<<nt * (nt + 1) / 2, dim3(kT, kRows), 0, s>>>(A, ld, n, sign);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sym_check(const SymJob& j, int* flags, cudaStream_t s) {
   if (j.r <= 0 || j.c <= 0) return cudaSuccess;

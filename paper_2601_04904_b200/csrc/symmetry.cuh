@@ -40,4 +40,8 @@ struct TransJob {
 };
 cudaError_t launch_conj_transpose(const TransJob* jobs, int njobs, int sign, cudaStream_t s);
 
+// A (n x n): A[r][c] = sign * conj(A[c][r]) for c > r (the strict upper
+// triangle from the lower one; pairs with Level::lower_only()).
+cudaError_t launch_mirror_lower(double2* A, int64_t ld, int n, int sign, cudaStream_t s);
+
 }  // namespace bsel

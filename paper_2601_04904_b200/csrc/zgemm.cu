@@ -159,8 +159,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   while (pi + 1 < batch.nproblems && bid >= batch.p[pi + 1].tile_begin) ++pi;
   const GemmProblem& P = batch.p[pi];
   const int local = bid - P.tile_begin;
-  const int m0 = (local / P.tiles_n) * C::BM;
-  const int n0 = (local % P.tiles_n) * C::BN;
+  int m0 = (local / P.tiles_n) * C::BM;
+  int n0 = (local % P.tiles_n) * C::BN;
+  if (P.lower_only) {  // local = tr (tr + 1) / 2 + tc, tc <= tr
+    int tr = (int)((sqrt(8.0 * local + 1.0) - 1.0) * 0.5);
+    while ((tr + 1) * (tr + 2) / 2 <= local) ++tr;
+    while (tr * (tr + 1) / 2 > local) --tr;
+    m0 = tr * C::BM;
+    n0 = (local - tr * (tr + 1) / 2) * C::BN;
+  }
 
   int nchunks = 0;
   for (int t = 0; t < P.nterms; ++t) nchunks += (P.term[t].K + C::BK - 1) / C::BK;
@@ -286,7 +293,8 @@ cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
     GemmProblem& P = batch.p[i];
     P.tiles_n = (P.N + C::BN - 1) / C::BN;
     P.tile_begin = tiles;
-    tiles += ((P.M + C::BM - 1) / C::BM) * P.tiles_n;
+    if (P.lower_only && (P.M != P.N || C::BM != C::BN)) return cudaErrorInvalidValue;
+    tiles += P.lower_only ? P.tiles_n * (P.tiles_n + 1) / 2 : ((P.M + C::BM - 1) / C::BM) * P.tiles_n;
   }
   batch.total_tiles = tiles;
   if (tiles == 0) return cudaSuccess;
@@ -297,7 +305,9 @@ cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
     // D written once (the compulsory DRAM traffic of the launch).
     for (int i = 0; i < batch.nproblems; ++i) {
       const GemmProblem& P = batch.p[i];
-      const double M = P.M, N = P.N;
+      const double tn = P.tiles_n;
+      const double frac = P.lower_only ? (tn + 1.0) / (2.0 * tn) : 1.0;  // share of tiles computed
+      const double M = P.M * frac, N = P.N;
       bytes += 16.0 * M * N * (1 + P.naddends);
       for (int t = 0; t < P.nterms; ++t) {
         flops += 8.0 * M * N * P.term[t].K;

@@ -55,6 +55,8 @@ struct GemmProblem {
   int32_t nterms, naddends;
   int32_t tiles_n;    // filled by the launcher
   int32_t tile_begin; // filled by the launcher
+  int32_t lower_only; // M == N: only tiles on / below the tile diagonal are computed
+  int32_t pad_;
   GemmAddend add[kMaxAddends];
   GemmTerm term[kMaxTerms];
 };
