@@ -339,6 +339,7 @@ int bsel_bta_forward(bsel_context_t* ctx, const bsel_bta_t* a_work, const bsel_b
       sym_check_couplings(cx, B, 0, B.n - 1, cx.stream());
       sym_check_tip(cx, B, nullptr, cx.stream());
     }
+    cx.set_forward_symmetry(b_work ? cx.sym_now(cx.stream()) : 0);
     bta_forward(cx, A, b_work ? &B : nullptr, to_dev(*f));
     raise_if_singular(*ctx->impl, a_work->n);
   });
@@ -447,6 +448,7 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
       F.elim_q = at(15);
       F.elim_k = as > 0 ? at(16) : nullptr;
     }
+    cx.set_forward_symmetry(fused ? cx.sym_now(s) : 0);
     bta_forward(cx, A, fused ? &B : nullptr, F);
     raise_if_singular(cx, n);
     BtaDev XA = to_dev(*x_a), XB;

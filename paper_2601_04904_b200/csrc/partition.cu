@@ -170,6 +170,9 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
     stage(A, WA, false);
     if (fused) stage(*B, *WB, true);
   }
+  // Device-resident inputs: the staging check of this partition's B is known
+  // before the sweep starts (streamed chunks are checked only as they land).
+  ctx.set_forward_symmetry(fused && !streamed ? ctx.sym_now(ctx.stream()) : 0);
   cuda_check(cudaEventRecord(ctx.timer(0), ctx.stream()), "timer");
   auto d = [&](const BtaDev& w, int64_t i) { return w.D(i - lo); };
   auto ar = [&](const BtaDev& w, int64_t i) { return w.AR(i - lo); };

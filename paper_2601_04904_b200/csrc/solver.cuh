@@ -106,6 +106,14 @@ class Context {
   void set_b_symmetry(int mode) { sym_mode_ = mode; }
   int b_symmetry() const;
   int sym_flags() const { return sym_checked_ ? sym_flags_ : 3; }
+  // Synchronize the stream and read the flags of the checks queued so far;
+  // returns +1 / -1 when THAT data is exactly (anti-)Hermitian, else 0.  The
+  // forward of a partition may use its own data's symmetry (its recursion
+  // never reads another partition's blocks); set_forward_symmetry() passes it
+  // to the forward steps.
+  int sym_now(cudaStream_t s);
+  void set_forward_symmetry(int s) { fwd_sym_ = s; }
+  int forward_symmetry() const { return fwd_sym_; }
 
   // Singularity bookkeeping (device side, checked at synchronize()).
   void reset_status();
@@ -141,7 +149,7 @@ class Context {
   int64_t inv_work_elems_ = 0;
   int* d_flag_ = nullptr;
   int* d_sym_ = nullptr;
-  int sym_flags_ = 3, sym_mode_ = kSymAuto;
+  int sym_flags_ = 3, sym_mode_ = kSymAuto, fwd_sym_ = 0;
   bool sym_checked_ = false;
   unsigned long long* d_status_ = nullptr;
   std::vector<cudaEvent_t> events_;

@@ -123,11 +123,26 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   L.out(st.ar_j).add(+1, st.ar_j).mm(-1, g, N, st.Uk, N);
   L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
   L.out(k).add(-1, st.bc_i).mm(+1, st.bd_i, N, g, H);
+  // B = s B^H (this partition's data, checked before the sweep): S_B and the
+  // updated B diagonal stay (anti-)Hermitian -> lower-triangle tiles + mirror,
+  // and the arrow column is the (conjugate) transpose of the arrow row.
+  const int sym = ctx.forward_symmetry();
   L.out(st.sb).mm(+1, w, N, S, H);
+  if (sym) L.lower_only();
   L.out(st.bd_j).add(+1, st.bd_j).mm(+1, f, N, q, N).mm(-1, st.BL, N, f, H);
+  if (sym) L.lower_only();
   L.out(st.br_j).add(+1, st.br_j).mm(+1, g, N, q, N).mm(-1, st.br_i, N, f, H);
   L.flush();
-  L.out(st.bc_j).add(+1, st.bc_j).mm(+1, f, N, k, N).mm(-1, st.BL, N, g, H);
+  if (sym) {
+    cuda_check(launch_mirror_lower(st.sb.p, st.sb.ld, st.sb.r, sym, sB), "mirror");
+    cuda_check(launch_mirror_lower(st.bd_j.p, st.bd_j.ld, st.bd_j.r, sym, sB), "mirror");
+    TransJob tj;
+    tj.src = st.br_j.p, tj.lds = st.br_j.ld, tj.r = st.br_j.r, tj.c = st.br_j.c;
+    tj.dst = st.bc_j.p, tj.ldd = st.bc_j.ld;
+    cuda_check(launch_conj_transpose(&tj, 1, sym, sB), "conjugate transpose");
+  } else {
+    L.out(st.bc_j).add(+1, st.bc_j).mm(+1, f, N, k, N).mm(-1, st.BL, N, g, H);
+  }
   L.out(st.tipB).add(+1, st.tipB).mm(+1, g, N, k, N).mm(-1, st.br_i, N, g, H);
   L.flush();
   cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");

@@ -127,6 +127,15 @@ void Context::sym_check(const SymJob& j, cudaStream_t s) {
   sym_checked_ = true;
 }
 
+int Context::sym_now(cudaStream_t s) {
+  int f = 3;
+  cuda_check(cudaMemcpyAsync(&f, d_sym_, sizeof(f), cudaMemcpyDeviceToHost, s), "symmetry d2h");
+  cuda_check(cudaStreamSynchronize(s), "symmetry sync");
+  if (!sym_checked_) return 0;
+  sym_flags_ = f;
+  return !(f & kNotHermitian) ? +1 : !(f & kNotSkew) ? -1 : 0;
+}
+
 int Context::b_symmetry() const {
   if (sym_mode_ != kSymAuto) return sym_mode_;
   if (!sym_checked_) return 0;

@@ -185,8 +185,10 @@ def test_solve_selected_partitions_match_sequential(n, b, a, mode):
 @pytest.mark.parametrize("mode", ["si", "siq"])
 def test_streamed_host_io_matches_device_path(parts, chunk, mode, monkeypatch):
     """Pinned host inputs/outputs streamed chunk by chunk behind the partition
-    sweeps (bsel_host_io_t) give bit-identical results to device-resident
-    inputs, for first/middle/last partitions and ragged chunk tails."""
+    sweeps (bsel_host_io_t) give the results of device-resident inputs, for
+    first/middle/last partitions and ragged chunk tails: X_A bit-identical;
+    X_B to rounding (device-resident Hermitian B lets the forward skip the
+    mirrored B-side products, which streamed chunks cannot know in advance)."""
     monkeypatch.setenv("BSEL_STREAM_CHUNK", str(chunk))
     n, b, a = 23, 8, 3
     A = bs.generate_dd_bta(n, b, a, seed=31, pinned=True)
@@ -199,6 +201,6 @@ def test_streamed_host_io_matches_device_path(parts, chunk, mode, monkeypatch):
             got = bs.solve_selected(inp[0], inp[1], mode, partitions=parts, out=out)
             assert got.x_a.equals_exact(want_a)
             if mode == "siq":
-                assert got.x_b.equals_exact(want_b)
+                assert max_block_rel_err(got.x_b, want_b) <= 1e-13
     seq = bs.solve_selected(A, B, mode, partitions=1)
     assert max_block_rel_err(got.x_a, seq.x_a) <= 1e-12
