@@ -355,6 +355,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # pinned host buffers (e2e) on this GPU's NUMA node; the CPU-baseline leg
+    # restores the full affinity
+    all_cpus = bs.bind_host_to_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -383,7 +386,11 @@ def main():
         def step():
             bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, partitions=parts)
     else:
-        solver = bdist.DistSolver(A, B, "siq", world, rank, dev)
+        # BSEL_PLAN_COSTS="end,mid": partition sizes from measured per-block
+        # times instead of the reference's product counts
+        pc = os.environ.get("BSEL_PLAN_COSTS")
+        plan_costs = tuple(float(x) for x in pc.split(",")) if pc else None
+        solver = bdist.DistSolver(A, B, "siq", world, rank, dev, plan_costs=plan_costs)
 
         def step():
             solver.solve()
@@ -431,6 +438,13 @@ def main():
     else:
         phases = solver.phase_seconds()
     phases = {k: v * 1e3 for k, v in phases.items()}
+    rank_phases = None
+    if dist:
+        keys = sorted(phases)
+        t = torch.tensor([phases[k] for k in keys], device=dev, dtype=torch.float64)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        rank_phases = [{k: round(float(v), 2) for k, v in zip(keys, x.tolist())} for x in allt]
 
     # ---- live per-kernel timing of the dominant kernel (one extra step) ----
     # Every launch is bracketed by CUDA events on its own stream; launches of
@@ -489,6 +503,8 @@ def main():
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
+        if all_cpus:
+            os.sched_setaffinity(0, all_cpus)
         n_s = args.cpu_sample_n
         t_s = cpu_sample(n_s, b, a)
         _, kind = reference_impl()
@@ -534,6 +550,8 @@ def main():
                          "inverse_busy_ms_per_step": prof.inverse_busy_ms,
                          "gemm_launches_per_step": prof.gemm_launches},
             "phases_ms": phases,
+            "rank_phases_ms": rank_phases,
+            "partition_sizes": ([hi - lo for lo, hi in solver.plan.ranges] if world > 1 else None),
             "value_sequential_rgf_ms": seq_ms,
             "gpu_launches": launches,
             "clocks": clocks,

@@ -35,7 +35,8 @@ from .errors import (
 from .matrix import BtaMatrix, SelectedSolution, generate_dd_bta, hermitianize, mask_to_pattern, to_dense
 from .partition import PartitionPlan, plan_partitions
 from .kernels import OpCounter, block_inverse, block_multiply_acc, mm
-from .device import DeviceBta, generate_dd_bta_device, hermitianize_device, kernel_launches, to_device, to_host
+from .device import (DeviceBta, bind_host_to_device, generate_dd_bta_device, hermitianize_device, kernel_launches,
+                     to_device, to_host)
 from .rgf import (RgfFactors, bt_backward, bt_forward, bta_backward, bta_forward, default_partitions,
                   release_caches, solve_selected)
 from .collectives import Collectives, LocalHub, TorchCollectives, TraceEvent
@@ -49,6 +50,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BtaMatrix", "SelectedSolution", "RgfFactors", "OpCounter", "PartitionPlan", "DeviceBta",
+    "bind_host_to_device",
     "generate_dd_bta", "hermitianize", "to_dense", "mask_to_pattern", "to_device", "to_host",
     "block_multiply_acc", "mm", "block_inverse",
     "bt_forward", "bt_backward", "bta_forward", "bta_backward", "solve_selected", "default_partitions",

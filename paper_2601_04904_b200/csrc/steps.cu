@@ -198,18 +198,40 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   }
   L.out(qr).add(-1, st.bfill_c).mm(+1, st.bd_i, N, fr, H);
   L.out(kk).add(-1, st.bc_i).mm(+1, st.bd_i, N, g, H);
+  // B = s B^H (see end_step): Hermitian blocks as lower-triangle tiles +
+  // mirror, column-side blocks (bc_n, bc_lo, the new column fill) as
+  // transposes of their row-side partners.
+  const int sym = ctx.forward_symmetry();
   L.out(st.sb).mm(+1, w, N, S, H);
+  if (sym) L.lower_only();
   L.out(st.bd_n).add(+1, st.bd_n).mm(+1, fn, N, qn, N).mm(-1, st.BL, N, fn, H);
+  if (sym) L.lower_only();
   L.out(st.br_n).add(+1, st.br_n).mm(+1, g, N, qn, N).mm(-1, st.br_i, N, fn, H);
   L.out(st.nbfill_r).mm(+1, fr, N, qn, N).mm(-1, st.bfill_r, N, fn, H);
   L.flush();
   L.out(st.br_lo).add(+1, st.br_lo).mm(+1, g, N, qr, N).mm(-1, st.br_i, N, fr, H);
   L.out(st.tipB).add(+1, st.tipB).mm(+1, g, N, kk, N).mm(-1, st.br_i, N, g, H);
-  L.out(st.nbfill_c).mm(+1, fn, N, qr, N).mm(-1, st.BL, N, fr, H);
   L.out(st.bd_lo).add(+1, st.bd_lo).mm(+1, fr, N, qr, N).mm(-1, st.bfill_r, N, fr, H);
-  L.out(st.bc_n).add(+1, st.bc_n).mm(+1, fn, N, kk, N).mm(-1, st.BL, N, g, H);
-  L.out(st.bc_lo).add(+1, st.bc_lo).mm(+1, fr, N, kk, N).mm(-1, st.bfill_r, N, g, H);
+  if (sym) {
+    L.lower_only();
+  } else {
+    L.out(st.nbfill_c).mm(+1, fn, N, qr, N).mm(-1, st.BL, N, fr, H);
+    L.out(st.bc_n).add(+1, st.bc_n).mm(+1, fn, N, kk, N).mm(-1, st.BL, N, g, H);
+    L.out(st.bc_lo).add(+1, st.bc_lo).mm(+1, fr, N, kk, N).mm(-1, st.bfill_r, N, g, H);
+  }
   L.flush();
+  if (sym) {
+    for (const Mat* m : {&st.sb, &st.bd_n, &st.bd_lo})
+      cuda_check(launch_mirror_lower(m->p, m->ld, m->r, sym, sB), "mirror");
+    TransJob tj[3];
+    const Mat* src[3] = {&st.br_n, &st.br_lo, &st.nbfill_r};
+    const Mat* dst[3] = {&st.bc_n, &st.bc_lo, &st.nbfill_c};
+    for (int q = 0; q < 3; ++q) {
+      tj[q].src = src[q]->p, tj[q].lds = src[q]->ld, tj[q].r = src[q]->r, tj[q].c = src[q]->c;
+      tj[q].dst = dst[q]->p, tj[q].ldd = dst[q]->ld;
+    }
+    cuda_check(launch_conj_transpose(tj, 3, sym, sB), "conjugate transpose");
+  }
   cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
 }
 

@@ -130,3 +130,36 @@ def hermitianize_device(m: DeviceBta) -> DeviceBta:
 def kernel_launches() -> int:
     """Kernels launched by libbtasel_b200.so in this process."""
     return int(_native.load_library().bsel_kernel_launches())
+
+
+def bind_host_to_device(index: int | None = None):
+    """Bind the calling process to the CPUs local to CUDA device ``index``
+    (NVML CPU affinity of the GPU's PCI address), so pinned host buffers
+    allocated afterwards are first-touched on the GPU's NUMA node and the
+    host<->device streams of concurrent GPUs do not cross the socket
+    interconnect.  Returns the previous affinity set (pass it to
+    os.sched_setaffinity to undo), or None when NVML is unavailable."""
+    import os
+
+    try:
+        import pynvml
+    except Exception:  # pragma: no cover - optional dependency
+        return None
+    if index is None:
+        index = torch.cuda.current_device()
+    try:
+        prop = torch.cuda.get_device_properties(index)
+        bus = f"{prop.pci_domain_id:08x}:{prop.pci_bus_id:02x}:{prop.pci_device_id:02x}.0"
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {w * 64 + bit for w, m in enumerate(words) for bit in range(64) if (m >> bit) & 1}
+        cpus &= set(range(ncpu))
+        if not cpus:
+            return None
+        prev = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, cpus)
+        return prev
+    except Exception:  # NVML / affinity not permitted: leave the process as is
+        return None

@@ -739,9 +739,11 @@ class DistSolver:
     device buffers preallocated (the bench / multi-GPU production path)."""
 
     def __init__(self, A: DeviceBta, B: DeviceBta | None, mode: str, world: int, rank: int, device,
-                 transport: TorchCollectives | None = None):
+                 transport: TorchCollectives | None = None, plan_costs=None):
         self.A, self.B, self.mode = A, B if mode == "siq" else None, mode
-        self.plan = plan_partitions(A.n, world, mode)
+        # plan_costs: per-block (end, middle) costs for the partition sizes
+        # (default: the reference's plan, partition.py:52-90)
+        self.plan = plan_partitions(A.n, world, mode, costs=plan_costs)
         self.rank = rank
         self.coll = transport or TorchCollectives()
         self.out = (DeviceBta.empty(A.n, A.b, A.a, device),

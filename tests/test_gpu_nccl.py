@@ -62,11 +62,15 @@ def _rank(rank, world, port, n, b, a, q):
         for _ in range(2):
             s.solve(host_in=win, host_out=hout)
             torch.cuda.synchronize()
-            for R, H in zip(ref, hout):
-                assert torch.equal(H.diag, R[0]) and torch.equal(H.arrow_row, R[1])
-                assert torch.equal(H.lower, R[2]) and torch.equal(H.upper, R[3])
-                if rank == 0:
-                    assert torch.equal(H.tip, R[4])
+            # X_A bit-identical; X_B to rounding (the device-resident forward may
+            # take the Hermitian-B path, streamed chunks cannot know it in advance)
+            for side, (R, H) in enumerate(zip(ref, hout)):
+                got = (H.diag, H.arrow_row, H.lower, H.upper) + ((H.tip,) if rank == 0 else ())
+                for g_, r_ in zip(got, R):
+                    if side == 0:
+                        assert torch.equal(g_, r_)
+                    elif r_.numel():
+                        assert torch.linalg.norm(g_ - r_) <= 1e-12 * torch.linalg.norm(r_)
         dist.barrier()
         q.put((rank, err, kinds, None))
         dist.destroy_process_group()
