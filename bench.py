@@ -157,11 +157,29 @@ def reference_impl():
     return oracle, "port"
 
 
+def set_host_blas_threads(count):
+    """All host cores for the CPU reference path.  torchrun exports
+    OMP_NUM_THREADS=1 to every rank, which would make OpenBLAS single-threaded:
+    use the reference's own pool control (btasel.set_blas_threads,
+    threads.py:41-70), else threadpoolctl."""
+    ref, _ = reference_impl()
+    if hasattr(ref, "set_blas_threads"):
+        ref.set_blas_threads(count)
+        return
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(count)
+    except Exception:  # pragma: no cover
+        pass
+
+
 def cpu_sample(n_s, b, a, threads=None):
     """Time the CPU reference path (btasel solve_selected, or its oracle port,
     NumPy/SciPy on the host BLAS) on an n_s-block sample of the workload with
     the reference bench protocol inputs (bench.py:202-203).  Returns seconds."""
     ref, _ = reference_impl()
+    set_host_blas_threads(threads or host_cores())
     A = ref.generate_dd_bta(n_s, b, a, seed=0)
     B = ref.hermitianize(ref.generate_dd_bta(n_s, b, a, seed=1))
     t0 = time.perf_counter()
@@ -188,7 +206,7 @@ def run_reference(args, n, b, a):
     per = statistics.mean(times) / n_s * n * 1e3
     _, kind = reference_impl()
     what = ("unmodified reference btasel (baseline/_ref)" if kind == "reference" else "oracle port of btasel")
-    sample = (f"{what} solve_selected (NumPy/SciPy, OpenBLAS default threads) on "
+    sample = (f"{what} solve_selected (NumPy/SciPy, OpenBLAS on all {host_cores()} host cores) on "
               f"n={n_s} of {n} blocks (b={b}, a={a}), extrapolated linearly in n (reference acceptance "
               f"criterion 7)")
     cores = host_cores()
@@ -510,7 +528,7 @@ def main():
         _, kind = reference_impl()
         what = "reference btasel (baseline/_ref)" if kind == "reference" else "oracle port"
         cpu = {"value": t_s / n_s * n * 1e3, "unit": "ms", "cores": host_cores(), "kind": kind,
-               "sample": f"{what} (NumPy/SciPy, OpenBLAS default threads) solve_selected on n={n_s} of "
+               "sample": f"{what} (NumPy/SciPy, OpenBLAS on all host cores) solve_selected on n={n_s} of "
                          f"{n} blocks (b={b}, a={a}) took {t_s:.2f} s; extrapolated linearly in n"}
 
     if rank == 0:

@@ -20,6 +20,7 @@ constexpr int kBackBase = 16;   // first slot used by back_step (2 x kBackSlots)
 // The forward ring (kFwdDepth x kRing slots) overlaps the backward slots:
 // forward and backward never run concurrently on one context.
 static_assert(kFwdDepth * kRing <= 64, "forward ring exceeds the slot pool");
+static_assert(8 + 2 * kFwdDepth <= 64, "forward ring events");
 Mat rt(Context& ctx, int slot, int k, int r, int c) { return ctx.tmp(slot * kRing + k, r, c); }
 // CTA cap of the forward's aux-stream levels (BSEL_AUX_CTAS, 0 = none): a
 // capped level loops its tiles over fewer CTAs and leaves SMs to the chain.

@@ -23,7 +23,10 @@ struct EndStep {
 };
 // Forward ring: temporaries of step k live in ring slot fwd_slot(k); the
 // B side (aux stream) may lag the A chain by up to kFwdDepth - 1 steps.
-constexpr int kFwdDepth = 4;
+#ifndef BSEL_FWD_DEPTH
+#define BSEL_FWD_DEPTH 4
+#endif
+constexpr int kFwdDepth = BSEL_FWD_DEPTH;
 inline int fwd_slot(int64_t step) { return (int)(step % kFwdDepth); }
 cudaEvent_t ring_a_event(Context& ctx, int slot);  // A side of the slot's step reached its B fork
 cudaEvent_t ring_b_event(Context& ctx, int slot);  // B side of the slot's step done
@@ -88,7 +91,10 @@ struct BackStep {
 // runs ahead on the side stream, the X_A chain (2 levels per step) on the
 // high-priority chain stream, the X_B chain (2 levels per step, lagging) on
 // the aux stream; a ring of kBackDepth steps bounds the lag.
-constexpr int kBackDepth = 4;
+#ifndef BSEL_BACK_DEPTH
+#define BSEL_BACK_DEPTH 4
+#endif
+constexpr int kBackDepth = BSEL_BACK_DEPTH;
 // Slots of the context pool a backward sweep uses (reserve before begin()).
 int back_sweep_slots();
 class BackSweep {
