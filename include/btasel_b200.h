@@ -107,6 +107,10 @@ int bsel_context_set_inverse_grid(bsel_context_t* ctx, int ctas);
  * flags: bit 0 = B is not Hermitian, bit 1 = B is not anti-Hermitian
  * (3 if nothing was checked since the last forward began).               */
 int bsel_context_set_b_symmetry(bsel_context_t* ctx, int mode);
+/* Forward sweeps on this context keep SMs [0, n) free of their throughput
+ * (aux-stream) GEMM levels, so the Schur chain's inverse runs on SMs of its
+ * own (one partition per GPU: the chain is the critical path).  0 = off.  */
+int bsel_context_set_aux_avoid_sms(bsel_context_t* ctx, int n);
 int bsel_context_b_symmetry(bsel_context_t* ctx, int* flags, int* mode);
 /* Synchronizes; reports deferred device errors (singular pivots). */
 int bsel_synchronize(bsel_context_t* ctx, bsel_status_t* st);

@@ -28,6 +28,7 @@ EXPORTS = (
     "bsel_context_set_inverse_grid",
     "bsel_context_set_b_symmetry",
     "bsel_context_b_symmetry",
+    "bsel_context_set_aux_avoid_sms",
     "bsel_synchronize",
     "bsel_last_timings",
     "bsel_block_multiply_acc",
@@ -182,6 +183,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             "bsel_context_set_inverse_grid": ([vp, i32], i32),
             "bsel_context_set_b_symmetry": ([vp, i32], i32),
             "bsel_context_b_symmetry": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
+            "bsel_context_set_aux_avoid_sms": ([vp, i32], i32),
             "bsel_synchronize": ([vp, st], i32),
             "bsel_last_timings": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], i32),
             "bsel_block_multiply_acc": (
@@ -284,6 +286,11 @@ class Context:
         (general) or SYM_AUTO (this context's own check of B)."""
         if self.lib.bsel_context_set_b_symmetry(self.handle, int(mode)) != 0:
             raise ValueError(f"invalid symmetry mode {mode}")
+
+    def set_aux_avoid_sms(self, n: int) -> None:
+        """Forward aux GEMM levels leave SMs [0, n) to the chain (0 = off)."""
+        if self.lib.bsel_context_set_aux_avoid_sms(self.handle, int(n)) != 0:
+            raise ValueError(f"invalid SM count {n}")
 
     def b_symmetry(self) -> tuple[int, int]:
         """(flags of the last check of B, path the backward would take)."""

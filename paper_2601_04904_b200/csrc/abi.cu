@@ -226,6 +226,12 @@ int bsel_context_set_b_symmetry(bsel_context_t* ctx, int mode) {
   return BSEL_OK;
 }
 
+int bsel_context_set_aux_avoid_sms(bsel_context_t* ctx, int n) {
+  if (!ctx || n < 0 || n >= device_sm_count()) return BSEL_ERR_ARG;
+  ctx->impl->set_aux_avoid_sms(n);
+  return BSEL_OK;
+}
+
 int bsel_context_b_symmetry(bsel_context_t* ctx, int* flags, int* mode) {
   if (!ctx) return BSEL_ERR_ARG;
   if (flags) *flags = ctx->impl->sym_flags();

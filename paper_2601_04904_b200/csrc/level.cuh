@@ -42,6 +42,15 @@ class Level {
   explicit Level(cudaStream_t s, int tile_cfg = kTileAuto, int max_ctas = 0) : s_(s), cfg_(tile_cfg) {
     b_.nproblems = 0;
     b_.max_ctas = max_ctas;
+    b_.avoid_sms = 0;
+    b_.tile_counter = nullptr;
+  }
+  // Keep SMs [0, n) free of this level's CTAs (zgemm.cuh avoid_sms); counter:
+  // a device u32 owned by this level's stream.
+  Level& avoid_sms(int n, unsigned* counter) {
+    b_.avoid_sms = counter ? n : 0;
+    b_.tile_counter = counter;
+    return *this;
   }
   ~Level() noexcept(false) {}
 

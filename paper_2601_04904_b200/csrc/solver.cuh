@@ -113,6 +113,11 @@ class Context {
   // to the forward steps.
   int sym_now(cudaStream_t s);
   void set_forward_symmetry(int s) { fwd_sym_ = s; }
+  // Forward aux-stream levels keep SMs [0, n) free for the Schur chain's
+  // inverse (zgemm.cuh avoid_sms); 0 = off.  aux_counter(): their tile counter.
+  void set_aux_avoid_sms(int n) { aux_avoid_ = n; }
+  int aux_avoid_sms() const { return aux_avoid_; }
+  unsigned* aux_counter() const { return d_aux_counter_; }
   int forward_symmetry() const { return fwd_sym_; }
 
   // Singularity bookkeeping (device side, checked at synchronize()).
@@ -149,6 +154,8 @@ class Context {
   int64_t inv_work_elems_ = 0;
   int* d_flag_ = nullptr;
   int* d_sym_ = nullptr;
+  unsigned* d_aux_counter_ = nullptr;
+  int aux_avoid_ = 0;
   int sym_flags_ = 3, sym_mode_ = kSymAuto, fwd_sym_ = 0;
   bool sym_checked_ = false;
   unsigned long long* d_status_ = nullptr;

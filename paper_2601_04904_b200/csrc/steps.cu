@@ -82,6 +82,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     }
     cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
     Level LB(sB, kTileAuto, aux_ctas());
+    LB.avoid_sms(ctx.aux_avoid_sms(), ctx.aux_counter());
     LB.out(t2).mm(+1, S, N, st.ac_i, N);
     LB.out(st.ar_j).add(+1, st.ar_j).mm(-1, st.ar_i, N, t1, N);
     LB.flush();
@@ -116,6 +117,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   // which also removes the reference's serial chain w -> S_B -> v -> Bd.
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
   Level L(sB, kTileAuto, aux_ctas());
+  L.avoid_sms(ctx.aux_avoid_sms(), ctx.aux_counter());
   L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(w).mm(+1, S, N, st.bd_i, N);
   L.out(q).add(-1, st.BU).mm(+1, st.bd_i, N, f, H);
@@ -171,6 +173,7 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   }
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
   Level L(sB, kTileAuto, aux_ctas());
+  L.avoid_sms(ctx.aux_avoid_sms(), ctx.aux_counter());
   L.out(fr).mm(+1, st.fill_r, N, S, N);
   L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(st.nfill_c).mm(-1, fn, N, st.fill_c, N);

@@ -32,6 +32,7 @@ Context::Context(int device) : device_(device) {
   cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "flag");
   cuda_check(cudaMalloc(&d_status_, sizeof(unsigned long long)), "status");
   cuda_check(cudaMalloc(&d_sym_, sizeof(int)), "symmetry flags");
+  cuda_check(cudaMalloc(&d_aux_counter_, 2 * sizeof(unsigned)), "aux tile counter");
   events_.resize(64);
   for (auto& e : events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& t : timers_) cuda_check(cudaEventCreate(&t), "timer");
@@ -47,6 +48,7 @@ Context::~Context() {
   if (d_flag_) cudaFree(d_flag_);
   if (d_status_) cudaFree(d_status_);
   if (d_sym_) cudaFree(d_sym_);
+  if (d_aux_counter_) cudaFree(d_aux_counter_);
   for (auto& e : events_) cudaEventDestroy(e);
   for (auto& t : timers_) cudaEventDestroy(t);
   for (auto& e : xfer_events_) cudaEventDestroy(e);

@@ -152,8 +152,24 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const int wm = warp / C::WN;
   const int wn = warp % C::WN;
 
-  for (int bid = blockIdx.x; bid < batch.total_tiles; bid += gridDim.x) {
-  if (bid != (int)blockIdx.x) __syncthreads();  // previous tile's readers of the stages are done
+  const bool dyn = batch.avoid_sms > 0;
+  __shared__ int s_tile;
+  if (dyn) {
+    // CTAs on avoided SMs leave at once, except the grid's last CTA to
+    // leave, which then works off whatever no other CTA took (a small launch
+    // on an idle GPU may land entirely on the avoided SMs).
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if ((int)smid < batch.avoid_sms) {
+      if (tid == 0) s_tile = (int)atomicAdd(batch.tile_counter + 1, 1u);
+      __syncthreads();
+      if (s_tile != (int)gridDim.x - 1) return;
+      __syncthreads();
+    }
+    if (tid == 0) s_tile = (int)atomicAdd(batch.tile_counter, 1u);
+    __syncthreads();
+  }
+  for (int bid = dyn ? s_tile : (int)blockIdx.x; bid < batch.total_tiles;) {
   // Locate the problem / tile of this CTA.
   int pi = 0;
   while (pi + 1 < batch.nproblems && bid >= batch.p[pi + 1].tile_begin) ++pi;
@@ -279,6 +295,26 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       P.D[(int64_t)m * P.ldd + n] = make_double2(re, imv);
     }
   }
+  // next tile (the barrier also orders this tile's stage reads before the
+  // next tile's prologue overwrites the stages)
+  if (dyn) {
+    __syncthreads();
+    if (tid == 0) s_tile = (int)atomicAdd(batch.tile_counter, 1u);
+    __syncthreads();
+    bid = s_tile;
+    if (bid >= batch.total_tiles) {  // leaving: count it (see above)
+      __syncthreads();
+      if (tid == 0) s_tile = (int)atomicAdd(batch.tile_counter + 1, 1u);
+      __syncthreads();
+      if (s_tile != (int)gridDim.x - 1) break;
+      // the last CTA to leave: take what is left (nothing, since this CTA
+      // fetched until the tiles ran out)
+      break;
+    }
+  } else {
+    bid += gridDim.x;
+    __syncthreads();
+  }
   }  // tile loop
 }
 
@@ -317,6 +353,11 @@ cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
     prof = profile_open(stream);
   }
   const int grid = batch.max_ctas > 0 && batch.max_ctas < tiles ? batch.max_ctas : tiles;
+  if (batch.avoid_sms > 0) {
+    if (!batch.tile_counter) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(batch.tile_counter, 0, 2 * sizeof(unsigned), stream);
+    if (e != cudaSuccess) return e;
+  }
   zgemm_grouped_kernel<C><<<grid, C::THREADS, C::SMEM, stream>>>(batch);
   count_launch();
   profile_close(prof, stream, 0, flops, bytes);

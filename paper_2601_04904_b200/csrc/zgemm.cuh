@@ -67,7 +67,12 @@ struct GemmBatch {
   // > 0: launch at most max_ctas CTAs that loop over the tiles (leaves SMs
   // free for a concurrent latency-critical chain); 0: one CTA per tile
   int32_t max_ctas;
-  int32_t pad_;
+  // > 0: CTAs landing on SMs with id < avoid_sms exit at once and the others
+  // fetch tiles dynamically from tile_counter[0] (tile_counter[1] counts the
+  // CTAs that left; both zeroed by the launcher):
+  // those SMs stay free for a concurrent latency-critical kernel
+  int32_t avoid_sms;
+  unsigned* tile_counter;
   GemmProblem p[kMaxProblems];
 };
 

@@ -675,7 +675,12 @@ def dist_solve(a, b=None, num_parts=2, mode=None, transport=None, *, counter=Non
         cnt = OpCounter(b=A.b, a=A.a)
         try:
             tm.start("forward")
-            pay, delta, fac = local_forward(A, B, plan, rank, cnt)
+            ctx = _native.Context.get(dev.index)
+            ctx.set_aux_avoid_sms(AUX_AVOID_SMS)
+            try:
+                pay, delta, fac = local_forward(A, B, plan, rank, cnt, _ctx=ctx)
+            finally:
+                ctx.set_aux_avoid_sms(0)
             tm.stop("forward")
         except Exception as exc:  # rank attribution (dist.py:875-885)
             raise WorkerError(rank, exc) from exc
@@ -734,6 +739,11 @@ def dist_solve(a, b=None, num_parts=2, mode=None, transport=None, *, counter=Non
     return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
 
 
+# SMs the forward's throughput GEMM levels leave to a single lane's chain
+# (measured, n=512 one lane: forward 343 -> 322 ms with 32; 16 and 48 worse)
+AUX_AVOID_SMS = int(os.environ.get("BSEL_AUX_AVOID_SMS", "32"))
+
+
 class DistSolver:
     """Repeated distributed solves of one energy point on this rank with all
     device buffers preallocated (the bench / multi-GPU production path)."""
@@ -771,8 +781,15 @@ class DistSolver:
             lo, hi = self.plan.ranges[self.rank]
             self._fac = _alloc_factors(self.plan.kinds[self.rank], lo, hi, fused, self.A.b, self.A.a,
                                        self.A.device)
-        pay, delta, self._fac = local_forward(self.A, self.B, self.plan, self.rank, _factors=self._fac,
-                                              _sync=io_in)
+        # one partition per GPU: its Schur chain is the forward's critical
+        # path, so the throughput levels leave the inverse SMs of its own
+        ctx = _native.Context.get(self.A.device.index)
+        ctx.set_aux_avoid_sms(AUX_AVOID_SMS)
+        try:
+            pay, delta, self._fac = local_forward(self.A, self.B, self.plan, self.rank, _factors=self._fac,
+                                                  _ctx=ctx, _sync=io_in)
+        finally:
+            ctx.set_aux_avoid_sms(0)
         tm.stop("forward")
         tm.start("communication")
         reduced = assemble_reduced(self.coll, self.A, self.B, self.plan, pay, delta)

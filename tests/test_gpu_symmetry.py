@@ -151,3 +151,23 @@ def test_zero_leaf_pivot_fallback(monkeypatch, b, schur):
     xa, xb = oracle.solve_selected(A2, B, "siq")
     assert max_block_rel_err(sol.x_a, xa) <= TOL
     assert max_block_rel_err(sol.x_b, xb) <= TOL
+
+
+@pytest.mark.parametrize("avoid", [32, 147])
+@pytest.mark.parametrize("kind", ["hermitian", "general"])
+def test_aux_levels_avoiding_sms(avoid, kind):
+    """Forward aux GEMM levels that keep SMs [0, avoid) free (one partition
+    per GPU) fetch tiles dynamically; with nearly every SM avoided the last
+    CTA to leave works off the tiles -- results unchanged."""
+    n, b, a = 9, 72, 20
+    A = bs.generate_dd_bta(n, b, a, seed=15)
+    B = rhs(n, b, a, kind, seed=16)
+    ctx = _native.Context.get(torch.cuda.current_device())
+    ctx.set_aux_avoid_sms(avoid)
+    try:
+        sol = bs.solve_selected(A, B, "siq", partitions=1)
+    finally:
+        ctx.set_aux_avoid_sms(0)
+    xa, xb = oracle.solve_selected(A, B, "siq")
+    assert max_block_rel_err(sol.x_a, xa) <= TOL
+    assert max_block_rel_err(sol.x_b, xb) <= TOL
