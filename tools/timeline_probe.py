@@ -13,6 +13,8 @@ parts = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 mode = sys.argv[3] if len(sys.argv) > 3 else "siq"
 path = os.environ.setdefault("BSEL_PROFILE_DUMP", "/tmp/timeline.csv")
+if os.environ.get("PROBE_AVOID_SMS"):  # one lane: aux levels leave SMs to the chain (DistSolver default)
+    _native.Context.get(torch.cuda.current_device()).set_aux_avoid_sms(int(os.environ["PROBE_AVOID_SMS"]))
 A = bs.generate_dd_bta_device(n, 512, 256, seed=0)
 B = bs.hermitianize_device(bs.generate_dd_bta_device(n, 512, 256, seed=1))
 Bm = B if mode == "siq" else None
