@@ -775,7 +775,8 @@ class DistSolver:
             self._copy_separators(host_in)
         if host_out is not None:
             io_out = _host_io(chunk, x_a=host_out[0], x_b=host_out[1] if fused else None)
-        tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
+        tm = _PhaseTimer(("forward", "communication", "reduced", "backward", "step"))
+        tm.start("step")
         tm.start("forward")
         if self._fac is None:
             lo, hi = self.plan.ranges[self.rank]
@@ -801,6 +802,7 @@ class DistSolver:
         local_backward(self.A, self.B, self.plan, self.rank, self._fac, reduced, red_sol, out=self.out,
                        _sync=io_out)
         tm.stop("backward")
+        tm.stop("step")
         self._tm = tm
         return self.out
 
