@@ -84,6 +84,9 @@ typedef struct {
   double* elim_q;           /* [n][b][b]   (fused)                          */
   double* elim_k;           /* [n][b][a]   (fused)                          */
   double* elim_h;           /* [n][b][b]   S_i A(i,j)                       */
+  double* elim_ha;          /* [n][b][a]   S_i AC_i                         */
+  double* elim_eq;          /* [n][b][b]   -S_i elim_q      (fused)         */
+  double* elim_ek;          /* [n][b][a]   -S_i elim_k      (fused)         */
 } bsel_factors_t;
 
 typedef struct bsel_context bsel_context_t;
@@ -176,6 +179,9 @@ typedef struct {
   double* elim_fr;    /* [len][b][b]  (middle)                           */
   double* elim_qr;    /* [len][b][b]  (middle, fused)                    */
   double* elim_h;     /* [len][b][b]  S_i U_i (U = the coupling eliminated along) */
+  double* elim_ha;    /* [len][b][a]  S_i AC_i                           */
+  double* elim_eq;    /* [len][b][b]  -S_i elim_q   (fused)              */
+  double* elim_ek;    /* [len][b][a]  -S_i elim_k   (fused)              */
 } bsel_local_factors_t;
 /* Optional end-to-end mode (no reference counterpart; the reference moves
  * whole matrices with cupy before/after its sweeps): the full-size matrices

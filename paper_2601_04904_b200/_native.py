@@ -91,6 +91,9 @@ class Factors(ctypes.Structure):
         ("elim_q", ctypes.c_void_p),
         ("elim_k", ctypes.c_void_p),
         ("elim_h", ctypes.c_void_p),
+        ("elim_ha", ctypes.c_void_p),
+        ("elim_eq", ctypes.c_void_p),
+        ("elim_ek", ctypes.c_void_p),
     ]
 
 
@@ -139,6 +142,9 @@ class LocalFactors(ctypes.Structure):
         ("elim_fr", ctypes.c_void_p),
         ("elim_qr", ctypes.c_void_p),
         ("elim_h", ctypes.c_void_p),
+        ("elim_ha", ctypes.c_void_p),
+        ("elim_eq", ctypes.c_void_p),
+        ("elim_ek", ctypes.c_void_p),
     ]
 
 

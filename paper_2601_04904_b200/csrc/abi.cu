@@ -9,6 +9,7 @@
 #include "generate.cuh"
 #include "inverse.cuh"
 #include "partition.cuh"
+#include "steps.cuh"
 #include "solver.cuh"
 
 struct bsel_context {
@@ -100,6 +101,9 @@ FactorsDev to_dev(const bsel_factors_t& f) {
   d.elim_q = dp(f.elim_q);
   d.elim_k = dp(f.elim_k);
   d.elim_h = dp(f.elim_h);
+  d.elim_ha = dp(f.elim_ha);
+  d.elim_eq = dp(f.elim_eq);
+  d.elim_ek = dp(f.elim_ek);
   return d;
 }
 
@@ -142,7 +146,7 @@ __global__ void axpby_kernel(double2* d, int64_t ldd, const double2* x, int64_t 
 }
 
 struct SolveLayout {
-  size_t off[18];
+  size_t off[21];
   size_t total;
 };
 
@@ -176,6 +180,12 @@ SolveLayout solve_layout(int64_t n, int64_t b, int64_t a, bool fused) {
   take(13, n * b * b);  // elim_f
   take(14, n * a * b);  // elim_g
   take(17, n * b * b);  // elim_h
+  const bool extra = fwd_backward_products();
+  if (extra || !fused) take(18, n * b * a);  // elim_ha
+  if (fused && extra) {
+    take(19, n * b * b);  // elim_eq
+    take(20, n * b * a);  // elim_ek
+  }
   L.total = cur + 256;
   return L;
 }
@@ -433,6 +443,12 @@ int bsel_solve_selected(bsel_context_t* ctx, const bsel_bta_t* a, const bsel_bta
     F.elim_f = at(13);
     F.elim_g = as > 0 ? at(14) : nullptr;
     F.elim_h = at(17);
+    const bool extra = fwd_backward_products();
+    F.elim_ha = as > 0 && (extra || !fused) ? at(18) : nullptr;
+    if (fused && extra) {
+      F.elim_eq = at(19);
+      F.elim_ek = as > 0 ? at(20) : nullptr;
+    }
     BtaDev B;
     if (fused) {
       B = to_dev(*b);
@@ -486,6 +502,9 @@ static LocalFactorsDev to_dev(const bsel_local_factors_t& f, int64_t b, int64_t 
   d.elim_fr = dp(f.elim_fr);
   d.elim_qr = dp(f.elim_qr);
   d.elim_h = dp(f.elim_h);
+  d.elim_ha = dp(f.elim_ha);
+  d.elim_eq = dp(f.elim_eq);
+  d.elim_ek = dp(f.elim_ek);
   return d;
 }
 

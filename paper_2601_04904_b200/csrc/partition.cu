@@ -212,8 +212,11 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.bc_i = ac(*WB, i), st.bc_j = ac(*WB, j), st.tipB = WB->T();
         st.sb = F.SB(i - lo);
         st.f_out = F.EF(i - lo), st.g_out = F.EG(i - lo), st.q_out = F.EQ(i - lo), st.k_out = F.EK(i - lo);
+        if (fwd_backward_products()) st.eq_out = F.EEQ(i - lo), st.ek_out = F.EEK(i - lo);
       }
-      st.h_out = F.EH(i - lo);
+      const bool extra = !fused || fwd_backward_products();
+      if (extra || ctx.schur_ok((int)b)) st.h_out = F.EH(i - lo);
+      if (extra) st.ha_out = F.EHA(i - lo);
       end_step(ctx, st, fused, (uint64_t)s, i, fwd_slot(s));
       if (trace && (s + 1) % C == 0) tev(tstep, ctx.chain());
     }
@@ -240,8 +243,9 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.sb = F.SB(i - lo);
         st.fn_out = F.EF(i - lo), st.fr_out = F.EFR(i - lo), st.g_out = F.EG(i - lo);
         st.qn_out = F.EQ(i - lo), st.qr_out = F.EQR(i - lo), st.kk_out = F.EK(i - lo);
+        if (fwd_backward_products()) st.ha_out = F.EHA(i - lo), st.eq_out = F.EEQ(i - lo), st.ek_out = F.EEK(i - lo);
       }
-      st.h_out = F.EH(i - lo);
+      if ((fused && fwd_backward_products()) || ctx.schur_ok((int)b)) st.h_out = F.EH(i - lo);
       middle_step(ctx, st, fused, (uint64_t)s, i, fwd_slot(s));
     }
   }
@@ -354,11 +358,16 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
       st.ya[0][0] = XA.D(p), st.ya[0][1] = XA.AC(p), st.ya[1][0] = XA.AR(p), st.ya[1][1] = ytt;
       st.row[0] = down ? XA.U(e) : XA.L(e), st.row[1] = XA.AC(i);
       st.col[0] = down ? XA.L(e) : XA.U(e), st.col[1] = XA.AR(i);
+      {  // retained by the forward (see local_forward)
+        const bool extra = !fused || fwd_backward_products();
+        if (extra || ctx.schur_ok((int)b)) st.hpre[0] = F.EH(i - lo);
+        if (extra) st.hpre[1] = F.EHA(i - lo);
+      }
       st.diag = XA.D(i);
       if (fused) {
         st.sc = F.SB(i - lo);
         st.cpre[0] = F.EF(i - lo), st.cpre[1] = F.EG(i - lo), st.qpre[0] = F.EQ(i - lo), st.qpre[1] = F.EK(i - lo);
-        if (ctx.schur_ok((int)b)) st.hpre[0] = F.EH(i - lo);
+        if (fwd_backward_products()) st.epre[0] = F.EEQ(i - lo), st.epre[1] = F.EEK(i - lo);
         st.ss[0] = down ? B->U(e) : B->L(e), st.ss[1] = el(*WB, i, false);
         st.ws[0] = down ? B->L(e) : B->U(e), st.ws[1] = el(*WB, i, true);
         st.yb[0][0] = XB->D(p), st.yb[0][1] = XB->AC(p), st.yb[1][0] = XB->AR(p), st.yb[1][1] = ztt;
@@ -406,7 +415,12 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
         st.sc = F.SB(i - lo);
         st.cpre[0] = F.EFR(i - lo), st.cpre[1] = F.EF(i - lo), st.cpre[2] = F.EG(i - lo);
         st.qpre[0] = F.EQR(i - lo), st.qpre[1] = F.EQ(i - lo), st.qpre[2] = F.EK(i - lo);
-        if (ctx.schur_ok((int)b)) st.hpre[1] = F.EH(i - lo);
+        if (fwd_backward_products()) {
+          st.hpre[1] = F.EH(i - lo), st.hpre[2] = F.EHA(i - lo);
+          st.epre[1] = F.EEQ(i - lo), st.epre[2] = F.EEK(i - lo);
+        } else if (ctx.schur_ok((int)b)) {
+          st.hpre[1] = F.EH(i - lo);
+        }
         st.ss[0] = F.BFC(i - lo), st.ss[1] = B->U(i), st.ss[2] = el(*WB, i, false);
         st.ws[0] = F.BFR(i - lo), st.ws[1] = B->L(i), st.ws[2] = el(*WB, i, true);
         const Mat z00 = XB->D(lo), z0t = XB->AC(lo), zt0 = XB->AR(lo);

@@ -28,7 +28,13 @@ struct LocalFactorsDev {
   double2* elim_fr = nullptr;
   double2* elim_qr = nullptr;
   double2* elim_h = nullptr;
+  double2* elim_ha = nullptr;
+  double2* elim_eq = nullptr;
+  double2* elim_ek = nullptr;
   Mat EH(int64_t k) const { return elim_h ? blk(elim_h, k, (int)b, (int)b) : Mat{}; }
+  Mat EHA(int64_t k) const { return elim_ha ? blk(elim_ha, k, (int)b, (int)a) : Mat{}; }
+  Mat EEQ(int64_t k) const { return elim_eq ? blk(elim_eq, k, (int)b, (int)b) : Mat{}; }
+  Mat EEK(int64_t k) const { return elim_ek ? blk(elim_ek, k, (int)b, (int)a) : Mat{}; }
   Mat EF(int64_t k) const { return elim_f ? blk(elim_f, k, (int)b, (int)b) : Mat{}; }
   Mat EG(int64_t k) const { return elim_g ? blk(elim_g, k, (int)a, (int)b) : Mat{}; }
   Mat EQ(int64_t k) const { return elim_q ? blk(elim_q, k, (int)b, (int)b) : Mat{}; }

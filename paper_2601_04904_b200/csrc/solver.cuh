@@ -46,8 +46,14 @@ struct FactorsDev {
   double2* elim_g = nullptr;  // [n][a][b]  AR_i S_i
   double2* elim_q = nullptr;  // [n][b][b]  Bd_i f^H - B(i,j)
   double2* elim_k = nullptr;  // [n][b][a]  Bd_i g^H - BC_i
-  double2* elim_h = nullptr;  // [n][b][b]  S_i A(i,j)
+  double2* elim_h = nullptr;   // [n][b][b]  S_i A(i,j)
+  double2* elim_ha = nullptr;  // [n][b][a]  S_i AC_i
+  double2* elim_eq = nullptr;  // [n][b][b]  -S_i elim_q
+  double2* elim_ek = nullptr;  // [n][b][a]  -S_i elim_k
   Mat EH(int64_t i) const { return elim_h ? blk(elim_h, i, (int)b, (int)b) : Mat{}; }
+  Mat EHA(int64_t i) const { return elim_ha ? blk(elim_ha, i, (int)b, (int)a) : Mat{}; }
+  Mat EEQ(int64_t i) const { return elim_eq ? blk(elim_eq, i, (int)b, (int)b) : Mat{}; }
+  Mat EEK(int64_t i) const { return elim_ek ? blk(elim_ek, i, (int)b, (int)a) : Mat{}; }
   Mat EF(int64_t i) const { return elim_f ? blk(elim_f, i, (int)b, (int)b) : Mat{}; }
   Mat EG(int64_t i) const { return elim_g ? blk(elim_g, i, (int)a, (int)b) : Mat{}; }
   Mat EQ(int64_t i) const { return elim_q ? blk(elim_q, i, (int)b, (int)b) : Mat{}; }

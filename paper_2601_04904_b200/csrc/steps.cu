@@ -33,6 +33,14 @@ int aux_ctas() {
 }
 }  // namespace
 
+bool fwd_backward_products() {
+  static const bool on = [] {
+    const char* e = getenv("BSEL_FWD_BWD_PRODUCTS");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
 cudaEvent_t ring_a_event(Context& ctx, int slot) { return ctx.event(8 + slot); }
 cudaEvent_t ring_b_event(Context& ctx, int slot) { return ctx.event(8 + kFwdDepth + slot); }
 
@@ -66,7 +74,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   const Mat& S = st.S;
   if (!fused) {
     // rgf.py:283-288 / dist.py:252-257: right-hand temporaries.
-    Mat t1 = st.h_out.p ? st.h_out : rt(ctx, slot, 0, b, b), t2 = rt(ctx, slot, 1, b, a);
+    Mat t1 = st.h_out.p ? st.h_out : rt(ctx, slot, 0, b, b), t2 = st.ha_out.p ? st.ha_out : rt(ctx, slot, 1, b, a);
     if (schur) {  // S, t1 = S Uk and ad_j -= Lk t1 in one launch
       ctx.schur(st.ad_i, st.Uk, st.Lk, st.ad_j, S, t1, st.f_out.p ? st.f_out : rt(ctx, slot, 2, b, b), order, index,
                 sA);
@@ -122,6 +130,10 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   L.out(w).mm(+1, S, N, st.bd_i, N);
   L.out(q).add(-1, st.BU).mm(+1, st.bd_i, N, f, H);
   L.out(st.ac_j).add(+1, st.ac_j).mm(-1, f, N, st.ac_i, N);
+  // the backward step's h_l (g rs_l) formed here, where the chain-bound
+  // forward leaves the SMs room, instead of in the throughput-bound backward
+  if (st.h_out.p && !schur) L.out(st.h_out).mm(+1, S, N, st.Uk, N);
+  if (st.ha_out.p) L.out(st.ha_out).mm(+1, S, N, st.ac_i, N);
   L.flush();
   L.out(st.ar_j).add(+1, st.ar_j).mm(-1, g, N, st.Uk, N);
   L.out(st.tipA).add(+1, st.tipA).mm(-1, g, N, st.ac_i, N);
@@ -135,6 +147,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   L.out(st.bd_j).add(+1, st.bd_j).mm(+1, f, N, q, N).mm(-1, st.BL, N, f, H);
   if (sym) L.lower_only();
   L.out(st.br_j).add(+1, st.br_j).mm(+1, g, N, q, N).mm(-1, st.br_i, N, f, H);
+  if (st.eq_out.p) L.out(st.eq_out).mm(-1, S, N, q, N);  // the backward's e_0 = -g q
   L.flush();
   if (sym) {
     cuda_check(launch_mirror_lower(st.sb.p, st.sb.ld, st.sb.r, sym, sB), "mirror");
@@ -147,6 +160,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     L.out(st.bc_j).add(+1, st.bc_j).mm(+1, f, N, k, N).mm(-1, st.BL, N, g, H);
   }
   L.out(st.tipB).add(+1, st.tipB).mm(+1, g, N, k, N).mm(-1, st.br_i, N, g, H);
+  if (st.ek_out.p) L.out(st.ek_out).mm(-1, S, N, k, N);  // the backward's e_1 = -g k
   L.flush();
   cuda_check(cudaEventRecord(ring_b_event(ctx, slot), sB), "record B");
 }
@@ -187,6 +201,9 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     kk = keep(st.kk_out, 7, b, a);
     L.out(w).mm(+1, S, N, st.bd_i, N);
     L.out(qn).add(-1, st.BU).mm(+1, st.bd_i, N, fn, H);
+    // the backward step's h for the U and arrow couplings (see end_step)
+    if (st.h_out.p && !ctx.schur_ok(b)) L.out(st.h_out).mm(+1, S, N, st.U, N);
+    if (st.ha_out.p) L.out(st.ha_out).mm(+1, S, N, st.ac_i, N);
   }
   L.flush();
   L.out(st.nfill_r).mm(-1, fr, N, st.U, N);
@@ -212,7 +229,9 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   if (sym) L.lower_only();
   L.out(st.br_n).add(+1, st.br_n).mm(+1, g, N, qn, N).mm(-1, st.br_i, N, fn, H);
   L.out(st.nbfill_r).mm(+1, fr, N, qn, N).mm(-1, st.bfill_r, N, fn, H);
+  if (st.eq_out.p) L.out(st.eq_out).mm(-1, S, N, qn, N);
   L.flush();
+  if (st.ek_out.p) L.out(st.ek_out).mm(-1, S, N, kk, N);
   L.out(st.br_lo).add(+1, st.br_lo).mm(+1, g, N, qr, N).mm(-1, st.br_i, N, fr, H);
   L.out(st.tipB).add(+1, st.tipB).mm(+1, g, N, kk, N).mm(-1, st.br_i, N, g, H);
   L.out(st.bd_lo).add(+1, st.bd_lo).mm(+1, fr, N, qr, N).mm(-1, st.bfill_r, N, fr, H);
@@ -326,7 +345,8 @@ void BackSweep::step(BackStep& st) {
       else P.out(c[l]).mm(+1, st.qs[l], N, st.g, N);
       if (fused) {
         // e_l = g ss_l - sc qs_l^H = -g (Bd c_l^H - ss_l)  (sc = g Bd g^H)
-        if (st.qpre[l].p) P.out(e[l]).mm(-1, st.g, N, st.qpre[l], N);
+        if (st.epre[l].p) e[l] = st.epre[l];
+        else if (st.qpre[l].p) P.out(e[l]).mm(-1, st.g, N, st.qpre[l], N);
         else P.out(e[l]).mm(+1, st.g, N, st.ss[l], N).mm(-1, st.sc, N, st.qs[l], H);
         if (!sym) P.out(f[l]).mm(+1, st.ws[l], N, st.g, H).mm(-1, st.qs[l], N, st.sc, N);
       }

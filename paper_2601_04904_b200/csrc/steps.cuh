@@ -20,6 +20,9 @@ struct EndStep {
   // here (the backward step of block i reuses them) instead of ring slots
   Mat f_out, g_out, q_out, k_out;
   Mat h_out;  // optional: h = S Uk (the backward's h_0), free with the fused Schur step
+  // optional, formed on the aux stream for the backward step of this block
+  // (which then has no prologue): ha = S AC_i, eq = -S q, ek = -S k
+  Mat ha_out, eq_out, ek_out;
 };
 // Forward ring: temporaries of step k live in ring slot fwd_slot(k); the
 // B side (aux stream) may lag the A chain by up to kFwdDepth - 1 steps.
@@ -46,8 +49,16 @@ struct MiddleStep {
   // g = AR_i S, qn = Bd fn^H - BU, qr = Bd fr^H - bfill_c, kk = Bd g^H - BC_i
   Mat fn_out, fr_out, g_out, qn_out, qr_out, kk_out;
   Mat h_out;  // optional: h = S U
+  Mat ha_out, eq_out, ek_out;  // optional: S AC_i, -S qn, -S kk (see EndStep)
 };
 void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order, int64_t index, int slot);
+
+// BSEL_FWD_BWD_PRODUCTS=1: the fused forward also forms the backward step's
+// h and e products (EndStep/MiddleStep ha_out, eq_out, ek_out, h_out) on its
+// aux stream.  Off by default: the chain-bound forward absorbs them only at
+// the cost of more contention on its chain (config 4: 1 GPU 1057 vs 1055 ms,
+// 2 GPUs 626 vs 684 ms).
+bool fwd_backward_products();
 
 // Wait for the B side of the step that last used ring slot `parity` (call
 // before reusing it) and join both streams at the end of a sweep.
@@ -68,7 +79,8 @@ struct BackStep {
   // optional products retained by the forward step of this block:
   // cpre[l] = qs_l g, qpre[l] = Bd (qs_l g)^H - ss_l  (then e_l = -g qpre[l])
   Mat cpre[3], qpre[3];
-  Mat hpre[3];  // optional: h_l = g rs_l (from the fused Schur step)
+  Mat hpre[3];  // optional: h_l = g rs_l (retained by the forward)
+  Mat epre[3];  // optional: e_l (retained by the forward)
   // outputs
   Mat row[3], col[3], diag;
   Mat zrow[3], zcol[3], zdiag;

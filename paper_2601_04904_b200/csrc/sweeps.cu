@@ -313,8 +313,13 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
       st.bc_i = B->AC(i), st.bc_j = B->AC(i + 1), st.tipB = B->T();
       st.sb = F.SB(i);
       st.f_out = F.EF(i), st.g_out = F.EG(i), st.q_out = F.EQ(i), st.k_out = F.EK(i);
+      if (fwd_backward_products()) st.eq_out = F.EEQ(i), st.ek_out = F.EEK(i);
     }
-    st.h_out = F.EH(i);
+    // SI: h = S U and S AC_i are the forward's own temporaries; fused: only
+    // with the Schur step (h) or BSEL_FWD_BWD_PRODUCTS
+    const bool extra = !fused || fwd_backward_products();
+    if (extra || ctx.schur_ok(b)) st.h_out = F.EH(i);
+    if (extra) st.ha_out = F.EHA(i);
     end_step(ctx, st, fused, i, i, fwd_slot(i));
   }
   // Epilogue (rgf.py:290-318).  The last block's arrow strips and the tip
@@ -448,10 +453,15 @@ void bta_backward_arrow(Context& ctx, const FactorsDev& F, const BtaDev& A, cons
       st.ya[0][0] = XA.D(i + 1), st.ya[0][1] = XA.AC(i + 1), st.ya[1][0] = XA.AR(i + 1), st.ya[1][1] = Xtt;
       if (!diag_only) st.row[0] = XA.U(i), st.col[0] = XA.L(i);
       st.row[1] = XA.AC(i), st.col[1] = XA.AR(i);
+      {  // retained by the forward (see bta_forward_arrow)
+        const bool extra = !fused || fwd_backward_products();
+        if (extra || ctx.schur_ok(b)) st.hpre[0] = F.EH(i);
+        if (extra) st.hpre[1] = F.EHA(i);
+      }
       if (fused) {
         st.sc = F.SB(i);
         st.cpre[0] = F.EF(i), st.cpre[1] = F.EG(i), st.qpre[0] = F.EQ(i), st.qpre[1] = F.EK(i);
-        if (ctx.schur_ok(b)) st.hpre[0] = F.EH(i);
+        if (fwd_backward_products()) st.epre[0] = F.EEQ(i), st.epre[1] = F.EEK(i);
         st.ss[0] = B->U(i), st.ss[1] = F.BCe(i);
         st.ws[0] = B->L(i), st.ws[1] = F.BRe(i);
         st.yb[0][0] = XB->D(i + 1), st.yb[0][1] = XB->AC(i + 1), st.yb[1][0] = XB->AR(i + 1);

@@ -166,7 +166,7 @@ class LocalFactors:
         f = _native.LocalFactors()
         f.lo, f.hi, f.kind, f.fused = self.lo, self.hi, _KIND_CODES[self.kind], int(self.mode == "siq")
         for k in ("s_a", "s_b", "fill_row", "fill_col", "b_fill_row", "b_fill_col", "elim_f", "elim_g", "elim_q",
-                  "elim_k", "elim_fr", "elim_qr", "elim_h"):
+                  "elim_k", "elim_fr", "elim_qr", "elim_h", "elim_ha", "elim_eq", "elim_ek"):
             t = self.tensors.get(k)
             setattr(f, k, t.data_ptr() if (t is not None and t.numel()) else None)
         return f
@@ -224,10 +224,16 @@ def _alloc_factors(kind, lo, hi, fused, bs, asz, dev) -> "LocalFactors":
     t["elim_f"] = torch.empty((length, bs, bs), **c128)
     t["elim_g"] = torch.empty((length, asz, bs), **c128)
     t["elim_h"] = torch.empty((length, bs, bs), **c128)
+    extra = os.environ.get("BSEL_FWD_BWD_PRODUCTS", "0") not in ("", "0")  # steps.cuh fwd_backward_products
+    if extra or not fused:
+        t["elim_ha"] = torch.empty((length, bs, asz), **c128)
     if fused:
         t["s_b"] = torch.empty((length, bs, bs), **c128)
         t["elim_q"] = torch.empty((length, bs, bs), **c128)
         t["elim_k"] = torch.empty((length, bs, asz), **c128)
+        if extra:
+            t["elim_eq"] = torch.empty((length, bs, bs), **c128)
+            t["elim_ek"] = torch.empty((length, bs, asz), **c128)
     if kind == "middle":
         t["fill_row"] = torch.empty((length, bs, bs), **c128)
         t["fill_col"] = torch.empty((length, bs, bs), **c128)
