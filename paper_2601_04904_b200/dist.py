@@ -428,8 +428,9 @@ class _Lanes:
         self.count = count
         self.streams = [torch.cuda.Stream(device) for _ in range(count)]
         # Concurrent chains share the SMs: each block inverse gets fewer CTAs
-        # (cfg4, 2 lanes: 28-36 CTAs -> 2000 ms vs 2035 ms at the default 64).
-        self.inverse_grid = int(os.environ.get("BSEL_LANE_INV_GRID", "32")) if count > 1 else 0
+        # (cfg4, 2 lanes, current sweeps: 32 / 36 / 40 / 44 / 48 / 64 CTAs ->
+        # 1070 / 1045 / 1019-1023 / 1028 / 1035 / 1060 ms per energy point).
+        self.inverse_grid = int(os.environ.get("BSEL_LANE_INV_GRID", "40")) if count > 1 else 0
 
     def run(self, fn) -> list:
         import threading
