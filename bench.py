@@ -288,13 +288,19 @@ def run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist):
             dist.barrier()
         torch.cuda.synchronize()
         start.record()
+        marks = []
         for _ in range(args.steps):
             step()
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append(ev)
         end.record()
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
     ms = start.elapsed_time(end) / args.steps
+    step_ms = [round(start.elapsed_time(marks[0]), 1)] + [round(marks[i - 1].elapsed_time(marks[i]), 1)
+                                                          for i in range(1, len(marks))]
     launches = (bs.kernel_launches() - launches0) // args.steps
     if dist:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -425,13 +431,19 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         start.record()
+        marks = []
         for _ in range(args.steps):
             step()
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append(ev)
         end.record()
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
     ms = start.elapsed_time(end) / args.steps
+    step_ms = [round(start.elapsed_time(marks[0]), 1)] + [round(marks[i - 1].elapsed_time(marks[i]), 1)
+                                                          for i in range(1, len(marks))]
     launches = (bs.kernel_launches() - launches0) // args.steps
     if dist:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -569,6 +581,7 @@ def main():
                          "gemm_launches_per_step": prof.gemm_launches},
             "phases_ms": phases,
             "rank_phases_ms": rank_phases,
+            "step_ms": step_ms,
             "partition_sizes": ([hi - lo for lo, hi in solver.plan.ranges] if world > 1 else None),
             "value_sequential_rgf_ms": seq_ms,
             "gpu_launches": launches,
