@@ -78,8 +78,8 @@ struct GemmBatch {
 
 // Tile configurations (complex tile BM x BN).
 // kTileAuto: 64x64 tiles once a launch has >= 2 waves of them; kTileAutoWide:
-// already from fewer tiles (backward sweeps: their launches overlap the
-// next level's on the same stream less, and 64x64 tiles run the pipe hotter).
+// the partition backward's threshold (BSEL_GEMM_MIN_TILES64_WIDE; since the
+// re-associated backward the same 2 waves, measured best).
 enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3 };
 
 // Launch one grouped batch on `stream`.  Problems with M==0 or N==0 are
