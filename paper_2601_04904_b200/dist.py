@@ -431,6 +431,8 @@ class _Lanes:
         # (cfg4, 2 lanes, current sweeps: 32 / 36 / 40 / 44 / 48 / 64 CTAs ->
         # 1070 / 1045 / 1019-1023 / 1028 / 1035 / 1060 ms per energy point).
         self.inverse_grid = int(os.environ.get("BSEL_LANE_INV_GRID", "40")) if count > 1 else 0
+        # SMs the lanes' forward aux levels leave to the chains (experiment; 0 = off)
+        self.avoid_sms = int(os.environ.get("BSEL_LANE_AVOID_SMS", "0"))
 
     def run(self, fn) -> list:
         import threading
@@ -446,10 +448,12 @@ class _Lanes:
                     self.streams[rank].wait_event(start)
                     ctx = _native.Context.get(self.device.index, lane=rank)
                     ctx.set_inverse_grid(self.inverse_grid)
+                    ctx.set_aux_avoid_sms(self.avoid_sms)
                     try:
                         fn(rank, ctx)
                     finally:
                         ctx.set_inverse_grid(0)
+                        ctx.set_aux_avoid_sms(0)
             except Exception as exc:  # noqa: BLE001 - rank attribution
                 errors.append((rank, exc))
 
