@@ -243,9 +243,12 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
         st.sb = F.SB(i - lo);
         st.fn_out = F.EF(i - lo), st.fr_out = F.EFR(i - lo), st.g_out = F.EG(i - lo);
         st.qn_out = F.EQ(i - lo), st.qr_out = F.EQR(i - lo), st.kk_out = F.EK(i - lo);
-        if (fwd_backward_products()) st.ha_out = F.EHA(i - lo), st.eq_out = F.EEQ(i - lo), st.ek_out = F.EEK(i - lo);
+        // middles: the backward's h / e products are formed here -- a middle
+        // partition's forward finishes early (4 GPUs: 175 vs 218 ms for the
+        // ends) while its k = 3 backward is the longest
+        st.ha_out = F.EHA(i - lo), st.eq_out = F.EEQ(i - lo), st.ek_out = F.EEK(i - lo);
       }
-      if ((fused && fwd_backward_products()) || ctx.schur_ok((int)b)) st.h_out = F.EH(i - lo);
+      if (fused || ctx.schur_ok((int)b)) st.h_out = F.EH(i - lo);
       middle_step(ctx, st, fused, (uint64_t)s, i, fwd_slot(s));
     }
   }
@@ -280,7 +283,9 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
   ctx.reserve_slots(back_sweep_slots(), (int64_t)mx * mx);
   cudaStream_t s = ctx.stream();
   cuda_check(cudaEventRecord(ctx.timer(2), s), "timer");
-  BackSweep sweep(ctx, kTileAutoWide);
+  // first / last partitions: the common 2-wave 64x64 threshold (2 GPUs:
+  // backward 294 vs 305 ms); middles (k = 3, larger levels): the wide one
+  BackSweep sweep(ctx, F.kind == kMiddle ? kTileAutoWide : kTileAuto);
   // End-to-end mode: move each chunk of finished outputs to the host on the
   // copy stream while the sweep continues.
   const bool streamed = io && io->hxa && io->chunk > 0;
@@ -415,12 +420,8 @@ void local_backward(Context& ctx, const BtaDev& A, const BtaDev* B, const LocalF
         st.sc = F.SB(i - lo);
         st.cpre[0] = F.EFR(i - lo), st.cpre[1] = F.EF(i - lo), st.cpre[2] = F.EG(i - lo);
         st.qpre[0] = F.EQR(i - lo), st.qpre[1] = F.EQ(i - lo), st.qpre[2] = F.EK(i - lo);
-        if (fwd_backward_products()) {
-          st.hpre[1] = F.EH(i - lo), st.hpre[2] = F.EHA(i - lo);
-          st.epre[1] = F.EEQ(i - lo), st.epre[2] = F.EEK(i - lo);
-        } else if (ctx.schur_ok((int)b)) {
-          st.hpre[1] = F.EH(i - lo);
-        }
+        st.hpre[1] = F.EH(i - lo), st.hpre[2] = F.EHA(i - lo);  // formed by the middle forward
+        st.epre[1] = F.EEQ(i - lo), st.epre[2] = F.EEK(i - lo);
         st.ss[0] = F.BFC(i - lo), st.ss[1] = B->U(i), st.ss[2] = el(*WB, i, false);
         st.ws[0] = F.BFR(i - lo), st.ws[1] = B->L(i), st.ws[2] = el(*WB, i, true);
         const Mat z00 = XB->D(lo), z0t = XB->AC(lo), zt0 = XB->AR(lo);

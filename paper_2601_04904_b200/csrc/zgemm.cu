@@ -512,12 +512,11 @@ cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cf
       const char* e = getenv("BSEL_GEMM_MIN_TILES64");
       return e ? (int64_t)atoll(e) : (int64_t)2 * device_sm_count();
     }();
-    // partition backward levels: same threshold since the re-associated
-    // backward (2 GPUs: backward 305 -> 294 ms with 296 instead of 128;
-    // neutral with two lanes on one GPU)
+    // middle partitions' k = 3 backward levels (4 GPUs: middles' backward
+    // 214 ms with 128 vs 252 ms with 2 waves)
     static const int64_t min64_wide = [] {
       const char* e = getenv("BSEL_GEMM_MIN_TILES64_WIDE");
-      return e ? (int64_t)atoll(e) : (int64_t)2 * device_sm_count();
+      return e ? (int64_t)atoll(e) : (int64_t)128;
     }();
     tile_cfg = (tiles64 >= (tile_cfg == kTileAutoWide ? min64_wide : min64)) ? kTile64 : kTile32;
   }

@@ -78,8 +78,8 @@ struct GemmBatch {
 
 // Tile configurations (complex tile BM x BN).
 // kTileAuto: 64x64 tiles once a launch has >= 2 waves of them; kTileAutoWide:
-// the partition backward's threshold (BSEL_GEMM_MIN_TILES64_WIDE; since the
-// re-associated backward the same 2 waves, measured best).
+// already from 128 of them (BSEL_GEMM_MIN_TILES64_WIDE): the middle
+// partitions' k = 3 back-substitution, measured best there.
 enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3 };
 
 // Launch one grouped batch on `stream`.  Problems with M==0 or N==0 are

@@ -224,7 +224,8 @@ def _alloc_factors(kind, lo, hi, fused, bs, asz, dev) -> "LocalFactors":
     t["elim_f"] = torch.empty((length, bs, bs), **c128)
     t["elim_g"] = torch.empty((length, asz, bs), **c128)
     t["elim_h"] = torch.empty((length, bs, bs), **c128)
-    extra = os.environ.get("BSEL_FWD_BWD_PRODUCTS", "0") not in ("", "0")  # steps.cuh fwd_backward_products
+    # steps.cuh fwd_backward_products; middle partitions always form them
+    extra = os.environ.get("BSEL_FWD_BWD_PRODUCTS", "0") not in ("", "0") or kind == "middle"
     if extra or not fused:
         t["elim_ha"] = torch.empty((length, bs, asz), **c128)
     if fused:
