@@ -458,12 +458,33 @@ struct Quad {
   int64_t ld[4];
 };
 
+// As leaf_publish, with the diagonal tile already in shared memory.
+__device__ void leaf_publish_smem(Leaf32& L, const double2 (*src)[kTLD], int jb, double2* gDp, int* flag) {
+  for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+    const int i = e >> 5, j = e & 31;
+    L.a[i][j] = (i < jb && j < jb) ? src[i][j] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const bool zero = gj_leaf32(L, jb);
+  if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
+  const double2 (*Sx)[33] = L.a;
+  for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+    const int r = e >> 5, k = e & 31;
+    if (r < jb && k < jb)
+      gDp[r * kT + L.piv[k]] = Sx[L.piv[r]][k];
+    else
+      gDp[r * kT + k] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+}
+
 struct TileCtx {
   int b, ntq, nt, p, j0, jb;
   const Quad* Wc;  // current (in the __grid_constant__ kernel parameters)
   const Quad* Wn;  // next
   bool final_;      // this panel writes the caller's outputs
   bool skip_c;      // final: leave quadrant 3 untouched (fallback recomputes it)
+  bool keep;        // lookahead tile: also leave the result in S.r for the leaf
   int r_tk;  // column tile whose R = Dinv W[J,K] is cached in S.r
   unsigned long long* trace;  // debug (may be null)
   __device__ int quad(int ti, int tk) const { return 2 * (ti / ntq) + (tk / ntq); }
@@ -546,6 +567,12 @@ __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int
     return;
   }
   tile_mma(acc, S.c[buf], tk == p ? S.d : S.r);
+  if (T.keep) {  // the next leaf reads this tile from shared memory, not back through L2
+    __syncthreads();  // every warp is done reading S.r
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn)
+      S.r[orow][acc_col(jn)] = make_double2(is.w[jn].x - acc[jn][0], is.w[jn].y - acc[jn][1]);
+  }
   if (skip) return;
 #pragma unroll
   for (int jn = 0; jn < 4; ++jn) {
@@ -648,6 +675,7 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
   target += G;
   grid_barrier(g.barrier, target);
   TileCtx T;
+  T.keep = false;
   T.trace = g.trace;
   T.b = b;
   T.ntq = ntq;
@@ -669,11 +697,13 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
     const int sp = (p + 1 < ntq) ? (p + 1) * nt + (p + 1) : -1;
     if (blockIdx.x == 0) stamp(8 * p + 0);
     if (blockIdx.x == 0 && sp >= 0) {
+      T.keep = true;
       gj_tiles(S, T, sp, sp + 1, -1);
+      T.keep = false;
+      T.r_tk = -1;  // S.r now holds the tile, not an R
       __syncthreads();
       stamp(8 * p + 1);
-      leaf_publish(L, T.at(T.Wn, p + 1, p + 1), T.ld(T.Wn, p + 1, p + 1), 0, min(kT, b - (p + 1) * kT),
-                   g.gD + ((p + 1) & 1) * kT * kT, g.flag);
+      leaf_publish_smem(L, S.r, min(kT, b - (p + 1) * kT), g.gD + ((p + 1) & 1) * kT * kT, g.flag);
       stamp(8 * p + 2);
     }
     if (G == 1 || blockIdx.x > 0) {
