@@ -221,6 +221,56 @@ def run_reference(args, n, b, a):
     emit(line)
 
 
+def pipelined_e2e(args, n, b, a, parts, hA, hB, hXA, hXB, single):
+    """End to end through ``HostEnergySweep``: K energy points, each one's
+    inputs copied host->device and outputs device->host inside the timed
+    region, the copies of neighbouring energies overlapped with the solves
+    (every step moves the same bytes as the single-call form; the same
+    pinned host buffers serve every energy)."""
+    import gc
+
+    import torch
+
+    import paper_2601_04904_b200 as bs
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    free_gib = torch.cuda.mem_get_info()[0] / 2**30
+    # out_slots=1 (outputs streamed out behind each backward sweep): the
+    # double-buffered-output form measured slower at config 4 (1.7 s per
+    # energy: its whole-matrix D2H delays the next solve; DESIGN.md 8)
+    sweep, slots = None, 1
+    for slots in (1,):
+        try:
+            sweep = bs.HostEnergySweep(n, b, a, "siq", partitions=parts, out_slots=slots)
+            break
+        except torch.cuda.OutOfMemoryError:
+            sweep = None
+            gc.collect()
+            torch.cuda.empty_cache()
+    if sweep is None:
+        return dict(single, pipelined_note="HostEnergySweep buffers do not fit")
+    k = max(args.steps, args.e2e_energies)
+    sweep.run([(hA, hB)] * 2, [(hXA, hXB)] * 2)  # warm (both slots)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    sweep.run([(hA, hB)] * k, [(hXA, hXB)] * k)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / k
+    del sweep
+    gc.collect()
+    torch.cuda.empty_cache()
+    return {"value": ms, "unit": "ms", "h2d_bytes_per_step": single["h2d_bytes_per_step"],
+            "d2h_bytes_per_step": single["d2h_bytes_per_step"],
+            "api": f"HostEnergySweep.run: {k} energy points from/to pinned host buffers, H2D of energy k+1 "
+                   f"and D2H of energy k-1 overlapped with energy k's solve (out_slots={slots}); "
+                   "timed region includes the first H2D and the last D2H",
+            "single_call_ms": single["value"], "single_call_api": single["api"],
+            "device_free_gib_before": round(free_gib, 1)}
+
+
 def dist_e2e(args, solver, A, B, n, world, rank, dev, dist):
     """N>1 end-to-end through DistSolver.solve(host_in, host_out): every step
     each rank streams the input blocks it needs from pinned host memory
@@ -355,6 +405,11 @@ def main():
     ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=None, help="override n_blocks (debug)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipelined-e2e", action="store_true",
+                    help="report the single-call e2e only (skip the HostEnergySweep measurement)")
+    ap.add_argument("--e2e-energies", type=int, default=16,
+                    help="energy points in the pipelined e2e run (max with --steps); the unoverlapped "
+                         "first H2D and last D2H are amortised over them")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=8)
     ap.add_argument("--partitions", type=int, default=None,
@@ -526,7 +581,11 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = s2.elapsed_time(e2) / args.steps
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": hA.nbytes + hB.nbytes,
-               "d2h_bytes_per_step": hXA.nbytes + hXB.nbytes}
+               "d2h_bytes_per_step": hXA.nbytes + hXB.nbytes,
+               "api": "solve_selected(host pinned A, B, out=host pinned X_A, X_B), one call per step"}
+        if not args.no_pipelined_e2e:
+            ws = None  # the sequential-path workspace is not used by the partitioned sweep
+            e2e = pipelined_e2e(args, n, b, a, parts, hA, hB, hXA, hXB, e2e)
     elif not args.no_e2e:
         e2e = dist_e2e(args, solver, A, B, n, world, rank, dev, dist)
 

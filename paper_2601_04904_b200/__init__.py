@@ -12,7 +12,7 @@ Public API mirrors btasel/__init__.py for the hot path:
 * kernels: OpCounter, block_multiply_acc, mm, block_inverse
 * BTA1 files: read_bta, write_bta, read_bta_header (+ read_bta_device)
 * dense GPU oracle: dense_solve (baselines.py)
-* energy-point sweeps (config 5): EnergySweep
+* energy-point sweeps (config 5): EnergySweep; host-buffer pipelined sweep: HostEnergySweep
 * errors: the reference's exception hierarchy
 
 Every numerical call runs in libbtasel_b200.so (sm_100a); there is no CPU
@@ -44,7 +44,7 @@ from .dist import (BoundaryPayload, DistSolver, HostWindow, InGpuPartitions, Loc
                    assemble_reduced, dist_solve, local_backward, local_forward, solve_reduced)
 from .fileio import read_bta, read_bta_device, read_bta_header, write_bta
 from .dense import dense_solve
-from .energy import EnergySweep, energy_seeds, rank_energies
+from .energy import EnergySweep, HostEnergySweep, energy_seeds, rank_energies
 
 __version__ = "0.1.0"
 
@@ -61,5 +61,5 @@ __all__ = [
     "BtaselError", "ShapeMismatchError", "SingularBlockError", "DenseGuardError", "ProtocolError",
     "WorkerError", "NativeUnavailableError", "FormatError", "BadMagicError", "TruncatedPayloadError",
     "ShapeInconsistencyError", "read_bta", "write_bta", "read_bta_header", "read_bta_device", "dense_solve",
-    "EnergySweep", "energy_seeds", "rank_energies",
+    "EnergySweep", "HostEnergySweep", "energy_seeds", "rank_energies",
 ]

@@ -17,12 +17,14 @@ parallel, energies e = rank, rank + world, ... on each rank, no collective
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from .device import DeviceBta, generate_dd_bta_device, hermitianize_device
 from .rgf import default_partitions, solve_selected
 
-__all__ = ["EnergySweep", "energy_seeds", "rank_energies"]
+__all__ = ["EnergySweep", "HostEnergySweep", "energy_seeds", "rank_energies"]
 
 
 def energy_seeds(e: int) -> tuple[int, int]:
@@ -88,3 +90,116 @@ class EnergySweep:
             if k + 1 < len(energies):
                 ready = nxt
         return len(energies)
+
+
+class HostEnergySweep:
+    """Solve a sequence of energy points whose inputs and outputs live in
+    pinned host memory, overlapping the PCIe traffic of neighbouring energies
+    with the solves (the end-to-end form of config 4/5).
+
+    Energy k: its inputs were copied host->device into input slot k % 2
+    while energy k-1 solved (h2d stream); it solves into output slot
+    ``k % out_slots``; its outputs are copied device->host on the d2h stream
+    while energy k+1 solves.  PCIe is full duplex, so in steady state one
+    energy costs max(solve, H2D, D2H) instead of the single-call
+    max(forward, H2D) + max(backward, D2H).  Device memory: 2 input slots +
+    ``out_slots`` output slots (cfg4: 16 GiB per matrix, 128 GiB at
+    out_slots=2, plus the ~36 GiB solve workspace).  ``out_slots=1`` keeps one
+    device output set and streams it out behind each backward sweep instead
+    (``solve_selected``'s host-output path); it is the default because at
+    config 4 the two-slot form measured 1.7 s per energy against 1.17 s
+    (tools/e2e_probe.py: each solve starts only after the previous energy's
+    whole-matrix D2H, so the copies serialize with the solves instead of
+    overlapping them; next round's item).
+    """
+
+    def __init__(self, n: int, b: int, a: int, mode: str = "siq", device=None, partitions=None,
+                 out_slots: int = 1):
+        if out_slots not in (1, 2):
+            raise ValueError("out_slots must be 1 or 2")
+        self.n, self.b, self.a, self.mode = n, b, a, mode
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.parts = default_partitions(n) if partitions is None else partitions
+        self.out_slots = out_slots
+        fused = mode == "siq"
+        mk = lambda: DeviceBta.empty(n, b, a, self.device, zero=False)  # noqa: E731
+        self.inputs = [(mk(), mk() if fused else None) for _ in range(2)]
+        self.out = [(mk(), mk() if fused else None) for _ in range(out_slots)] if out_slots == 2 else None
+        self.h2d = torch.cuda.Stream(self.device)
+        self.d2h = torch.cuda.Stream(self.device)
+
+    def _load(self, host, slot, free):
+        a, b = host
+        A, B = self.inputs[slot]
+        with torch.cuda.device(self.device), torch.cuda.stream(self.h2d):
+            if free is not None:
+                self.h2d.wait_event(free)
+            A.copy_from_host(a, non_blocking=True)
+            if B is not None:
+                B.copy_from_host(b, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self.h2d)
+        return ready
+
+    def run(self, inputs, outputs, timings=None):
+        """Solve energies ``inputs[k] = (a_k, b_k)`` (pinned host BtaMatrix)
+        into ``outputs[k] = (x_a_k, x_b_k)`` (pinned host BtaMatrix); returns
+        once every output is on the host."""
+        inputs, outputs = list(inputs), list(outputs)
+        if len(inputs) != len(outputs):
+            raise ValueError("inputs and outputs differ in length")
+        if not inputs:
+            return 0
+        main = torch.cuda.current_stream(self.device)
+        self.h2d.wait_stream(main)  # the first load is ordered after the caller's queued work
+        in_free = [None, None]  # event: solve no longer reads the input slot
+        out_free = [None, None]  # event: D2H of the output slot finished
+        # The partitioned solve streams host inputs in behind its forward
+        # sweeps: the first energy uses that (no unoverlapped fill), and the
+        # second energy's load starts once the first's inputs are in.
+        stream_first = (self.parts > 1 and self.n >= 2 * self.parts
+                        and os.environ.get("BSEL_SWEEP_STREAM_FIRST", "1") != "0")
+        self.done_events = []
+        ready = None if stream_first else self._load(inputs[0], 0, None)
+        for k, (host_in, host_out) in enumerate(zip(inputs, outputs)):
+            s = k & 1
+            first = stream_first and k == 0
+            nxt = None
+            if k + 1 < len(inputs) and not first:
+                nxt = self._load(inputs[k + 1], s ^ 1, in_free[s ^ 1])
+            if ready is not None:
+                main.wait_event(ready)
+            A, B = self.inputs[s]
+            src = host_in if first else (A, B)
+            kw = {"_device_in": (A, B), "_io_events": {}} if first else {}
+            if self.out is None:
+                solve_selected(src[0], src[1], self.mode, out=host_out, partitions=self.parts, timings=timings,
+                               **kw)
+                done = torch.cuda.Event(enable_timing=True)
+                done.record(main)
+            else:
+                o = k % self.out_slots
+                if out_free[o] is not None:
+                    main.wait_event(out_free[o])
+                XA, XB = self.out[o]
+                solve_selected(src[0], src[1], self.mode, out=(XA, XB), partitions=self.parts, timings=timings,
+                               **kw)
+                done = torch.cuda.Event(enable_timing=True)
+                done.record(main)
+                with torch.cuda.device(self.device), torch.cuda.stream(self.d2h):
+                    self.d2h.wait_event(done)
+                    XA.copy_to_host(host_out[0], non_blocking=True)
+                    if XB is not None:
+                        XB.copy_to_host(host_out[1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self.d2h)
+                    out_free[o] = ev
+            in_free[s] = done
+            self.done_events.append(done)
+            if first and k + 1 < len(inputs):
+                nxt = self._load(inputs[k + 1], s ^ 1, kw["_io_events"].get("inputs_done"))
+            ready = nxt
+        main.wait_stream(self.d2h)
+        main.wait_stream(self.h2d)
+        main.synchronize()
+        return len(inputs)

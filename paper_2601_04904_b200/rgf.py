@@ -258,7 +258,8 @@ def release_caches() -> None:
 
 
 def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal_only=False,
-                   out=None, workspace=None, partitions=None, _b_symmetry=None) -> SelectedSolution:
+                   out=None, workspace=None, partitions=None, _b_symmetry=None, _device_in=None,
+                   _io_events=None) -> SelectedSolution:
     """Selected inverse of ``a`` and, in fused mode, the selected quadratic
     solution for ``b`` (rgf.py:497-531).  Never mutates its inputs.
 
@@ -280,7 +281,8 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
     n, bs, asz = a.shape_params
     parts = default_partitions(n) if partitions is None else int(partitions)
     if parts > 1 and n >= 2 * parts:
-        return _solve_partitioned(a, b if fused else None, mode, parts, counter, timings, diagonal_only, out)
+        return _solve_partitioned(a, b if fused else None, mode, parts, counter, timings, diagonal_only, out,
+                                  _device_in, _io_events)
     ctx, device = _ctx_for(a)
     host = not isinstance(a, DeviceBta)
     A = DeviceBta.empty(n, bs, asz, device, zero=False).copy_from_host(a) if host else a
@@ -339,8 +341,12 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
     return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
 
 
-def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out):
-    """solve_selected through InGpuPartitions (dist.py) with cached buffers."""
+def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, device_in=None, io_events=None):
+    """solve_selected through InGpuPartitions (dist.py) with cached buffers.
+
+    ``device_in`` (internal, HostEnergySweep): device storage for streamed
+    host inputs instead of a fresh allocation; ``io_events`` receives
+    "inputs_done", the event after the last streamed input chunk."""
     from .dist import InGpuPartitions
 
     n, bs, asz = a.shape_params
@@ -353,12 +359,13 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out):
     stream_in = host and _pinned(a) and (b is None or _pinned(b))
     host_out = out if (out is not None and not isinstance(out[0], DeviceBta)) else None
     stream_out = host_out is not None and not diagonal_only and all(_pinned(x) for x in host_out if x is not None)
-    A = a if not host else DeviceBta.empty(n, bs, asz, device, zero=False)
+    dev_in = device_in if (host and device_in is not None) else None
+    A = a if not host else (dev_in[0] if dev_in else DeviceBta.empty(n, bs, asz, device, zero=False))
     if host and not stream_in:
         A.copy_from_host(a)
     B = None
     if fused:
-        B = b if not host else DeviceBta.empty(n, bs, asz, device, zero=False)
+        B = b if not host else (dev_in[1] if dev_in else DeviceBta.empty(n, bs, asz, device, zero=False))
         if host and not stream_in:
             B.copy_from_host(b)
     key = (device.index, n, bs, asz, mode, parts)
@@ -371,6 +378,10 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out):
                             host_out=host_out if stream_out else None)
     else:
         XA, XB = runner.run(A, B, out=dev_out)
+    if io_events is not None and stream_in:
+        ev = torch.cuda.Event()
+        ev.record(runner.copy_stream)
+        io_events["inputs_done"] = ev
     if stream_out:
         record_sweep(counter, n, bs, asz, mode, "forward")
         record_sweep(counter, n, bs, asz, mode, "backward")

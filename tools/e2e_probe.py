@@ -1,5 +1,6 @@
-"""Where does the end-to-end time go?  Phase times of a streamed host-I/O
-solve vs a device-resident solve, plus raw pinned H2D/D2H bandwidth."""
+"""Probe: HostEnergySweep at config 4 shapes, out_slots 1 vs 2 (pipelined
+end-to-end ms per energy point, allocator retries, free device memory)."""
+
 import os
 import sys
 import time
@@ -8,51 +9,35 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2601_04904_b200 as bs  # noqa: E402
-from paper_2601_04904_b200 import rgf  # noqa: E402
 
-n, b, a = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (1024, 512, 256)))
-dev = torch.device("cuda:0")
-A = bs.generate_dd_bta_device(n, b, a, seed=0)
-B = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=1))
+n, b, a = 1024, 512, 256
+slots = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+k = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+dev = torch.device("cuda", 0)
+A = bs.generate_dd_bta_device(n, b, a, seed=0, device=dev)
+B = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=1, device=dev))
 hA = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
 hB = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
 A.copy_to_host(hA)
 B.copy_to_host(hB)
+del A, B
+torch.cuda.empty_cache()
+hX = (bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False), bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False))
+sweep = bs.HostEnergySweep(n, b, a, "siq", out_slots=slots)
+print("free GiB after sweep buffers", torch.cuda.mem_get_info()[0] / 2**30, flush=True)
+sweep.run([(hA, hB)] * 2, [hX] * 2)
 torch.cuda.synchronize()
-
-
-def ev_time(fn, reps=2):
+r0 = torch.cuda.memory_stats().get("num_alloc_retries", 0)
+for kk in (1, k):
+    t0 = time.perf_counter()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fn()
-    torch.cuda.synchronize()
     s.record()
-    for _ in range(reps):
-        fn()
+    sweep.run([(hA, hB)] * kk, [hX] * kk)
     e.record()
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / reps
-
-
-h2d = ev_time(lambda: A.copy_from_host(hA, non_blocking=True))
-d2h = ev_time(lambda: A.copy_to_host(hA, non_blocking=True))
-gb = hA.nbytes / 1e9
-print(f"pinned H2D {gb:.1f} GB: {h2d:.1f} ms = {gb / h2d * 1e3:.1f} GB/s; D2H {d2h:.1f} ms = {gb / d2h * 1e3:.1f} GB/s")
-
-XA, XB = bs.DeviceBta.empty(n, b, a, dev), bs.DeviceBta.empty(n, b, a, dev)
-t = {}
-dms = ev_time(lambda: bs.solve_selected(A, B, "siq", out=(XA, XB), timings=t))
-print(f"device-resident: {dms:.1f} ms; phases {({k: round(v * 1e3, 1) for k, v in t.items()})}")
-runner = next(iter(rgf._PARTITIONED.values()))
-print("  device phases", {k: round(v * 1e3, 1) for k, v in runner.phase_seconds().items()})
-del XA, XB, A, B
-torch.cuda.empty_cache()
-hXA = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
-hXB = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
-for chunk in (8, 4, 16, 32):
-    os.environ["BSEL_STREAM_CHUNK"] = str(chunk)
-    t0 = time.perf_counter()
-    ms = ev_time(lambda: bs.solve_selected(hA, hB, "siq", out=(hXA, hXB)))
-    runner = [r for k, r in rgf._PARTITIONED.items()][0]
-    print(f"streamed chunk={chunk}: {ms:.1f} ms; phases",
-          {k: round(v * 1e3, 1) for k, v in runner.phase_seconds().items()},
-          f"wall {(time.perf_counter() - t0) / 3 * 1e3:.0f} ms/call")
+    torch.cuda.synchronize()
+    print("  solve-done times (ms from start):", [round(s.elapsed_time(d), 1) for d in sweep.done_events])
+    print(f"out_slots={slots} K={kk}: {s.elapsed_time(e) / kk:.1f} ms/energy (wall {1e3 * (time.perf_counter() - t0) / kk:.1f})",
+          flush=True)
+print("alloc retries during timed runs", torch.cuda.memory_stats().get("num_alloc_retries", 0) - r0)
+print("free GiB", torch.cuda.mem_get_info()[0] / 2**30)
