@@ -240,7 +240,7 @@ def pipelined_e2e(args, n, b, a, parts, hA, hB, hXA, hXB, single):
     # double-buffered-output form measured slower at config 4 (1.7 s per
     # energy: its whole-matrix D2H delays the next solve)
     sweep, slots = None, 1
-    for slots in (1,):
+    for slots in ((int(os.environ["BSEL_E2E_OUT_SLOTS"]),) if os.environ.get("BSEL_E2E_OUT_SLOTS") else (1,)):
         try:
             sweep = bs.HostEnergySweep(n, b, a, "siq", partitions=parts, out_slots=slots)
             break

@@ -128,15 +128,31 @@ class HostEnergySweep:
         self.h2d = torch.cuda.Stream(self.device)
         self.d2h = torch.cuda.Stream(self.device)
 
+    @staticmethod
+    def _chunked(host_m, dev_m, to_host):
+        """Whole-matrix copy as ~32 MiB pieces: a multi-GiB copy holds its
+        copy engine for hundreds of ms, and the solve's own small copies
+        queued behind it would stall the sweeps."""
+        for k, arr in host_m.stacked().items():
+            if not arr.size:
+                continue
+            h, d = torch.from_numpy(arr), getattr(dev_m, k)
+            step = max(1, (32 << 20) // max(1, arr[0].nbytes)) if arr.ndim == 3 else len(arr)
+            for i in range(0, len(arr), step):
+                if to_host:
+                    h[i:i + step].copy_(d[i:i + step], non_blocking=True)
+                else:
+                    d[i:i + step].copy_(h[i:i + step], non_blocking=True)
+
     def _load(self, host, slot, free):
         a, b = host
         A, B = self.inputs[slot]
         with torch.cuda.device(self.device), torch.cuda.stream(self.h2d):
             if free is not None:
                 self.h2d.wait_event(free)
-            A.copy_from_host(a, non_blocking=True)
+            self._chunked(a, A, False)
             if B is not None:
-                B.copy_from_host(b, non_blocking=True)
+                self._chunked(b, B, False)
             ready = torch.cuda.Event()
             ready.record(self.h2d)
         return ready
@@ -157,7 +173,7 @@ class HostEnergySweep:
         # The partitioned solve streams host inputs in behind its forward
         # sweeps: the first energy uses that (no unoverlapped fill), and the
         # second energy's load starts once the first's inputs are in.
-        stream_first = (self.parts > 1 and self.n >= 2 * self.parts
+        stream_first = (self.parts > 1 and self.n >= 2 * self.parts and self.out is None
                         and os.environ.get("BSEL_SWEEP_STREAM_FIRST", "1") != "0")
         self.done_events = []
         ready = None if stream_first else self._load(inputs[0], 0, None)
@@ -188,9 +204,9 @@ class HostEnergySweep:
                 done.record(main)
                 with torch.cuda.device(self.device), torch.cuda.stream(self.d2h):
                     self.d2h.wait_event(done)
-                    XA.copy_to_host(host_out[0], non_blocking=True)
+                    self._chunked(host_out[0], XA, True)
                     if XB is not None:
-                        XB.copy_to_host(host_out[1], non_blocking=True)
+                        self._chunked(host_out[1], XB, True)
                     ev = torch.cuda.Event()
                     ev.record(self.d2h)
                     out_free[o] = ev
