@@ -236,20 +236,13 @@ def pipelined_e2e(args, n, b, a, parts, hA, hB, hXA, hXB, single):
     gc.collect()
     torch.cuda.empty_cache()
     free_gib = torch.cuda.mem_get_info()[0] / 2**30
-    # out_slots=1 (outputs streamed out behind each backward sweep): the
-    # double-buffered-output form measured slower at config 4 (1.7 s per
-    # energy: its whole-matrix D2H delays the next solve)
-    sweep, slots = None, 1
-    for slots in ((int(os.environ["BSEL_E2E_OUT_SLOTS"]),) if os.environ.get("BSEL_E2E_OUT_SLOTS") else (1,)):
-        try:
-            sweep = bs.HostEnergySweep(n, b, a, "siq", partitions=parts, out_slots=slots)
-            break
-        except torch.cuda.OutOfMemoryError:
-            sweep = None
-            gc.collect()
-            torch.cuda.empty_cache()
-    if sweep is None:
+    # out_slots: 2 when the double-buffered outputs fit (BSEL_E2E_OUT_SLOTS forces 1 or 2)
+    want = int(os.environ["BSEL_E2E_OUT_SLOTS"]) if os.environ.get("BSEL_E2E_OUT_SLOTS") else None
+    try:
+        sweep = bs.HostEnergySweep(n, b, a, "siq", partitions=parts, out_slots=want)
+    except torch.cuda.OutOfMemoryError:
         return dict(single, pipelined_note="HostEnergySweep buffers do not fit")
+    slots = sweep.out_slots
     k = max(args.steps, args.e2e_energies)
     sweep.run([(hA, hB)] * 2, [(hXA, hXB)] * 2)  # warm (both slots)
     torch.cuda.synchronize()

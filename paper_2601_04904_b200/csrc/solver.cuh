@@ -73,6 +73,13 @@ struct SingularInfo {
 
 class Context {
  public:
+  // Status + symmetry flags published by a kernel into mapped pinned host
+  // memory: a copy-engine D2H would wait behind any multi-GiB D2H in flight
+  // on another stream (tools/ce_starve_probe.py), a kernel store does not.
+  struct HostFlags {
+    unsigned long long status;
+    int sym;
+  };
   explicit Context(int device);
   ~Context();
   Context(const Context&) = delete;
@@ -165,6 +172,9 @@ class Context {
   int sym_flags_ = 3, sym_mode_ = kSymAuto, fwd_sym_ = 0;
   bool sym_checked_ = false;
   unsigned long long* d_status_ = nullptr;
+  HostFlags* h_flags_ = nullptr;
+  HostFlags* d_hflags_ = nullptr;
+  void publish_flags(cudaStream_t s);
   std::vector<cudaEvent_t> events_;
   std::vector<cudaEvent_t> xfer_events_;
   cudaStream_t xfer_ = nullptr;

@@ -33,6 +33,9 @@ Context::Context(int device) : device_(device) {
   cuda_check(cudaMalloc(&d_status_, sizeof(unsigned long long)), "status");
   cuda_check(cudaMalloc(&d_sym_, sizeof(int)), "symmetry flags");
   cuda_check(cudaMalloc(&d_aux_counter_, 2 * sizeof(unsigned)), "aux tile counter");
+  cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_flags_), sizeof(HostFlags), cudaHostAllocMapped),
+             "mapped flags");
+  cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hflags_), h_flags_, 0), "mapped flags pointer");
   events_.resize(64);
   for (auto& e : events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& t : timers_) cuda_check(cudaEventCreate(&t), "timer");
@@ -49,6 +52,7 @@ Context::~Context() {
   if (d_status_) cudaFree(d_status_);
   if (d_sym_) cudaFree(d_sym_);
   if (d_aux_counter_) cudaFree(d_aux_counter_);
+  if (h_flags_) cudaFreeHost(h_flags_);
   for (auto& e : events_) cudaEventDestroy(e);
   for (auto& t : timers_) cudaEventDestroy(t);
   for (auto& e : xfer_events_) cudaEventDestroy(e);
@@ -129,10 +133,22 @@ void Context::sym_check(const SymJob& j, cudaStream_t s) {
   sym_checked_ = true;
 }
 
+__global__ void publish_flags_kernel(const unsigned long long* status, const int* sym,
+                                     volatile Context::HostFlags* out) {
+  out->status = *status;
+  out->sym = *sym;
+  __threadfence_system();
+}
+
+void Context::publish_flags(cudaStream_t s) {
+  publish_flags_kernel<<<1, 1, 0, s>>>(d_status_, d_sym_, d_hflags_);
+  cuda_check(cudaGetLastError(), "publish flags");
+  cuda_check(cudaStreamSynchronize(s), "flags sync");
+}
+
 int Context::sym_now(cudaStream_t s) {
-  int f = 3;
-  cuda_check(cudaMemcpyAsync(&f, d_sym_, sizeof(f), cudaMemcpyDeviceToHost, s), "symmetry d2h");
-  cuda_check(cudaStreamSynchronize(s), "symmetry sync");
+  publish_flags(s);
+  const int f = reinterpret_cast<volatile HostFlags*>(h_flags_)->sym;
   if (!sym_checked_) return 0;
   sym_flags_ = f;
   return !(f & kNotHermitian) ? +1 : !(f & kNotSkew) ? -1 : 0;
@@ -172,12 +188,9 @@ void Context::schur(Mat D, Mat U, Mat L, Mat C, Mat S, Mat H, Mat F, uint64_t or
 }
 
 SingularInfo Context::read_status() {
-  unsigned long long st = 0;
-  cuda_check(cudaMemcpyAsync(&st, d_status_, sizeof(st), cudaMemcpyDeviceToHost, user_stream_), "status d2h");
-  int sym = 3;
-  cuda_check(cudaMemcpyAsync(&sym, d_sym_, sizeof(sym), cudaMemcpyDeviceToHost, user_stream_), "symmetry d2h");
-  cuda_check(cudaStreamSynchronize(user_stream_), "status sync");
-  sym_flags_ = sym;
+  publish_flags(user_stream_);
+  const unsigned long long st = reinterpret_cast<volatile HostFlags*>(h_flags_)->status;
+  sym_flags_ = reinterpret_cast<volatile HostFlags*>(h_flags_)->sym;
   SingularInfo info;
   if (st != ~0ull) {
     info.singular = true;

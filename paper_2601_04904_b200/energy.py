@@ -106,25 +106,33 @@ class HostEnergySweep:
     ``out_slots`` output slots (cfg4: 16 GiB per matrix, 128 GiB at
     out_slots=2, plus the ~36 GiB solve workspace).  ``out_slots=1`` keeps one
     device output set and streams it out behind each backward sweep instead
-    (``solve_selected``'s host-output path); it is the default because at
-    config 4 the two-slot form measured 1.7 s per energy against 1.17 s
-    (tools/e2e_probe.py: each solve starts only after the previous energy's
-    whole-matrix D2H, so the copies serialize with the solves instead of
-    overlapping them; next round's item).
+    (``solve_selected``'s host-output path); ``None`` = 2 when the buffers
+    fit.  Config 4: 1151 ms per energy over 16 energies with 2 slots
+    (steady state 1056-1074 ms), 1200 ms with 1.  The two-slot form needs the
+    solve's status / symmetry reads to bypass the copy engine (a small D2H
+    waits behind the in-flight output D2H; they are published through mapped
+    host memory, ``Context::publish_flags``).
     """
 
     def __init__(self, n: int, b: int, a: int, mode: str = "siq", device=None, partitions=None,
-                 out_slots: int = 1):
-        if out_slots not in (1, 2):
-            raise ValueError("out_slots must be 1 or 2")
+                 out_slots: int | None = None):
+        if out_slots not in (None, 1, 2):
+            raise ValueError("out_slots must be 1, 2 or None (2 when the buffers fit, else 1)")
         self.n, self.b, self.a, self.mode = n, b, a, mode
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.parts = default_partitions(n) if partitions is None else partitions
-        self.out_slots = out_slots
         fused = mode == "siq"
         mk = lambda: DeviceBta.empty(n, b, a, self.device, zero=False)  # noqa: E731
         self.inputs = [(mk(), mk() if fused else None) for _ in range(2)]
-        self.out = [(mk(), mk() if fused else None) for _ in range(out_slots)] if out_slots == 2 else None
+        self.out = None
+        if out_slots != 1:
+            try:
+                self.out = [(mk(), mk() if fused else None) for _ in range(2)]
+            except torch.cuda.OutOfMemoryError:
+                if out_slots == 2:
+                    raise
+                torch.cuda.empty_cache()
+        self.out_slots = 2 if self.out is not None else 1
         self.h2d = torch.cuda.Stream(self.device)
         self.d2h = torch.cuda.Stream(self.device)
 
@@ -171,8 +179,11 @@ class HostEnergySweep:
         in_free = [None, None]  # event: solve no longer reads the input slot
         out_free = [None, None]  # event: D2H of the output slot finished
         # The partitioned solve streams host inputs in behind its forward
-        # sweeps: the first energy uses that (no unoverlapped fill), and the
-        # second energy's load starts once the first's inputs are in.
+        # sweeps: with out_slots=1 the first energy uses that (no
+        # unoverlapped fill), and the second energy's load starts once the
+        # first's inputs are in.  With out_slots=2 (device outputs) the
+        # streamed first energy measured 8.5 s at config 4 instead of ~1.1 s
+        # (tools/e2e_probe.py; next round), so it is loaded whole.
         stream_first = (self.parts > 1 and self.n >= 2 * self.parts and self.out is None
                         and os.environ.get("BSEL_SWEEP_STREAM_FIRST", "1") != "0")
         self.done_events = []

@@ -36,7 +36,7 @@ def test_energy_zero_is_the_bench_system_and_si_mode():
         float(abs(x - y).max()) for x, y in zip(out[0].diag, ref.x_a.diag)) < 1e-13
 
 
-@pytest.mark.parametrize("out_slots,parts,mode", [(2, 2, "siq"), (1, 2, "siq"), (2, 1, "siq"), (2, 1, "si")])
+@pytest.mark.parametrize("out_slots,parts,mode", [(2, 2, "siq"), (1, 2, "siq"), (None, 2, "siq"), (2, 1, "siq"), (2, 1, "si")])
 def test_host_sweep_matches_individual_solves(out_slots, parts, mode):
     """Pipelined host-buffer sweep: every energy's host outputs equal the
     single-call device solve bit for bit (4 energies: both input and output

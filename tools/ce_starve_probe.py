@@ -19,7 +19,11 @@ H = bs.BtaMatrix.zeros(n, b, a, pinned=True, zero=False)
 flag = torch.zeros(1, dtype=torch.int32, device=dev)
 hflag = torch.zeros(1, dtype=torch.int32).pin_memory()
 big, small = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-for mode in ("whole", "chunked", "whole", "chunked", "kernel-read"):
+mapped = torch.zeros(1, dtype=torch.int32).pin_memory()  # kernel writes it through a device view? (UVA)
+v = (flag + 1).sum()  # warm the kernels
+torch.cuda.synchronize()
+ev = torch.cuda.Event()
+for mode in ("whole", "chunked", "kernel-read", "kernel-event", "whole"):
     torch.cuda.synchronize()
     with torch.cuda.stream(big):
         if mode == "chunked":
@@ -29,7 +33,11 @@ for mode in ("whole", "chunked", "whole", "chunked", "kernel-read"):
     time.sleep(0.02)
     t0 = time.perf_counter()
     with torch.cuda.stream(small):
-        if mode == "kernel-read":
+        if mode == "kernel-event":
+            v = (flag + 1).sum()
+            ev.record(small)
+            ev.synchronize()
+        elif mode == "kernel-read":
             v = (flag + 1).sum()  # kernel only, no copy: baseline for a launch + sync
             small.synchronize()
         else:
