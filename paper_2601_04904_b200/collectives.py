@@ -16,19 +16,25 @@ Transports:
   moved with a single ``all_gather_into_tensor``.  ``all_reduce_sum`` is an
   ``all_gather`` of the (tiny, 2*a*a) tip contributions followed by a
   rank-ordered local sum: same bytes on the wire as an allreduce tree at this
-  size, and bitwise-identical, order-fixed results on every rank.
+  size, and bitwise-identical, order-fixed results on every rank.  It also
+  takes the reference's own numpy payloads (``to_bytes``/``from_bytes``,
+  dist.py:73-131) and numpy tip arrays, so the reference's ``dist.py``
+  orchestration (``_run_rank``) runs over NCCL unchanged.
 * :class:`LocalHub` -- all partitions in one process on one GPU (the
   ``transport=None`` default of ``dist_solve``); rounds are recorded, data
   never leaves the device.
 
 Both record a trace of rounds (``TraceEvent``) for communication-contract
-checks (reference tests/test_dist.py:87-133).
+checks (reference tests/test_dist.py:87-133).  ``dist_solve`` also accepts
+any other Collectives -- the reference's ``ThreadHub`` (collectives.py:87-133)
+or ``SocketCollectives`` -- and then exchanges host payloads by value.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from .errors import ProtocolError
@@ -50,6 +56,8 @@ def _summary(obj):
         return obj.summary()
     if isinstance(obj, torch.Tensor):
         return {"nbytes": obj.numel() * obj.element_size(), "elements": obj.numel()}
+    if isinstance(obj, np.ndarray):
+        return {"nbytes": obj.nbytes, "elements": obj.size}
     return {"nbytes": None}
 
 
@@ -94,20 +102,62 @@ class TorchCollectives(Collectives):
             self._dist.all_gather(list(out.unbind(0)), flat.contiguous(), group=self.group)
         return out
 
+    def _device(self):
+        """Where the wire tensors live: CUDA for NCCL, host memory otherwise."""
+        if self._dist.get_backend(self.group) == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
+
+    def _gather_bytes(self, blob: bytes) -> list:
+        """all_gather of variable-length byte strings: the lengths first,
+        then every blob padded to the longest (two NCCL all_gathers)."""
+        dev = self._device()
+        sizes = self.gather_tensor(torch.tensor([len(blob)], dtype=torch.int64, device=dev)).view(-1).tolist()
+        buf = torch.zeros(max(sizes), dtype=torch.uint8)
+        if blob:
+            buf[:len(blob)] = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+        allb = self.gather_tensor(buf.to(dev)).cpu().numpy()
+        return [allb[r, :sizes[r]].tobytes() for r in range(self.world_size)]
+
     def all_gather(self, payload) -> list:
-        """Payloads exposing pack()/unpack() travel as one fixed-size slot per
-        rank; anything else must be a tensor of identical shape on all ranks."""
-        if hasattr(payload, "pack"):
+        """* device payloads exposing pack()/unpack() (this package's
+          BoundaryPayload) travel as one fixed-size slot per rank, all ranks'
+          headers read back with ONE device->host copy;
+        * payloads exposing to_bytes()/from_bytes() -- the reference's numpy
+          BoundaryPayload (dist.py:73-131), or a host payload of this package
+          -- travel as bytes, so the reference's own dist.py orchestration
+          runs over NCCL;
+        * tensors / numpy arrays of identical shape on all ranks."""
+        on_dev = getattr(payload, "on_device", None)
+        if hasattr(payload, "pack") and (on_dev is None or on_dev()):
             flat = payload.pack()
             allp = self.gather_tensor(flat)
-            out = [payload.unpack(allp[r], rank=r) for r in range(self.world_size)]
+            hdrs = allp[:, :4].cpu().tolist()
+            out = [payload.unpack(allp[r], rank=r, header=hdrs[r]) for r in range(self.world_size)]
+        elif hasattr(payload, "to_bytes"):
+            blobs = self._gather_bytes(payload.to_bytes())
+            out = [type(payload).from_bytes(bl) for bl in blobs]
+        elif isinstance(payload, np.ndarray):
+            allp = self.gather_tensor(torch.from_numpy(np.ascontiguousarray(payload)).to(self._device()))
+            out = [allp[r].cpu().numpy() for r in range(self.world_size)]
         else:
             allp = self.gather_tensor(payload)
             out = [allp[r] for r in range(self.world_size)]
         self._record("all_gather", [_summary(p) for p in out])
         return out
 
-    def all_reduce_sum(self, array: torch.Tensor) -> torch.Tensor:
+    def gather_to_root(self, blob: bytes):
+        """Rank 0 receives every rank's bytes (rank order); others get None
+        (the reference's SocketCollectives.gather_to_root contract)."""
+        blobs = self._gather_bytes(blob)
+        return blobs if self.rank == 0 else None
+
+    def all_reduce_sum(self, array):
+        """Elementwise sum in FIXED rank order (bitwise replicated).  numpy
+        arrays in -> numpy out (the reference's contract), tensors -> tensors."""
+        if isinstance(array, np.ndarray):
+            t = torch.from_numpy(np.ascontiguousarray(array)).to(self._device())
+            return self.all_reduce_sum(t).cpu().numpy()
         allp = self.gather_tensor(torch.view_as_real(array) if array.is_complex() else array)
         if array.is_complex():
             allp = torch.view_as_complex(allp)

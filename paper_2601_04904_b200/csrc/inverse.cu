@@ -742,7 +742,7 @@ int inverse_grid_cap() {
 }
 
 int coop_grid_limit() {
-  static const int limit = [] {
+  return per_device([] {
     int dev = 0, coop = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
@@ -752,8 +752,7 @@ int coop_grid_limit() {
                                                       sizeof(PinvSmem)) != cudaSuccess)
       per_sm = 0;
     return coop ? per_sm * device_sm_count() : 0;
-  }();
-  return limit;
+  });
 }
 }  // namespace
 
@@ -892,13 +891,13 @@ cudaError_t launch_gj(GjArgs& g, int grid, cudaStream_t stream) {
   }();
   // BSEL_INV_SMEM (bytes, experiment): request more shared memory per CTA
   // than the kernel uses, so that no GEMM CTA can share an SM with it.
-  static const size_t smem = [] {
+  const size_t smem = per_device([] {
     const char* e = getenv("BSEL_INV_SMEM");
     size_t v = e ? (size_t)atoll(e) : 0;
     if (v < sizeof(PinvSmem)) v = sizeof(PinvSmem);
     if (v != sizeof(PinvSmem)) cudaFuncSetAttribute(persistent_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v);
     return v;
-  }();
+  });
   cudaError_t err;
   if (coop) {
     void* args[] = {(void*)&g};
@@ -912,11 +911,13 @@ cudaError_t launch_gj(GjArgs& g, int grid, cudaStream_t stream) {
 }
 
 cudaError_t launch_exact_fallback_attr() {
-  static const cudaError_t a1 =  // thread-safe one-time init, sized for n <= 2048
-      cudaFuncSetAttribute(exact_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  static const cudaError_t a2 =
-      cudaFuncSetAttribute(exact_schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  return a1 != cudaSuccess ? a1 : a2;
+  return per_device([] {  // thread-safe one-time init per device, sized for n <= 2048
+    const cudaError_t a1 =
+        cudaFuncSetAttribute(exact_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const cudaError_t a2 =
+        cudaFuncSetAttribute(exact_schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return a1 != cudaSuccess ? a1 : a2;
+  });
 }
 }  // namespace
 

@@ -14,8 +14,16 @@ constexpr int kT = 32, kRows = 8;
 __global__ void __launch_bounds__(kT * kRows) sym_check_kernel(SymJob j, int* flags) {
   const int tj = blockIdx.x, ti = blockIdx.y;
   if (j.same && ti > tj) return;
-  if (!j.dX && *reinterpret_cast<volatile int*>(flags) == (kNotHermitian | kNotSkew)) return;
   __shared__ double2 sx[kT][kT + 1], sy[kT][kT + 1];
+  __shared__ int s_done;
+  if (!j.dX) {
+    // one read of the flags word decides the early exit for the whole block
+    // (other blocks may be OR-ing it concurrently)
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      s_done = *reinterpret_cast<volatile int*>(flags) == (kNotHermitian | kNotSkew);
+    __syncthreads();
+    if (s_done) return;
+  }
   const int64_t blk = blockIdx.z;
   const double2* X = j.X + blk * j.sx;
   const double2* Y = j.Y + blk * j.sy;

@@ -320,9 +320,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 
 template <class C>
 cudaError_t launch_cfg(GemmBatch& batch, cudaStream_t stream) {
-  // thread-safe one-time init (partitions may launch from several threads)
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(zgemm_grouped_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  // thread-safe one-time init per device (partitions may launch from several threads)
+  const cudaError_t attr = per_device([] {
+    return cudaFuncSetAttribute(zgemm_grouped_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  });
   if (attr != cudaSuccess) return attr;
   int tiles = 0;
   for (int i = 0; i < batch.nproblems; ++i) {
@@ -479,13 +480,12 @@ void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxe
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int device_sm_count() {
-  static const int sms = [] {
+  return per_device([] {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
-  }();
-  return sms;
+  });
 }
 
 cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cfg) {

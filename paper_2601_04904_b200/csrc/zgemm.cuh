@@ -20,9 +20,32 @@
 // complex k.  No flops are wasted (8 real flops per complex MAC).
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace bsel {
+
+// Value computed once PER DEVICE (f() runs with that device current): kernel
+// attributes such as the dynamic shared-memory opt-in and occupancy-derived
+// limits are per device, and one process may drive several GPUs.  Each call
+// site (lambda type) gets its own cache.
+constexpr int kMaxDevices = 64;
+template <class F>
+auto per_device(F&& f) -> decltype(f()) {
+  using T = decltype(f());
+  static std::mutex mu;
+  static bool done[kMaxDevices] = {};
+  static T val[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return f();
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done[dev]) {
+    val[dev] = f();
+    done[dev] = true;
+  }
+  return val[dev];
+}
 
 enum : uint8_t { kOpN = 0, kOpC = 1 };
 

@@ -18,8 +18,11 @@ from __future__ import annotations
 
 import ctypes
 import os
+import struct
+import threading
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _native
@@ -32,11 +35,36 @@ from .partition import PartitionPlan, plan_partitions
 from .rgf import solve_selected
 
 __all__ = ["BoundaryPayload", "LocalFactors", "ReducedSystem", "local_forward", "assemble_reduced",
-           "solve_reduced", "local_backward", "dist_solve", "DistSolver", "InGpuPartitions", "record_partition"]
+           "solve_reduced", "local_backward", "dist_solve", "DistSolver", "InGpuPartitions", "record_partition",
+           "owned_slices", "merge_slices"]
 
 _KIND_CODES = {"first": 0, "middle": 1, "last": 2}
 _KIND_NAMES = {v: k for k, v in _KIND_CODES.items()}
 _FIELDS = ("diag", "coupling", "arrow_row", "arrow_col", "b_diag", "b_coupling", "b_arrow_row", "b_arrow_col")
+
+
+def _np(t):
+    """Host numpy copy of a device/host tensor or array."""
+    if isinstance(t, torch.Tensor):
+        return t.detach().cpu().numpy()
+    return np.asarray(t)
+
+
+def _nbytes(t) -> int:
+    return t.numel() * t.element_size() if isinstance(t, torch.Tensor) else int(np.asarray(t).nbytes)
+
+
+def _dev_tensor(x, dev):
+    """Device tensor of a numpy array or tensor (no copy when already there)."""
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(dev)
+
+
+def _native_transport(coll) -> bool:
+    """Transports of this package move device tensors; any other
+    Collectives (the reference's ThreadHub endpoints / SocketCollectives, a
+    user's transport) gets host payloads, by value, like the reference."""
+    return isinstance(coll, TorchCollectives)
 
 # Logical per-step product inventory of the partition sweeps (dist.py:211-397,
 # 595-742), checked against the reference OpCounter in tests.
@@ -103,7 +131,60 @@ class BoundaryPayload:
     sym_flags: int = 3
 
     def nbytes(self) -> int:
-        return sum(t.numel() * t.element_size() for f in _FIELDS for t in getattr(self, f))
+        return sum(_nbytes(t) for f in _FIELDS for t in getattr(self, f))
+
+    def on_device(self) -> bool:
+        """True when the blocks are torch tensors (device slot path); False
+        for a host (numpy) payload."""
+        return bool(self.diag) and isinstance(self.diag[0], torch.Tensor)
+
+    def to_host(self) -> "BoundaryPayload":
+        """The same payload with numpy blocks (message passing by value over
+        a foreign transport, dist.py:73-131 semantics)."""
+        p = BoundaryPayload(rank=self.rank, kind=self.kind, b=self.b, a=self.a, fused=self.fused,
+                            sym_flags=self.sym_flags)
+        for f in _FIELDS:
+            setattr(p, f, [_np(t) for t in getattr(self, f)])
+        return p
+
+    def to_bytes(self) -> bytes:
+        """Wire form for byte transports (the reference SocketCollectives,
+        TorchCollectives' byte path): little-endian u32 rank, u8 kind code;
+        per field a u32 block count, then per block u64 rows, u64 cols and
+        the row-major complex128 data; a trailing i32 carries sym_flags."""
+        out = [struct.pack("<IB", self.rank, _KIND_CODES[self.kind])]
+        for f in _FIELDS:
+            blocks = [_np(t) for t in getattr(self, f)]
+            out.append(struct.pack("<I", len(blocks)))
+            for blk in blocks:
+                out.append(struct.pack("<QQ", *blk.shape))
+                out.append(np.ascontiguousarray(blk, dtype="<c16").tobytes())
+        out.append(struct.pack("<i", int(self.sym_flags)))
+        return b"".join(out)
+
+    @classmethod
+    def from_bytes(cls, buf: bytes) -> "BoundaryPayload":
+        rank, code = struct.unpack_from("<IB", buf, 0)
+        if code not in _KIND_NAMES:
+            raise ProtocolError(f"payload carries unknown kind code {code}")
+        off = 5
+        fields = {}
+        for f in _FIELDS:
+            (count,) = struct.unpack_from("<I", buf, off)
+            off += 4
+            blocks = []
+            for _ in range(count):
+                r, c = struct.unpack_from("<QQ", buf, off)
+                off += 16
+                blocks.append(np.frombuffer(buf, dtype="<c16", count=r * c, offset=off).reshape(r, c).copy())
+                off += 16 * r * c
+            fields[f] = blocks
+        (sym,) = struct.unpack_from("<i", buf, off) if len(buf) >= off + 4 else (3,)
+        d = fields["diag"]
+        b = d[0].shape[0] if d else 0
+        a = fields["arrow_row"][0].shape[0] if fields["arrow_row"] else 0
+        return cls(rank=rank, kind=_KIND_NAMES[code], b=b, a=a, fused=bool(fields["b_diag"]), sym_flags=sym,
+                   **fields)
 
     def summary(self) -> dict:
         blocks = {f: [tuple(t.shape) for t in getattr(self, f)] for f in _FIELDS if getattr(self, f)}
@@ -131,8 +212,11 @@ class BoundaryPayload:
             off += 2 * r * c * (2 - len(getattr(self, name)))
         return out
 
-    def unpack(self, flat: torch.Tensor, rank: int) -> "BoundaryPayload":
-        hdr = flat[:4].tolist()
+    def unpack(self, flat: torch.Tensor, rank: int, header=None) -> "BoundaryPayload":
+        """``header``: the slot's first 4 values already on the host
+        (TorchCollectives reads all ranks' headers with ONE device->host
+        copy); read from ``flat`` otherwise."""
+        hdr = flat[:4].tolist() if header is None else list(header)
         kind = _KIND_NAMES.get(int(hdr[1]))
         if kind is None or int(hdr[0]) != rank:
             raise ProtocolError(f"payload {rank} carries rank {int(hdr[0])} kind code {int(hdr[1])}")
@@ -162,6 +246,18 @@ class LocalFactors:
     work_a: object = None
     work_b: object = None
 
+    def eliminated(self) -> range:
+        """Global indices of the blocks this partition eliminated."""
+        lo, hi = self.lo, self.hi
+        return {"first": range(lo, hi - 1), "last": range(lo + 1, hi), "middle": range(lo + 1, hi - 1)}[self.kind]
+
+    @property
+    def s_a(self) -> dict:
+        """{global block index: inverted pivot} like the reference's
+        LocalFactors.s_a (dist.py:134-151); device tensors (views)."""
+        t = self.tensors.get("s_a")
+        return {g: t[g - self.lo] for g in self.eliminated()} if t is not None else {}
+
     def desc(self) -> _native.LocalFactors:
         f = _native.LocalFactors()
         f.lo, f.hi, f.kind, f.fused = self.lo, self.hi, _KIND_CODES[self.kind], int(self.mode == "siq")
@@ -183,6 +279,12 @@ class ReducedSystem:
     # backward path for the quadratic solve decided from every rank's check of
     # B: +1 / -1 when B = +-B^H exactly, 0 otherwise (Context.set_b_symmetry)
     b_symmetry: int = 0
+
+    def to_host(self) -> "ReducedSystem":
+        """Host BtaMatrix form (the reference's ReducedSystem types)."""
+        host = lambda m: m if (m is None or not isinstance(m, DeviceBta)) else to_host(m)  # noqa: E731
+        return ReducedSystem(matrix_a=host(self.matrix_a), matrix_b=host(self.matrix_b), provenance=self.provenance,
+                             index=self.index, b_symmetry=self.b_symmetry)
 
 
 class _Strips:
@@ -286,11 +388,16 @@ def local_forward(a, b, plan: PartitionPlan, rank: int, counter: OpCounter | Non
         if kind == "middle":
             pay.b_coupling = [fac.tensors["b_fill_row"][length - 1], fac.tensors["b_fill_col"][length - 1]]
     tip_delta = torch.stack([WA.tip, WB.tip]) if fused else WA.tip.unsqueeze(0)
+    if not isinstance(a, DeviceBta):
+        # host inputs -> host payload / tip delta (reference types); the
+        # factors stay on the device for local_backward
+        return pay.to_host(), _np(tip_delta), fac
     return pay, tip_delta, fac
 
 
-def _assemble(gathered, a, b, plan: PartitionPlan, tip_sum) -> ReducedSystem:
-    """Reduced system from all payloads (dist.py:440-504)."""
+def _assemble(gathered, a, b, plan: PartitionPlan, tip_sum, dev=None) -> ReducedSystem:
+    """Reduced system from all payloads (dist.py:440-504), on device ``dev``
+    (payload blocks may be device tensors or host arrays)."""
     fused = b is not None
     if len(gathered) != plan.num_parts:
         raise ProtocolError(f"expected {plan.num_parts} payloads, got {len(gathered)}")
@@ -331,24 +438,28 @@ def _assemble(gathered, a, b, plan: PartitionPlan, tip_sum) -> ReducedSystem:
                 bup.append(b.upper[g])
                 blw.append(b.lower[g])
     asz, bs = a.a, a.b
-    dev = d[0].device
+    if dev is None:
+        dev = d[0].device if isinstance(d[0], torch.Tensor) else torch.device("cuda", torch.cuda.current_device())
 
     def stack(lst, shape):
         if lst:
-            return torch.stack([x.to(dev) for x in lst]).contiguous()
+            return torch.stack([_dev_tensor(x, dev) for x in lst]).contiguous()
         return torch.empty((0,) + shape, dtype=torch.complex128, device=dev)
 
     flags = 0
     for pay in gathered:
         flags |= int(pay.sym_flags)
     sym = 0 if not fused else (1 if not flags & 1 else -1 if not flags & 2 else 0)
-    tip = (a.tip.to(dev) + tip_sum[0]) if asz else torch.empty((0, 0), dtype=torch.complex128, device=dev)
+    if tip_sum is not None:
+        tip_sum = _dev_tensor(tip_sum, dev)
+    tip = (_dev_tensor(a.tip, dev) + tip_sum[0]) if asz else torch.empty((0, 0), dtype=torch.complex128, device=dev)
     ra = DeviceBta(nr, bs, asz, {"diag": stack(d, (bs, bs)), "lower": stack(lw, (bs, bs)),
                                  "upper": stack(up, (bs, bs)), "arrow_row": stack(r, (asz, bs)),
                                  "arrow_col": stack(c, (bs, asz)), "tip": tip.contiguous()})
     rb = None
     if fused:
-        btip = (b.tip.to(dev) + tip_sum[1]) if asz else torch.empty((0, 0), dtype=torch.complex128, device=dev)
+        btip = (_dev_tensor(b.tip, dev) + tip_sum[1]) if asz else torch.empty((0, 0), dtype=torch.complex128,
+                                                                             device=dev)
         rb = DeviceBta(nr, bs, asz, {"diag": stack(bd, (bs, bs)), "lower": stack(blw, (bs, bs)),
                                      "upper": stack(bup, (bs, bs)), "arrow_row": stack(br, (asz, bs)),
                                      "arrow_col": stack(bc, (bs, asz)), "tip": btip.contiguous()})
@@ -359,10 +470,23 @@ def _assemble(gathered, a, b, plan: PartitionPlan, tip_sum) -> ReducedSystem:
 def assemble_reduced(coll: Collectives, a, b, plan: PartitionPlan, payload: BoundaryPayload,
                      tip_delta) -> ReducedSystem:
     """Exchange boundary data and build the replicated reduced system
-    (dist.py:419-504): one all_gather, plus one all_reduce when a > 0."""
-    gathered = coll.all_gather(payload)
-    tip_sum = coll.all_reduce_sum(tip_delta) if a.a > 0 else None
-    return _assemble(gathered, a, b, plan, tip_sum)
+    (dist.py:419-504): one all_gather, plus one all_reduce when a > 0.
+
+    ``coll``: a TorchCollectives endpoint (device payload slots over NCCL)
+    or any other Collectives (the reference's ThreadHub endpoints /
+    SocketCollectives): those receive host payloads and a numpy tip delta,
+    by value, as in the reference.  Host inputs give a host ReducedSystem.
+    """
+    if _native_transport(coll):
+        gathered = coll.all_gather(payload)
+        tip_sum = coll.all_reduce_sum(tip_delta) if a.a > 0 else None
+    else:
+        host_pay = payload.to_host() if isinstance(payload, BoundaryPayload) and payload.on_device() else payload
+        gathered = coll.all_gather(host_pay)
+        tip_sum = coll.all_reduce_sum(_np(tip_delta)) if a.a > 0 else None
+    dev = a.device if isinstance(a, DeviceBta) else torch.device("cuda", torch.cuda.current_device())
+    reduced = _assemble(gathered, a, b, plan, tip_sum, dev)
+    return reduced if isinstance(a, DeviceBta) else reduced.to_host()
 
 
 def solve_reduced(reduced: ReducedSystem, mode: str, counter=None, recursive_parts=None):
@@ -379,12 +503,17 @@ def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, 
     (dist.py:542-744).  Writes this rank's pattern blocks (and, on rank 0,
     the tip) into ``out`` = (x_a, x_b) full-size DeviceBta (allocated zeroed
     if None) and returns it."""
+    host = not isinstance(a, DeviceBta)
     A = _as_device(a)
     B = _as_device(b, A.device) if b is not None else None
     lo, hi = plan.ranges[rank]
     fused = factors.mode == "siq"
     if fused and B is None:
         raise ProtocolError("fused factors require the right-hand side")
+    if not isinstance(red_sol.x_a, DeviceBta):  # host reduced solution (reference types)
+        red_sol = SelectedSolution(x_a=to_device(red_sol.x_a, A.device),
+                                   x_b=to_device(red_sol.x_b, A.device) if red_sol.x_b is not None else None,
+                                   mode=red_sol.mode)
     if red_sol.x_a.shape_params != reduced.matrix_a.shape_params:
         raise ProtocolError("reduced solution shape disagrees with reduced system")
     n, bs, asz = A.shape_params
@@ -410,7 +539,90 @@ def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, 
     finally:
         ctx.set_b_symmetry(ctx.SYM_AUTO)
     record_partition(counter, kind, hi - lo, bs, asz, factors.mode, "backward")
+    if host:
+        return owned_slices(out, plan, rank)
     return out
+
+
+def owned_slices(out, plan: PartitionPlan, rank: int) -> dict:
+    """Host slice of the blocks partition ``rank`` owns, in the reference's
+    local_backward return form (dist.py:551-560): ``{"x_a": {kind: {g: blk}},
+    "x_b": ... | None}`` -- its diagonal blocks and arrow strips, its interior
+    off-diagonals and (except the last rank) its separator, and on rank 0
+    the tip."""
+    lo, hi = plan.ranges[rank]
+    last = rank == plan.num_parts - 1
+    offd = range(lo, hi - 1 if last else hi)
+
+    def one(X):
+        if X is None:
+            return None
+        h = {k: _np(getattr(X, k)[lo:hi]) for k in ("diag", "arrow_row", "arrow_col")}
+        o = {k: _np(getattr(X, k)[offd.start:offd.stop]) for k in ("lower", "upper")}
+        sl = {k: {g: h[k][g - lo] for g in range(lo, hi)} for k in h}
+        sl.update({k: {g: o[k][g - offd.start] for g in offd} for k in o})
+        sl["tip"] = _np(X.tip) if rank == 0 else None
+        return sl
+
+    return {"x_a": one(out[0]), "x_b": one(out[1])}
+
+
+def merge_slices(n, b, a, mode, slices) -> SelectedSolution:
+    """Host solution from every rank's owned slices (dist.py:752-780)."""
+    fused = mode == "siq"
+    xs = {"x_a": BtaMatrix.zeros(n, b, a), "x_b": BtaMatrix.zeros(n, b, a) if fused else None}
+    seen = set()
+    for sl in slices:
+        seen.update(sl["x_a"]["diag"].keys())
+        for side, m in xs.items():
+            if m is None:
+                continue
+            part = sl[side]
+            for kind in ("diag", "lower", "upper", "arrow_row", "arrow_col"):
+                for g, blk in part[kind].items():
+                    getattr(m, kind)[g][...] = blk
+            if part["tip"] is not None:
+                m.tip[...] = part["tip"]
+    if seen != set(range(n)):
+        raise ProtocolError(f"incomplete solution coverage: missing {sorted(set(range(n)) - seen)}")
+    return SelectedSolution(x_a=xs["x_a"], x_b=xs["x_b"], mode=mode)
+
+
+def _slices_to_bytes(sl: dict) -> bytes:
+    import io
+
+    arrays = {}
+    for side in ("x_a", "x_b"):
+        part = sl[side]
+        if part is None:
+            continue
+        for kind, blocks in part.items():
+            if kind == "tip":
+                if blocks is not None:
+                    arrays[f"{side}/tip/0"] = blocks
+                continue
+            for g, blk in blocks.items():
+                arrays[f"{side}/{kind}/{g}"] = blk
+    buf = io.BytesIO()
+    np.savez(buf, **arrays)
+    return buf.getvalue()
+
+
+def _slices_from_bytes(blob: bytes, fused: bool) -> dict:
+    import io
+
+    z = np.load(io.BytesIO(blob))
+    sl = {"x_a": None, "x_b": None}
+    for side in ("x_a", "x_b") if fused else ("x_a",):
+        sl[side] = {k: {} for k in ("diag", "lower", "upper", "arrow_row", "arrow_col")}
+        sl[side]["tip"] = None
+    for key in z.files:
+        side, kind, g = key.split("/")
+        if kind == "tip":
+            sl[side]["tip"] = z[key]
+        else:
+            sl[side][kind][int(g)] = z[key]
+    return sl
 
 
 # ---------------------------------------------------------------------------
@@ -729,6 +941,13 @@ def dist_solve(a, b=None, num_parts=2, mode=None, transport=None, *, counter=Non
             return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if XB is not None else None, mode=mode)
         return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
 
+    if transport is not None and not isinstance(transport, LocalHub):
+        if transport.world_size != num_parts:
+            raise ProtocolError(f"transport world size {transport.world_size} != num_parts {num_parts}")
+        if hasattr(transport, "endpoint"):
+            return _solve_over_hub(a, b, plan, transport, mode, counter, timings, rank_counters, recursive_parts)
+        return _solve_as_rank(a, b, plan, transport, mode, counter, timings, recursive_parts)
+
     hub = transport if transport is not None else LocalHub(num_parts)
     if hub.world_size != num_parts:
         raise ProtocolError(f"transport world size {hub.world_size} != num_parts {num_parts}")
@@ -749,6 +968,108 @@ def dist_solve(a, b=None, num_parts=2, mode=None, transport=None, *, counter=Non
     if host:
         return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if XB is not None else None, mode=mode)
     return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
+
+
+_REDUCED_LOCK = threading.Lock()
+
+
+def _solve_over_hub(a, b, plan, hub, mode, counter, timings, rank_counters, recursive_parts):
+    """dist_solve over a foreign in-process hub (``hub.endpoint(rank)``, e.g.
+    the reference's ThreadHub, collectives.py:87-133): every rank is a lane
+    on this GPU running the reference's per-rank pipeline (dist.py:787-801)
+    -- local forward, exchange through its endpoint (host payloads by
+    value), redundant reduced solve, local backward -- so the hub records
+    exactly the reference's rounds."""
+    num_parts = plan.num_parts
+    host = not isinstance(a, DeviceBta)
+    dev = a.device if not host else torch.device("cuda", torch.cuda.current_device())
+    A = _as_device(a, dev)
+    B = _as_device(b, dev) if b is not None else None
+    out = (DeviceBta.empty(A.n, A.b, A.a, dev), DeviceBta.empty(A.n, A.b, A.a, dev) if B is not None else None)
+    cnts = [OpCounter(b=A.b, a=A.a) for _ in range(num_parts)]
+    red_cnt = OpCounter(b=A.b, a=A.a)
+    timers = [None] * num_parts
+
+    def work(rank, ctx):
+        try:
+            tm = timers[rank] = _PhaseTimer(("forward", "communication", "reduced", "backward"))
+            tm.start("forward")
+            pay, delta, fac = local_forward(A, B, plan, rank, cnts[rank], _ctx=ctx)
+            tm.stop("forward")
+            tm.start("communication")
+            reduced = assemble_reduced(hub.endpoint(rank), A, B, plan, pay, delta)
+            tm.stop("communication")
+            tm.start("reduced")
+            with _REDUCED_LOCK:  # the reduced solves share the device's default context
+                red_sol = solve_reduced(reduced, mode, red_cnt if rank == 0 else None, recursive_parts)
+                torch.cuda.current_stream().synchronize()
+            tm.stop("reduced")
+            tm.start("backward")
+            local_backward(A, B, plan, rank, fac, reduced, red_sol, cnts[rank], out=out, _ctx=ctx)
+            tm.stop("backward")
+        except BaseException:
+            abort = getattr(hub, "abort", None)
+            if abort is not None:
+                abort()  # release peers blocked inside a collective round
+            raise
+
+    errors = _Lanes(dev, num_parts).run(work)
+    if errors:
+        primary = [e for e in errors if not isinstance(e[1], ProtocolError)]
+        rank, exc = min(primary or errors, key=lambda e: e[0])
+        raise WorkerError(rank, exc) from exc
+    if counter is not None:
+        for c in cnts:
+            counter.merge(c)
+        counter.merge(red_cnt)
+    if rank_counters is not None:
+        rank_counters.extend(cnts)
+    if timings is not None:
+        timings.update(timers[0].seconds())
+    XA, XB = out
+    if host:
+        return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if XB is not None else None, mode=mode)
+    return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
+
+
+def _solve_as_rank(a, b, plan, coll, mode, counter, timings, recursive_parts):
+    """dist_solve as ONE rank of a multi-process job over a foreign
+    Collectives endpoint (e.g. the reference's SocketCollectives,
+    collectives.py:187-331): this rank's partition on this process's GPU,
+    host payloads on the wire; with ``gather_to_root`` rank 0 returns the
+    merged host solution and the others None (dist.py:839-855), else every
+    rank returns its sharded device solution."""
+    rank = coll.rank
+    dev = torch.device("cuda", torch.cuda.current_device())
+    A = _as_device(a, dev)
+    B = _as_device(b, dev) if b is not None else None
+    cnt, red_cnt = OpCounter(b=A.b, a=A.a), OpCounter(b=A.b, a=A.a)
+    tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
+    tm.start("forward")
+    pay, delta, fac = local_forward(A, B, plan, rank, cnt)
+    tm.stop("forward")
+    tm.start("communication")
+    reduced = assemble_reduced(coll, A, B, plan, pay, delta)
+    tm.stop("communication")
+    tm.start("reduced")
+    red_sol = solve_reduced(reduced, mode, red_cnt, recursive_parts)
+    tm.stop("reduced")
+    tm.start("backward")
+    out = local_backward(A, B, plan, rank, fac, reduced, red_sol, cnt)
+    tm.stop("backward")
+    if timings is not None:
+        timings.update(tm.seconds())
+    if counter is not None:
+        counter.merge(cnt)
+        if rank == 0:
+            counter.merge(red_cnt)
+    if not hasattr(coll, "gather_to_root"):
+        return SelectedSolution(x_a=out[0], x_b=out[1], mode=mode)
+    blobs = coll.gather_to_root(_slices_to_bytes(owned_slices(out, plan, rank)))
+    if rank != 0 or blobs is None:
+        return None
+    fused = B is not None
+    return merge_slices(A.n, A.b, A.a, mode, [_slices_from_bytes(bl, fused) for bl in blobs])
 
 
 # SMs the forward's throughput GEMM levels leave to a single lane's chain

@@ -133,6 +133,7 @@ class HostEnergySweep:
                     raise
                 torch.cuda.empty_cache()
         self.out_slots = 2 if self.out is not None else 1
+        self._auto_slots = out_slots is None
         self.h2d = torch.cuda.Stream(self.device)
         self.d2h = torch.cuda.Stream(self.device)
 
@@ -188,17 +189,30 @@ class HostEnergySweep:
                         and os.environ.get("BSEL_SWEEP_STREAM_FIRST", "1") != "0")
         self.done_events = []
         ready = None if stream_first else self._load(inputs[0], 0, None)
-        for k, (host_in, host_out) in enumerate(zip(inputs, outputs)):
+        k = 0
+        preloaded = None  # next energy's load already enqueued (OOM retry)
+        while k < len(inputs):
+            host_in, host_out = inputs[k], outputs[k]
             s = k & 1
             first = stream_first and k == 0
             nxt = None
             if k + 1 < len(inputs) and not first:
-                nxt = self._load(inputs[k + 1], s ^ 1, in_free[s ^ 1])
+                nxt = preloaded if preloaded is not None else self._load(inputs[k + 1], s ^ 1, in_free[s ^ 1])
+            preloaded = None
             if ready is not None:
                 main.wait_event(ready)
             A, B = self.inputs[s]
             src = host_in if first else (A, B)
-            kw = {"_device_in": (A, B), "_io_events": {}} if first else {}
+            kw = {}
+            if first:
+                # the host-output solve synchronizes before it returns: the
+                # next energy's load is enqueued from the callback, right after
+                # this energy's last streamed input chunk (not after its solve)
+                held = []
+                io = {}
+                if k + 1 < len(inputs):
+                    io["on_inputs_done"] = lambda ev: held.append(self._load(inputs[k + 1], s ^ 1, ev))
+                kw = {"_device_in": (A, B), "_io_events": io}
             if self.out is None:
                 solve_selected(src[0], src[1], self.mode, out=host_out, partitions=self.parts, timings=timings,
                                **kw)
@@ -209,8 +223,22 @@ class HostEnergySweep:
                 if out_free[o] is not None:
                     main.wait_event(out_free[o])
                 XA, XB = self.out[o]
-                solve_selected(src[0], src[1], self.mode, out=(XA, XB), partitions=self.parts, timings=timings,
-                               **kw)
+                try:
+                    solve_selected(src[0], src[1], self.mode, out=(XA, XB), partitions=self.parts,
+                                   timings=timings, **kw)
+                except torch.cuda.OutOfMemoryError:
+                    # The solve workspace is allocated lazily by the first
+                    # solve: when two output slots leave too little room for
+                    # it, fall back to one slot (outputs streamed behind the
+                    # backward) and redo this energy.  Nothing of it has
+                    # reached the host yet.
+                    if not self._auto_slots or k != 0:
+                        raise
+                    self.out = None
+                    self.out_slots = 1
+                    torch.cuda.empty_cache()
+                    preloaded = nxt
+                    continue
                 done = torch.cuda.Event(enable_timing=True)
                 done.record(main)
                 with torch.cuda.device(self.device), torch.cuda.stream(self.d2h):
@@ -223,9 +251,10 @@ class HostEnergySweep:
                     out_free[o] = ev
             in_free[s] = done
             self.done_events.append(done)
-            if first and k + 1 < len(inputs):
-                nxt = self._load(inputs[k + 1], s ^ 1, kw["_io_events"].get("inputs_done"))
+            if first and held:
+                nxt = held[0]
             ready = nxt
+            k += 1
         main.wait_stream(self.d2h)
         main.wait_stream(self.h2d)
         main.synchronize()

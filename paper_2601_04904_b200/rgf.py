@@ -382,6 +382,9 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, 
         ev = torch.cuda.Event()
         ev.record(runner.copy_stream)
         io_events["inputs_done"] = ev
+        cb = io_events.get("on_inputs_done")
+        if cb is not None:  # before the host-output synchronization below
+            cb(ev)
     if stream_out:
         record_sweep(counter, n, bs, asz, mode, "forward")
         record_sweep(counter, n, bs, asz, mode, "backward")

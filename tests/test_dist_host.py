@@ -188,3 +188,90 @@ def test_host_windows_cover_pattern(n, parts):
         assert d.arrow_row + (hi - 1) * a * b * 16 == w.arrow_row[-1].data_ptr()
     assert sorted(owned["diag"]) == list(range(n))
     assert sorted(owned["lower"]) == list(range(n - 1))
+
+
+# --------------------------------------------------------------------------
+# the REFERENCE's own dist.py orchestration over TorchCollectives (gloo here,
+# NCCL on the GPU box: tests/test_gpu_nccl.py) -- numpy payloads as bytes
+# --------------------------------------------------------------------------
+
+REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def _ref_worker(rank, world, port, n, b, a, mode, q):
+    import sys
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, REF)
+    import torch.distributed as tdist
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import btasel  # the unmodified reference (baseline/_ref)
+        from btasel import dist as rdist
+        from paper_2601_04904_b200 import TorchCollectives
+        btasel.set_blas_threads(1)
+        A = btasel.generate_dd_bta(n, b, a, seed=5)
+        B = btasel.hermitianize(btasel.generate_dd_bta(n, b, a, seed=6)) if mode == "siq" else None
+        plan = btasel.plan_partitions(n, world, mode)
+        coll = TorchCollectives()
+        sl, _, _, _ = rdist._run_rank(A, B, plan, rank, coll, mode, None)
+        blobs = coll.gather_to_root(rdist._slice_to_bytes(sl))
+        kinds = [e.kind for e in coll.trace]
+        err = None
+        if rank == 0:
+            got = rdist._merge_slices(A, mode, [rdist._slice_from_bytes(x) for x in blobs])
+            ref = btasel.dist_solve(A, B, num_parts=world, mode=mode)  # reference ThreadHub
+            err = 0.0
+            for side in ("x_a", "x_b") if mode == "siq" else ("x_a",):
+                g, r = getattr(got, side), getattr(ref, side)
+                err = max(err, 0.0 if g.equals_exact(r) else 1.0)
+        q.put((rank, err, kinds, blobs is None))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc(), None, None))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "btasel")), reason="reference not installed (tools/stage_reference.sh)")
+@pytest.mark.parametrize("world,n,b,a,mode", [(2, 8, 3, 2, "siq"), (3, 12, 2, 1, "siq"), (3, 12, 3, 0, "si")])
+def test_reference_orchestration_over_torch_collectives(world, n, b, a, mode):
+    """The reference's own per-rank pipeline (dist.py:787-801: local_forward,
+    assemble_reduced, solve_reduced, local_backward) with TorchCollectives as
+    its Collectives: numpy BoundaryPayloads travel as bytes, the tip delta
+    sums in rank order, and the merged result is bit-identical to the
+    reference's in-process ThreadHub run."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ref_worker, args=(r, world, port, n, b, a, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=240) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, kinds, none_blobs in res:
+        assert not isinstance(err, str), err
+        assert kinds == (["all_gather", "all_reduce", "all_gather"] if a else ["all_gather", "all_gather"])[:len(kinds)]
+        assert none_blobs == (rank != 0)
+    assert res[0][1] == 0.0
+
+
+def test_host_payload_wire_roundtrip():
+    """BoundaryPayload.to_bytes/from_bytes (the byte form foreign transports
+    carry) round-trips blocks, kind, rank and the symmetry flags exactly."""
+    from paper_2601_04904_b200.dist import BoundaryPayload
+    rng = np.random.default_rng(1)
+    c = lambda r, k: rng.standard_normal((r, k)) + 1j * rng.standard_normal((r, k))  # noqa: E731
+    p = BoundaryPayload(rank=2, kind="middle", b=3, a=2, fused=True, sym_flags=1)
+    p.diag, p.coupling = [c(3, 3), c(3, 3)], [c(3, 3), c(3, 3)]
+    p.arrow_row, p.arrow_col = [c(2, 3), c(2, 3)], [c(3, 2), c(3, 2)]
+    p.b_diag, p.b_coupling = [c(3, 3), c(3, 3)], [c(3, 3), c(3, 3)]
+    p.b_arrow_row, p.b_arrow_col = [c(2, 3), c(2, 3)], [c(3, 2), c(3, 2)]
+    q = BoundaryPayload.from_bytes(p.to_bytes())
+    assert (q.rank, q.kind, q.b, q.a, q.fused, q.sym_flags) == (2, "middle", 3, 2, True, 1)
+    assert q.summary() == p.summary()
+    for f in ("diag", "coupling", "arrow_row", "arrow_col", "b_diag", "b_coupling", "b_arrow_row", "b_arrow_col"):
+        for x, y in zip(getattr(p, f), getattr(q, f)):
+            np.testing.assert_array_equal(x, y)
+    assert q.nbytes() == p.nbytes() == 16 * 2 * (4 * 9 + 4 * 6)

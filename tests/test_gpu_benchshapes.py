@@ -1,0 +1,222 @@
+"""GPU parity at the BENCHMARKED block shapes (BASELINE.json configs 4 and 5).
+
+* config-4 block shapes (b=512, tip a=256) at n=32, sequential RGF
+  (partitions=1) and the in-GPU 2-partition scheme (partitions=2, the bench
+  path), for Hermitian (bench protocol), anti-Hermitian (lesser/greater
+  self-energies) and general right-hand sides, vs the CPU oracle at the
+  north-star tolerance 1e-10 (max per-block relative Frobenius error,
+  reference tests/conftest.py:24-34);
+* config-5 block shapes (b=1024, a=256) at n=6 vs the oracle;
+* the block inverse at n=1024 (the 32-panel persistent Gauss-Jordan the
+  config-5 chain runs 256 times per energy) vs LAPACK;
+* the FULL config-4 bench inputs (n=1024) through the dense-free residuals
+  (A X_A = I on the block diagonal, reference tests/conftest.py:37-62; the
+  builder-derived block diagonal of A X_B - B X_A^H), evaluated on the GPU
+  with torch.matmul (cuBLAS ZGEMM) -- an independent checker, not the
+  library's own GEMM.
+"""
+
+import numpy as np
+import pytest
+from conftest import max_block_rel_err
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2601_04904_b200 as bs  # noqa: E402
+from paper_2601_04904_b200 import _native  # noqa: E402
+
+TOL = 1e-10
+
+
+def _scaled(m, z):
+    arr = {k: v * z for k, v in m.stacked().items()}
+    return bs.BtaMatrix.from_stacked(*m.shape_params, arr, copy=True)
+
+
+def _rhs(n, b, a, kind):
+    if kind == "general":
+        return bs.generate_dd_bta(n, b, a, seed=1)
+    h = bs.hermitianize(bs.generate_dd_bta(n, b, a, seed=1))
+    return h if kind == "hermitian" else _scaled(h, 1j)
+
+
+_ORACLE = {}
+
+
+def _oracle(n, b, a, kind):
+    key = (n, b, a, kind)
+    if key not in _ORACLE:
+        A = bs.generate_dd_bta(n, b, a, seed=0)
+        B = _rhs(n, b, a, kind)
+        _ORACLE[key] = (A, B, oracle.solve_selected(A, B, "siq"))
+    return _ORACLE[key]
+
+
+SYM = {"hermitian": 1, "skew": -1, "general": 0}
+
+
+@pytest.mark.parametrize("kind", ["hermitian", "skew", "general"])
+@pytest.mark.parametrize("parts", [1, 2])
+def test_config4_block_shapes_n32(kind, parts):
+    A, B, (xa, xb) = _oracle(32, 512, 256, kind)
+    dA, dB = bs.to_device(A), bs.to_device(B)
+    sol = bs.solve_selected(dA, dB, "siq", partitions=parts)
+    if parts == 1:  # the symmetric path taken is the one the exact check decided
+        assert _native.Context.get(torch.cuda.current_device()).b_symmetry()[1] == SYM[kind]
+    assert max_block_rel_err(bs.to_host(sol.x_a), xa) <= TOL
+    assert max_block_rel_err(bs.to_host(sol.x_b), xb) <= TOL
+
+
+def test_config4_block_shapes_si_mode():
+    A, _, _ = _oracle(32, 512, 256, "hermitian")
+    xa, _ = oracle.solve_selected(A, None, "si")
+    for parts in (1, 2):
+        sol = bs.solve_selected(bs.to_device(A), None, "si", partitions=parts)
+        assert max_block_rel_err(bs.to_host(sol.x_a), xa) <= TOL
+
+
+def test_config5_block_shapes_n6():
+    A, B, (xa, xb) = _oracle(6, 1024, 256, "hermitian")
+    sol = bs.solve_selected(bs.to_device(A), bs.to_device(B), "siq", partitions=1)
+    assert max_block_rel_err(bs.to_host(sol.x_a), xa) <= TOL
+    assert max_block_rel_err(bs.to_host(sol.x_b), xb) <= TOL
+
+
+def test_config5_energy_sweep_vs_oracle():
+    """The config-5 energy driver (EnergySweep, energy e = seeds (2e, 2e+1))
+    at config-5 block shapes, n=4: each energy's solution vs the oracle."""
+    n, b, a = 4, 1024, 256
+    sweep = bs.EnergySweep(n, b, a, "siq", partitions=1)
+    got = {}
+    sweep.run([0, 3], consume=lambda e, sol: got.__setitem__(e, (bs.to_host(sol.x_a), bs.to_host(sol.x_b))))
+    for e, (ga, gb) in got.items():
+        sa, sb = bs.energy_seeds(e)
+        A = bs.generate_dd_bta(n, b, a, seed=sa)
+        B = bs.hermitianize(bs.generate_dd_bta(n, b, a, seed=sb))
+        xa, xb = oracle.solve_selected(A, B, "siq")
+        assert max_block_rel_err(ga, xa) <= TOL
+        assert max_block_rel_err(gb, xb) <= TOL
+
+
+@pytest.mark.parametrize("n", [768, 1024])
+def test_block_inverse_large(n):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    x += np.diag(1.5 * (np.abs(x).sum(axis=1) + 1.0))
+    got = bs.block_inverse(x)
+    ref = np.linalg.inv(x)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert np.linalg.norm(x @ got - np.eye(n)) / np.sqrt(n) <= 1e-13
+
+
+def test_block_inverse_large_non_dd():
+    """A nonsingular, NOT diagonally dominant 1024 block (a Schur pivot of a
+    general matrix) still inverts to LAPACK accuracy."""
+    n = 1024
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    got = bs.block_inverse(x)
+    ref = np.linalg.inv(x)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+# --------------------------------------------------------------------------
+# full config-4 inputs: dense-free residuals with an independent checker
+# --------------------------------------------------------------------------
+
+
+def _bmm(x, y, hy=False):
+    return torch.matmul(x, y.conj().transpose(-1, -2) if hy else y)
+
+
+def _identity_residual(A, X, chunk=64):
+    """max_j ||(A X)_jj - I|| / sqrt(b) and the tip row (conftest.py:37-62)."""
+    n, b, a = A.shape_params
+    eye = torch.eye(b, dtype=torch.complex128, device=A.diag.device)
+    worst = 0.0
+    for j0 in range(0, n, chunk):
+        j1 = min(n, j0 + chunk)
+        acc = _bmm(A.diag[j0:j1], X.diag[j0:j1])
+        lo = max(j0, 1)
+        if lo < j1:  # lower[j-1] X.upper[j-1]
+            acc[lo - j0:] += _bmm(A.lower[lo - 1:j1 - 1], X.upper[lo - 1:j1 - 1])
+        hi = min(j1, n - 1)
+        if j0 < hi:  # upper[j] X.lower[j]
+            acc[:hi - j0] += _bmm(A.upper[j0:hi], X.lower[j0:hi])
+        if a:
+            acc += _bmm(A.arrow_col[j0:j1], X.arrow_row[j0:j1])
+        r = torch.linalg.matrix_norm(acc - eye).max().item() / np.sqrt(b)
+        worst = max(worst, r)
+    if a:
+        acc = A.tip @ X.tip + _bmm(A.arrow_row, X.arrow_col).sum(0)
+        worst = max(worst, torch.linalg.matrix_norm(acc - torch.eye(a, dtype=acc.dtype, device=acc.device))
+                    .item() / np.sqrt(a))
+    return worst
+
+
+def _quadratic_residual(A, B, XA, XB, chunk=64):
+    """max_j ||(A X_B - B X_A^H)_jj|| / ||(B X_A^H)_jj|| (+ tip row)."""
+    n, b, a = A.shape_params
+    worst = 0.0
+    for j0 in range(0, n, chunk):
+        j1 = min(n, j0 + chunk)
+        lhs = _bmm(A.diag[j0:j1], XB.diag[j0:j1])
+        rhs = _bmm(B.diag[j0:j1], XA.diag[j0:j1], hy=True)
+        lo = max(j0, 1)
+        if lo < j1:
+            lhs[lo - j0:] += _bmm(A.lower[lo - 1:j1 - 1], XB.upper[lo - 1:j1 - 1])
+            rhs[lo - j0:] += _bmm(B.lower[lo - 1:j1 - 1], XA.lower[lo - 1:j1 - 1], hy=True)
+        hi = min(j1, n - 1)
+        if j0 < hi:
+            lhs[:hi - j0] += _bmm(A.upper[j0:hi], XB.lower[j0:hi])
+            rhs[:hi - j0] += _bmm(B.upper[j0:hi], XA.upper[j0:hi], hy=True)
+        if a:
+            lhs += _bmm(A.arrow_col[j0:j1], XB.arrow_row[j0:j1])
+            rhs += _bmm(B.arrow_col[j0:j1], XA.arrow_col[j0:j1], hy=True)
+        r = (torch.linalg.matrix_norm(lhs - rhs) / torch.linalg.matrix_norm(rhs)).max().item()
+        worst = max(worst, r)
+    if a:
+        lhs = A.tip @ XB.tip + _bmm(A.arrow_row, XB.arrow_col).sum(0)
+        rhs = _bmm(B.tip, XA.tip, hy=True) + _bmm(B.arrow_row, XA.arrow_row, hy=True).sum(0)
+        worst = max(worst, (torch.linalg.matrix_norm(lhs - rhs) / torch.linalg.matrix_norm(rhs)).item())
+    return worst
+
+
+@pytest.mark.parametrize("parts", [2, 1])
+def test_config4_full_bench_inputs_dense_free(parts):
+    """The exact bench.py workload (n=1024, b=512, a=256, seeds 0/1, B
+    hermitianized, device generator) -- the output the headline times."""
+    n, b, a = 1024, 512, 256
+    A = bs.generate_dd_bta_device(n, b, a, seed=0)
+    B = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=1))
+    sol = bs.solve_selected(A, B, "siq", partitions=parts)
+    ra = _identity_residual(A, sol.x_a)
+    rq = _quadratic_residual(A, B, sol.x_a, sol.x_b)
+    del sol, A, B
+    bs.release_caches()
+    torch.cuda.empty_cache()
+    assert ra <= 1e-12, ra
+    assert rq <= 1e-11, rq
+
+
+def test_dense_free_checker_detects_errors():
+    """The torch checker itself: exact on a small oracle solution, and it
+    flags a perturbed block."""
+    n, b, a = 5, 16, 4
+    A = bs.generate_dd_bta(n, b, a, seed=0)
+    B = bs.hermitianize(bs.generate_dd_bta(n, b, a, seed=1))
+    xa, xb = oracle.solve_selected(A, B, "siq")
+    XA = bs.BtaMatrix(n, b, a, xa.diag, xa.lower, xa.upper, xa.arrow_row, xa.arrow_col, xa.tip)
+    XB = bs.BtaMatrix(n, b, a, xb.diag, xb.lower, xb.upper, xb.arrow_row, xb.arrow_col, xb.tip)
+    dA, dB, dXA, dXB = (bs.to_device(m) for m in (A, B, XA, XB))
+    assert _identity_residual(dA, dXA) <= 1e-13
+    assert _quadratic_residual(dA, dB, dXA, dXB) <= 1e-12
+    dXA.diag[2][3, 4] += 1e-6
+    dXB.lower[1][0, 0] += 1e-6
+    assert _identity_residual(dA, dXA) > 1e-9
+    assert _quadratic_residual(dA, dB, dXA, dXB) > 1e-9
