@@ -251,6 +251,9 @@ typedef struct {
                          /* (launches on concurrent streams overlap)      */
   double inverse_busy_ms;/* union of the inverses' spans                   */
   double inverse_flops;  /* sum of 8*n^3 over the inverses                 */
+  double gemm_exec_flops;/* tensor-pipe flops the GEMM launches executed:   */
+                         /* 6*M*N*K per product in the 3M kernel, 8*M*N*K */
+                         /* in the real-embedding kernel                   */
 } bsel_profile_t;
 /* Bracket every launch with CUDA events on its stream until _end (which
  * synchronizes the device and returns the totals).                        */

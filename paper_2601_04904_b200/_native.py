@@ -159,6 +159,7 @@ class Profile(ctypes.Structure):
         ("gemm_busy_ms", ctypes.c_double),
         ("inverse_busy_ms", ctypes.c_double),
         ("inverse_flops", ctypes.c_double),
+        ("gemm_exec_flops", ctypes.c_double),
     ]
 
 

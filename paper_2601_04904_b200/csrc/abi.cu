@@ -620,6 +620,7 @@ int bsel_profile_end(bsel_profile_t* out) {
     out->gemm_busy_ms = t.gemm_busy_ms;
     out->inverse_busy_ms = t.inverse_busy_ms;
     out->inverse_flops = t.inverse_flops;
+    out->gemm_exec_flops = t.gemm_exec_flops;
   }
   return BSEL_OK;
 }

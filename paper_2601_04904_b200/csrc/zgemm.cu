@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <deque>
 #include <mutex>
+#include <string>
 
 namespace bsel {
 
@@ -381,6 +382,7 @@ struct ProfRec {
   int kind;
   double flops;
   double bytes;
+  double exec_flops;
 };
 // Partitions of one solve may run in concurrent host threads (dist.py
 // _Lanes): records are appended under a mutex (deque: stable references),
@@ -416,12 +418,13 @@ int profile_open(cudaStream_t s) {
   cudaEventRecord(g_prof[id].t0, s);
   return id;
 }
-void profile_close(int id, cudaStream_t s, int kind, double flops, double bytes) {
+void profile_close(int id, cudaStream_t s, int kind, double flops, double bytes, double exec_flops) {
   if (id < 0) return;
   std::lock_guard<std::mutex> lock(g_prof_mu);
   g_prof[id].kind = kind;
   g_prof[id].flops = flops;
   g_prof[id].bytes = bytes;
+  g_prof[id].exec_flops = exec_flops < 0.0 ? flops : exec_flops;
   cudaEventRecord(g_prof[id].t1, s);
 }
 ProfileTotals profile_end() {
@@ -446,6 +449,7 @@ ProfileTotals profile_end() {
     if (kind == 0) {
       ++t.gemm_launches;
       t.gemm_flops += g_prof[i].flops;
+      t.gemm_exec_flops += g_prof[i].exec_flops;
       t.gemm_bytes += g_prof[i].bytes;
       t.gemm_ms += ms;
     } else {
@@ -502,6 +506,36 @@ cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cf
   std::stable_sort(batch.p, batch.p + w, [](const GemmProblem& x, const GemmProblem& y) {
     return problem_weight(x) > problem_weight(y);
   });
+  // Kernel choice.  The 3M TMA kernel (zgemm3m.cu) forms each complex
+  // product from three real products: 25 % fewer tensor-pipe flops, but the
+  // pre-added operands (Re + Im) round, so even a product with an exactly
+  // real / identity factor is no longer exact.  Products of small blocks
+  // (any of M, N, K below BSEL_GEMM3M_MIN, default 32 complex) cost little
+  // and keep the exact real-embedding form (this kernel): the reference's
+  // exact small-system answers (identity systems: X_B == B bit for bit,
+  // pkg/tests/test_rgf.py:64-72) stay exact.  BSEL_GEMM=4m / 3m forces one
+  // kernel everywhere.
+  static const int mode = [] {
+    const char* e = getenv("BSEL_GEMM");
+    return !e ? 0 : std::string(e) == "4m" ? 4 : std::string(e) == "3m" ? 3 : 0;
+  }();
+  static const int min3 = [] {
+    const char* e = getenv("BSEL_GEMM3M_MIN");
+    return e ? atoi(e) : 32;
+  }();
+  if (tile_cfg == kTile4m64 || tile_cfg == kTile4m32) {
+    tile_cfg = tile_cfg == kTile4m64 ? kTile64 : kTile32;
+  } else if (tile_cfg >= kTile3m64 && tile_cfg <= kTile3m32) {
+    return launch_gemm_batch_3m(batch, stream, tile_cfg);
+  } else if (mode != 4) {
+    bool big = true;
+    for (int i = 0; i < w && big; ++i) {
+      const GemmProblem& P = batch.p[i];
+      big = P.M >= min3 && P.N >= min3;
+      for (int t = 0; t < P.nterms && big; ++t) big = P.term[t].K >= min3;
+    }
+    if (mode == 3 || big) return launch_gemm_batch_3m(batch, stream, tile_cfg);
+  }
   if (tile_cfg == kTileAuto || tile_cfg == kTileAutoWide) {
     int64_t tiles64 = 0;
     for (int i = 0; i < w; ++i)

@@ -62,6 +62,7 @@ struct GemmTerm {
   uint8_t opA, opB;
   int8_t sign;        // +1 / -1
   uint8_t pad_;
+  uint32_t tmaA, tmaB;  // TMA descriptor slots (filled by the 3M launcher)
 };
 
 struct GemmAddend {
@@ -96,6 +97,7 @@ struct GemmBatch {
   // those SMs stay free for a concurrent latency-critical kernel
   int32_t avoid_sms;
   unsigned* tile_counter;
+  const void* tma_table;  // device table of CUtensorMap descriptors (3M launcher)
   GemmProblem p[kMaxProblems];
 };
 
@@ -103,11 +105,15 @@ struct GemmBatch {
 // kTileAuto: 64x64 tiles once a launch has >= 2 waves of them; kTileAutoWide:
 // already from 128 of them (BSEL_GEMM_MIN_TILES64_WIDE): the middle
 // partitions' k = 3 back-substitution, measured best there.
-enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3 };
+enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3,
+                     // forced kernel variants (microbenchmarks / A-B tests)
+                     kTile3m64 = 10, kTile3m6432 = 11, kTile3m32 = 12, kTile4m64 = 20, kTile4m32 = 21 };
 
 // Launch one grouped batch on `stream`.  Problems with M==0 or N==0 are
 // dropped.  Returns cudaSuccess or the launch error.
 cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cfg = kTileAuto);
+// The 3-multiplication bulk-async kernel (zgemm3m.cu) behind launch_gemm_batch.
+cudaError_t launch_gemm_batch_3m(GemmBatch& batch, cudaStream_t stream, int tile_cfg);
 
 // Number of SMs of the current device (cached).
 int device_sm_count();
@@ -127,12 +133,13 @@ struct ProfileTotals {
   double inverse_ms;
   double gemm_bytes;
   double gemm_busy_ms, inverse_busy_ms, inverse_flops;
+  double gemm_exec_flops;  // executed tensor-pipe flops (3M: 6MNK, real embedding: 8MNK)
 };
 void profile_begin();
 ProfileTotals profile_end();
 bool profiling();
 void profile_suspend(bool on);  // temporarily ignore GEMM launches (inside an inverse)
 int profile_open(cudaStream_t s);                          // returns record id (or -1)
-void profile_close(int id, cudaStream_t s, int kind, double flops, double bytes = 0.0);
+void profile_close(int id, cudaStream_t s, int kind, double flops, double bytes = 0.0, double exec_flops = -1.0);
 
 }  // namespace bsel

@@ -90,7 +90,36 @@ def _factor_desc(n, b, a, fused, dev: dict, A: DeviceBta, B: DeviceBta | None) -
         f.b_tip = _ptr(dev["b_tip"])
         f.b_arrow_row_elim = _ptr(B.arrow_row)
         f.b_arrow_col_elim = _ptr(B.arrow_col)
+    for k in _ELIM:
+        setattr(f, k, _ptr(dev.get(k)))
     return f
+
+
+_ELIM = ("elim_f", "elim_g", "elim_q", "elim_k", "elim_h", "elim_ha", "elim_eq", "elim_ek")
+
+
+def _alloc_elim(n, b, a, fused, c128) -> dict:
+    """Elimination products retained forward -> backward (bsel_factors_t),
+    the same set bsel_solve_selected keeps, so the split forward / backward
+    runs exactly the facade's kernels (bitwise equal results, reference
+    acceptance criterion 8, test_acceptance.py:290-305)."""
+    import os
+
+    extra = os.environ.get("BSEL_FWD_BWD_PRODUCTS", "0") not in ("", "0")
+    e = {"elim_f": torch.empty((n, b, b), **c128), "elim_h": torch.empty((n, b, b), **c128)}
+    if a:
+        e["elim_g"] = torch.empty((n, a, b), **c128)
+        if extra or not fused:
+            e["elim_ha"] = torch.empty((n, b, a), **c128)
+    if fused:
+        e["elim_q"] = torch.empty((n, b, b), **c128)
+        if a:
+            e["elim_k"] = torch.empty((n, b, a), **c128)
+        if extra:
+            e["elim_eq"] = torch.empty((n, b, b), **c128)
+            if a:
+                e["elim_ek"] = torch.empty((n, b, a), **c128)
+    return e
 
 
 def _forward(a, b, counter, require_bt):
@@ -111,6 +140,7 @@ def _forward(a, b, counter, require_bt):
     if fused:
         dev.update(s_b=torch.empty((max(n - 1, 0), bs, bs), **c128),
                    b_diag_last=torch.empty((bs, bs), **c128), b_tip=torch.empty((asz, asz), **c128))
+    dev.update(_alloc_elim(n, bs, asz, fused, c128))
     fd = _factor_desc(n, bs, asz, fused, dev, A, B)
     ad = A.desc()
     bd = B.desc() if fused else None

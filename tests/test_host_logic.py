@@ -138,7 +138,7 @@ def test_abi_struct_layouts():
     import tempfile
     names = {"Status": "bsel_status_t", "Bta": "bsel_bta_t", "Factors": "bsel_factors_t",
              "LocalFactors": "bsel_local_factors_t", "Profile": "bsel_profile_t", "HostIo": "bsel_host_io_t"}
-    sizes = {"Status": 272, "Bta": 72, "Factors": 104, "LocalFactors": 96, "Profile": 48, "HostIo": 56}
+    sizes = {"Status": 272, "Bta": 72, "Factors": 104, "LocalFactors": 96, "Profile": 80, "HostIo": 56}
     if shutil.which("gcc"):
         fmt = " ".join(["%zu"] * len(names))
         src = ('#include <stdio.h>\n#include "btasel_b200.h"\nint main(void){printf("' + fmt + '",'
