@@ -5,8 +5,9 @@
 // stream diag | lower | upper | arrow_row | arrow_col | tip uses positions
 // 2e+1 (re) and 2e+2 (im).  This is bit-identical to the host generator.
 // The dominance shift needs |row| sums across blocks; they are accumulated
-// left-to-right in double (the host uses numpy pairwise sums, so the shifted
-// diagonal can differ from the host generator in the last bit).
+// in numpy's pairwise order with numpy's rounding of the shift (see
+// pairwise_abs / shift_entry), so the shifted diagonal matches the host
+// generator up to the last-bit behaviour of the two libm's hypot.
 #include <cstdint>
 
 #include "generate.cuh"
@@ -34,54 +35,77 @@ __global__ void fill_uniform_kernel(double2* out, int64_t count, uint64_t seed, 
 
 __device__ __forceinline__ double cabs_(double2 z) { return hypot(z.x, z.y); }
 
-// One thread per global diagonal row r = i*b + row: off-diagonal |row| sum
-// (diag block without its diagonal entry, lower[i-1], upper[i], arrow_col[i]),
-// then push the diagonal entry along its phase.
+// numpy's pairwise summation (umath loops_utils pairwise_sum) of |x_j| over
+// a contiguous run of n complex entries: below 8 a plain loop, up to 128
+// eight interleaved accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+// plus the tail, above that the two halves (first half rounded down to a
+// multiple of 8) summed recursively.  The reference's np.abs(X).sum(axis=1)
+// row sums (matrix.py:262-282) therefore come out with numpy's rounding.
+__device__ double pairwise_abs(const double2* x, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, cabs_(x[i]));
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = cabs_(x[j]);
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], cabs_(x[i + j]));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, cabs_(x[i]));
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_abs(x, n2), pairwise_abs(x + n2, n - n2));
+}
+
+// d + dominance (rs + 1) phase(d), evaluated as numpy does: phase = d / |d|
+// by numpy's complex division (Smith's form: d * (1/|d|) for a real
+// divisor), then a real x complex product and a complex add, each rounded
+// separately (no FMA contraction).
+__device__ __forceinline__ double2 shift_entry(double2 v, double rs, double dominance) {
+  const double mag = cabs_(v);
+  double px = 1.0, py = 0.0;
+  if (mag > 0) {
+    const double scl = __drcp_rn(mag);
+    px = __dmul_rn(v.x, scl);
+    py = __dmul_rn(v.y, scl);
+  }
+  const double shift = __dmul_rn(dominance, __dadd_rn(rs, 1.0));
+  return make_double2(__dadd_rn(v.x, __dmul_rn(shift, px)), __dadd_rn(v.y, __dmul_rn(shift, py)));
+}
+
+// One thread per global diagonal row r = i*b + row: the reference's
+// off-diagonal |row| sum (rs = sum(|diag row|) - |d|, then + lower[i-1] row,
+// + upper[i] row, + arrow_col[i] row, matrix.py:271-279), then the shift.
 __global__ void dominance_rows_kernel(BtaDevView m, double dominance) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= m.n * m.b) return;
   const int64_t i = r / m.b, row = r % m.b, b = m.b, a = m.a;
   const double2* d = m.diag + i * b * b + row * b;
-  double s = 0.0;
-  for (int64_t j = 0; j < b; ++j)
-    if (j != row) s += cabs_(d[j]);
-  if (i > 0) {
-    const double2* l = m.lower + (i - 1) * b * b + row * b;
-    for (int64_t j = 0; j < b; ++j) s += cabs_(l[j]);
-  }
-  if (i < m.n - 1) {
-    const double2* u = m.upper + i * b * b + row * b;
-    for (int64_t j = 0; j < b; ++j) s += cabs_(u[j]);
-  }
-  if (a > 0) {
-    const double2* c = m.arrow_col + i * b * a + row * a;
-    for (int64_t j = 0; j < a; ++j) s += cabs_(c[j]);
-  }
+  double s = __dadd_rn(pairwise_abs(d, b), -cabs_(d[row]));
+  if (i > 0) s = __dadd_rn(s, pairwise_abs(m.lower + (i - 1) * b * b + row * b, b));
+  if (i < m.n - 1) s = __dadd_rn(s, pairwise_abs(m.upper + i * b * b + row * b, b));
+  if (a > 0) s = __dadd_rn(s, pairwise_abs(m.arrow_col + i * b * a + row * a, a));
   double2* dd = m.diag + i * b * b + row * b + row;
-  const double2 v = *dd;
-  const double mag = cabs_(v);
-  const double px = mag > 0 ? v.x / mag : 1.0, py = mag > 0 ? v.y / mag : 0.0;
-  const double shift = dominance * (s + 1.0);
-  *dd = make_double2(v.x + shift * px, v.y + shift * py);
+  *dd = shift_entry(*dd, s, dominance);
 }
 
 __global__ void dominance_tip_kernel(BtaDevView m, double dominance) {
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t a = m.a, b = m.b;
   if (row >= a) return;
-  double s = 0.0;
-  for (int64_t j = 0; j < a; ++j)
-    if (j != row) s += cabs_(m.tip[row * a + j]);
-  for (int64_t i = 0; i < m.n; ++i) {
-    const double2* r = m.arrow_row + i * a * b + row * b;
-    for (int64_t j = 0; j < b; ++j) s += cabs_(r[j]);
-  }
+  const double2* t = m.tip + row * a;
+  double s = __dadd_rn(pairwise_abs(t, a), -cabs_(t[row]));
+  for (int64_t i = 0; i < m.n; ++i) s = __dadd_rn(s, pairwise_abs(m.arrow_row + i * a * b + row * b, b));
   double2* dd = m.tip + row * a + row;
-  const double2 v = *dd;
-  const double mag = cabs_(v);
-  const double px = mag > 0 ? v.x / mag : 1.0, py = mag > 0 ? v.y / mag : 0.0;
-  const double shift = dominance * (s + 1.0);
-  *dd = make_double2(v.x + shift * px, v.y + shift * py);
+  *dd = shift_entry(*dd, s, dominance);
 }
 
 // (X + X^H)/2 on the pattern (matrix.py:337-354); out-of-place pairs.

@@ -613,7 +613,15 @@ cudaError_t launch3(GemmBatch& batch, cudaStream_t stream) {
     }
     hold.lock();
   }
-  int grid = std::min(tiles, resident);
+  // persistent grid (one wave of CTAs looping over the tiles; the producer
+  // overlaps the next tile's loads with the epilogue) or, with
+  // BSEL_GEMM3M_PERSIST=0, one CTA per tile (the CTA scheduler can then slot
+  // a higher-priority stream's CTAs in between tiles)
+  static const bool persist = [] {
+    const char* e = getenv("BSEL_GEMM3M_PERSIST");
+    return !(e && atoi(e) == 0);
+  }();
+  int grid = persist ? std::min(tiles, resident) : tiles;
   if (batch.max_ctas > 0 && batch.max_ctas < grid) grid = batch.max_ctas;
   if (batch.avoid_sms > 0) {
     if (!batch.tile_counter) return cudaErrorInvalidValue;

@@ -769,14 +769,19 @@ class InGpuPartitions:
     latency-bound chain of a single sweep leaves idle.  Factor buffers are
     kept between runs for repeated solves of one shape."""
 
-    def __init__(self, shape, mode, parts, device, plan=None):
+    def __init__(self, shape, mode, parts, device, plan=None, local=None):
+        """``local``: the partition indices this process runs (default: all
+        ``parts``, the single-GPU scheme); with a subset -- k partitions per
+        GPU of a multi-GPU job -- ``run`` needs a hub that exchanges with the
+        other ranks (_RankHub)."""
         self.n, self.b, self.a = shape
         self.mode = mode
         self.parts = parts
         self.device = device
         self.plan = plan or plan_partitions(self.n, parts, mode)
-        self.lanes = _Lanes(device, parts)
-        self._factors = [None] * parts
+        self.local = list(range(parts)) if local is None else list(local)
+        self.lanes = _Lanes(device, len(self.local))
+        self._factors = [None] * len(self.local)
         self.chunk = None
         self.copy_stream = torch.cuda.Stream(device)  # shared by the partitions' input chunks
         self.counters = []
@@ -797,25 +802,27 @@ class InGpuPartitions:
         chunk = self.chunk or int(os.environ.get("BSEL_STREAM_CHUNK", "8"))
         hub = hub or LocalHub(parts)
         tm = _PhaseTimer(("forward", "communication", "reduced", "backward"))
-        self.counters = counters = [OpCounter(b=A.b, a=A.a) for _ in range(parts)]
-        results = [None] * parts
+        loc = self.local
+        self.counters = counters = [OpCounter(b=A.b, a=A.a) for _ in loc]
+        results = [None] * len(loc)
         tm.start("forward")
 
-        def fwd(rank, ctx):
+        def fwd(lane, ctx):
+            rank = loc[lane]
             sync = None
             if host_in is not None:
-                sync = _host_io(chunk, a=host_in[0], b=host_in[1] if B is not None else None, copy_tip=rank == 0,
-                                stream=self.copy_stream)
-            results[rank] = local_forward(A, B, plan, rank, counters[rank], _factors=self._factors[rank], _ctx=ctx,
+                sync = _host_io(chunk, a=host_in[0], b=host_in[1] if B is not None else None,
+                                copy_tip=rank == loc[0], stream=self.copy_stream)
+            results[lane] = local_forward(A, B, plan, rank, counters[lane], _factors=self._factors[lane], _ctx=ctx,
                                           _sync=sync)
-            self._factors[rank] = results[rank][2]
+            self._factors[lane] = results[lane][2]
 
         errors = self.lanes.run(fwd)
         tm.stop("forward")
         if errors:
             primary = [e for e in errors if not isinstance(e[1], ProtocolError)]
-            rank, exc = min(primary or errors, key=lambda e: e[0])
-            raise WorkerError(rank, exc) from exc
+            lane, exc = min(primary or errors, key=lambda e: e[0])
+            raise WorkerError(loc[lane], exc) from exc
         tm.start("communication")
         gathered = hub.all_gather_all([r[0] for r in results])
         tip_sum = hub.all_reduce_all([r[1] for r in results]) if A.a > 0 else None
@@ -831,11 +838,12 @@ class InGpuPartitions:
         io_out = None
         if host_out is not None:
             io_out = _host_io(chunk, x_a=host_out[0], x_b=host_out[1] if B is not None else None)
-        errors = self.lanes.run(lambda rank, ctx: local_backward(
-            A, B, plan, rank, results[rank][2], reduced, red_sol, counters[rank], out=out, _ctx=ctx, _sync=io_out))
+        errors = self.lanes.run(lambda lane, ctx: local_backward(
+            A, B, plan, loc[lane], results[lane][2], reduced, red_sol, counters[lane], out=out, _ctx=ctx,
+            _sync=io_out))
         if errors:
-            rank, exc = min(errors, key=lambda e: e[0])
-            raise WorkerError(rank, exc) from exc
+            lane, exc = min(errors, key=lambda e: e[0])
+            raise WorkerError(loc[lane], exc) from exc
         tm.stop("backward")
         self._tm = tm
         return out
@@ -1077,24 +1085,75 @@ def _solve_as_rank(a, b, plan, coll, mode, counter, timings, recursive_parts):
 AUX_AVOID_SMS = int(os.environ.get("BSEL_AUX_AVOID_SMS", "32"))
 
 
+class _RankHub:
+    """The exchange of k partitions per rank over a TorchCollectives endpoint
+    (InGpuPartitions with ``local``): this rank's k payload slots travel in
+    ONE NCCL all_gather (rank-major = partition order), the k tip deltas are
+    summed locally in partition order and then across ranks in rank order
+    (one rank-ordered all_reduce): still exactly one all_gather + one
+    all_reduce per solve (test_acceptance.py:201-243)."""
+
+    def __init__(self, coll: TorchCollectives, k: int):
+        self.coll, self.k = coll, k
+        self.world_size = coll.world_size * k
+
+    def all_gather_all(self, payloads: list) -> list:
+        if len(payloads) != self.k:
+            raise ProtocolError(f"expected {self.k} local payloads, got {len(payloads)}")
+        slot = payloads[0].slot_elems()
+        allp = self.coll.gather_tensor(torch.cat([p.pack() for p in payloads])).view(-1, slot)
+        hdrs = allp[:, :4].cpu().tolist()
+        out = [payloads[0].unpack(allp[q], rank=q, header=hdrs[q]) for q in range(allp.shape[0])]
+        self.coll._record("all_gather", [p.summary() for p in out])
+        return out
+
+    def all_reduce_all(self, arrays: list):
+        total = arrays[0].clone()
+        for part in arrays[1:]:
+            total += part
+        return self.coll.all_reduce_sum(total)
+
+
 class DistSolver:
     """Repeated distributed solves of one energy point on this rank with all
-    device buffers preallocated (the bench / multi-GPU production path)."""
+    device buffers preallocated (the bench / multi-GPU production path).
+
+    ``parts_per_rank`` = k: the plan has world x k partitions and this rank
+    runs partitions [rank k, rank k + k) concurrently as lanes on its GPU
+    (k Schur chains per GPU instead of one; e.g. the reference's 8-partition
+    plan on 4 GPUs)."""
 
     def __init__(self, A: DeviceBta, B: DeviceBta | None, mode: str, world: int, rank: int, device,
-                 transport: TorchCollectives | None = None, plan_costs=None):
+                 transport: TorchCollectives | None = None, plan_costs=None, parts_per_rank: int = 1):
         self.A, self.B, self.mode = A, B if mode == "siq" else None, mode
+        self.k = int(parts_per_rank)
         # plan_costs: per-block (end, middle) costs for the partition sizes
         # (default: the reference's plan, partition.py:52-90)
-        self.plan = plan_partitions(A.n, world, mode, costs=plan_costs)
+        self.plan = plan_partitions(A.n, world * self.k, mode, costs=plan_costs)
         self.rank = rank
         self.coll = transport or TorchCollectives()
         self.out = (DeviceBta.empty(A.n, A.b, A.a, device),
                     DeviceBta.empty(A.n, A.b, A.a, device) if self.B is not None else None)
         self._fac = None
         self.timings = {}
+        self._runner = None
+        if self.k > 1:
+            local = list(range(rank * self.k, (rank + 1) * self.k))
+            self._runner = InGpuPartitions(A.shape_params, mode, world * self.k, device, plan=self.plan, local=local)
+            self._hub = _RankHub(self.coll, self.k)
+
+    def owned_range(self):
+        """[lo, hi) of the diagonal blocks this rank's partitions cover."""
+        r = self.plan.ranges
+        return r[self.rank * self.k][0], r[self.rank * self.k + self.k - 1][1]
 
     def solve(self, host_in=None, host_out=None):
+        if self._runner is not None:
+            if host_in is not None:
+                self._copy_separators(host_in)
+            out = self._runner.run(self.A, self.B, out=self.out, hub=self._hub, host_in=host_in, host_out=host_out)
+            self._tm = self._runner._tm
+            return out
         """One distributed solve.  ``host_in`` = (a, b) full-size pinned host
         BtaMatrix: this rank's partition streams in behind its forward sweep
         (plus the separators and tip every rank needs for the replicated
@@ -1142,7 +1201,7 @@ class DistSolver:
     def _copy_separators(self, host_in):
         """Couplings at the other partitions' boundaries (the reduced system
         is assembled on every rank)."""
-        lo, hi = self.plan.ranges[self.rank]
+        lo, hi = self.owned_range()
         for p in range(self.plan.num_parts - 1):
             g = self.plan.ranges[p][1] - 1
             if lo <= g < hi:

@@ -95,3 +95,133 @@ def test_nccl_dist_solve_matches_oracle(world, n, b, a):
         assert tb is None, tb
         assert kinds == (["all_gather", "all_reduce"] if a else ["all_gather"])
     assert res[0][1] <= 1e-10
+
+
+def _rank_k(rank, world, k, port, n, b, a, q):
+    """k partitions per rank (DistSolver parts_per_rank): the world*k plan
+    (e.g. the reference's 8-partition plan on 4 GPUs) vs the oracle, device
+    path and host-window streaming path."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        import oracle
+        import paper_2601_04904_b200 as bs
+        from conftest import max_block_rel_err
+        dA = bs.generate_dd_bta_device(n, b, a, seed=0)
+        dB = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=1))
+        coll = bs.TorchCollectives()
+        s = bs.DistSolver(dA, dB, "siq", world, rank, dev, transport=coll, parts_per_rank=k)
+        XA, XB = s.solve()
+        kinds = [e.kind for e in coll.trace]
+        # merge the sharded outputs on rank 0 (disjoint blocks: exact sum)
+        for m in (XA, XB):
+            for t in m.tensors().values():
+                if t.numel():
+                    dist.reduce(torch.view_as_real(t), dst=0)
+        err = None
+        if rank == 0:
+            A = bs.to_host(dA)
+            B = bs.to_host(dB)
+            xa, xb = oracle.dist_solve(A, B, num_parts=world * k, mode="siq")
+            err = max(max_block_rel_err(bs.to_host(XA), xa), max_block_rel_err(bs.to_host(XB), xb))
+        # host-window streaming over the union of this rank's partitions
+        lo, hi = s.owned_range()
+        seps = [s.plan.ranges[p][1] - 1 for p in range(world * k - 1)]
+        win = tuple(bs.HostWindow(n, b, a, lo, hi, seps).fill_from(M) for M in (dA, dB))
+        hout = (bs.HostWindow(n, b, a, lo, hi), bs.HostWindow(n, b, a, lo, hi))
+        ref = s.solve()
+        c = min(hi, n - 1)
+        refc = [(X.diag[lo:hi].cpu(), X.lower[lo:c].cpu()) for X in ref]
+        s.solve(host_in=win, host_out=hout)
+        torch.cuda.synchronize()
+        serr = 0.0
+        for (rd, rl), H in zip(refc, hout):
+            for g_, r_ in ((H.diag, rd), (H.lower, rl)):
+                if r_.numel():
+                    serr = max(serr, float(torch.linalg.norm(g_ - r_) / torch.linalg.norm(r_)))
+        dist.barrier()
+        q.put((rank, err, kinds, serr, None))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, None, None, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,k,n,b,a", [(2, 2, 20, 48, 8), (4, 2, 24, 32, 8), (4, 2, 40, 64, 16)])
+def test_nccl_k_partitions_per_rank(world, k, n, b, a):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_k, args=(r, world, k, port, n, b, a, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+    for rank, err, kinds, serr, tb in res:
+        assert tb is None, tb
+        assert kinds == ["all_gather", "all_reduce"]  # one of each per solve, k partitions per rank
+        assert serr <= 1e-12
+    assert res[0][1] <= 1e-10
+
+
+REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def _ref_rank(rank, world, port, n, b, a, q):
+    """The reference's own dist.py per-rank pipeline driven over NCCL through
+    TorchCollectives (numpy payloads as bytes), vs the reference's ThreadHub run."""
+    try:
+        import sys
+        sys.path.insert(0, REF)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+        import btasel
+        from btasel import dist as rdist
+        import paper_2601_04904_b200 as bs
+        btasel.set_blas_threads(1)
+        A = btasel.generate_dd_bta(n, b, a, seed=5)
+        B = btasel.hermitianize(btasel.generate_dd_bta(n, b, a, seed=6))
+        plan = btasel.plan_partitions(n, world, "siq")
+        coll = bs.TorchCollectives()
+        sl, _, _, _ = rdist._run_rank(A, B, plan, rank, coll, "siq", None)
+        blobs = coll.gather_to_root(rdist._slice_to_bytes(sl))
+        kinds = [e.kind for e in coll.trace]
+        ok = None
+        if rank == 0:
+            got = rdist._merge_slices(A, "siq", [rdist._slice_from_bytes(x) for x in blobs])
+            ref = btasel.dist_solve(A, B, num_parts=world, mode="siq")
+            ok = got.x_a.equals_exact(ref.x_a) and got.x_b.equals_exact(ref.x_b)
+        dist.barrier()
+        q.put((rank, ok, kinds, None))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, None, None, traceback.format_exc()))
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "btasel")), reason="reference not staged")
+@pytest.mark.parametrize("world,n,b,a", [(2, 10, 8, 4), (4, 24, 8, 4)])
+def test_reference_dist_over_nccl(world, n, b, a):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ref_rank, args=(r, world, port, n, b, a, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok, kinds, tb in res:
+        assert tb is None, tb
+        assert kinds[:2] == ["all_gather", "all_reduce"]  # + the output gather_to_root round
+    assert res[0][1] is True

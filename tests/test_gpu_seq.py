@@ -285,17 +285,34 @@ def test_timings_and_device_path():
     assert max_block_rel_err(bs.to_host(sol.x_b), host.x_b) == 0.0
 
 
-def test_device_generator_matches_host_generator():
+@pytest.mark.parametrize("n,b,a,seed", [(5, 16, 4, 0), (3, 33, 0, 7), (4, 8, 12, 123), (3, 512, 256, 0),
+                                        (2, 1024, 256, 5), (6, 7, 300, 9)])
+def test_device_generator_matches_host_generator(n, b, a, seed):
+    """splitmix64 stream bit-identical; the dominance-shifted diagonal within
+    1 ulp of the host (numpy) generator per component -- the device sums |row|
+    in numpy's pairwise order with numpy's rounding of the shift
+    (generate.cu pairwise_abs / shift_entry); only the two libm's hypot may
+    differ in the last bit."""
+    d = bs.to_host(bs.generate_dd_bta_device(n, b, a, seed=seed))
+    h = bs.generate_dd_bta(n, b, a, seed=seed)
+    same = total = 0
+    for (k, i, x), (_, _, y) in zip(d.pattern_blocks(), h.pattern_blocks()):
+        if k in ("diag", "tip"):
+            off = ~np.eye(x.shape[0], dtype=bool)
+            np.testing.assert_array_equal(x[off], y[off])
+            for comp in (np.real, np.imag):
+                gx, gy = comp(np.diagonal(x)), comp(np.diagonal(y))
+                assert np.all(np.abs(gx - gy) <= np.spacing(np.abs(gy))), (k, i)
+                same += int(np.sum(gx == gy))
+                total += gx.size
+        else:
+            np.testing.assert_array_equal(x, y)
+    assert same >= 0.99 * total, (same, total)
+
+
+def test_device_hermitianize_matches_host():
     for n, b, a, seed in ((5, 16, 4, 0), (3, 33, 0, 7), (4, 8, 12, 123)):
-        d = bs.to_host(bs.generate_dd_bta_device(n, b, a, seed=seed))
         h = bs.generate_dd_bta(n, b, a, seed=seed)
-        for (k, i, x), (_, _, y) in zip(d.pattern_blocks(), h.pattern_blocks()):
-            if k in ("diag", "tip"):
-                off = ~np.eye(x.shape[0], dtype=bool)
-                np.testing.assert_array_equal(x[off], y[off])
-                np.testing.assert_allclose(np.diagonal(x), np.diagonal(y), rtol=2e-15, atol=0)  # row sums: sequential vs pairwise
-            else:
-                np.testing.assert_array_equal(x, y)
         hd = bs.to_host(bs.hermitianize_device(bs.to_device(h)))
         hh = bs.hermitianize(h)
         assert hd.equals_exact(hh)
