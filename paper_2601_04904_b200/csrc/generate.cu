@@ -6,8 +6,8 @@
 // 2e+1 (re) and 2e+2 (im).  This is bit-identical to the host generator.
 // The dominance shift needs |row| sums across blocks; they are accumulated
 // in numpy's pairwise order with numpy's rounding of the shift (see
-// pairwise_abs / shift_entry), so the shifted diagonal matches the host
-// generator up to the last-bit behaviour of the two libm's hypot.
+// pairwise_abs / shift_entry) and numpy's complex absolute (cabs_), so the
+// shifted diagonal matches the host generator bit for bit.
 #include <cstdint>
 
 #include "generate.cuh"
@@ -33,7 +33,17 @@ __global__ void fill_uniform_kernel(double2* out, int64_t count, uint64_t seed, 
   }
 }
 
-__device__ __forceinline__ double cabs_(double2 z) { return hypot(z.x, z.y); }
+// |z| exactly as numpy's SIMD complex absolute (numpy 2.x, AVX2 / AVX-512
+// hosts) computes it: larger * sqrt(fma(r, r, 1)) with r = smaller / larger
+// (checked bit for bit against np.abs on 2e5 random entries; libm hypot
+// differs from it in ~35 % of the last bits).
+__device__ __forceinline__ double cabs_(double2 z) {
+  const double ax = fabs(z.x), ay = fabs(z.y);
+  const double mx = fmax(ax, ay), mn = fmin(ax, ay);
+  if (mx == 0.0) return 0.0;
+  const double r = __ddiv_rn(mn, mx);
+  return __dmul_rn(mx, __dsqrt_rn(__fma_rn(r, r, 1.0)));
+}
 
 // numpy's pairwise summation (umath loops_utils pairwise_sum) of |x_j| over
 // a contiguous run of n complex entries: below 8 a plain loop, up to 128
