@@ -51,7 +51,7 @@ WORKLOADS = {
     "cfg5": (256, 1024, 256, 4),
 }
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
-NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_zgemm_traffic_r01.json")
+NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_gemm3m_step_r02.json")
 METRIC = "ms per energy point, fused BTA SI+SQ at 1/2/4/8 B200; % FP64 TC peak"
 
 
@@ -352,7 +352,7 @@ def run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist):
     import paper_2601_04904_b200 as bs
 
     E = args.energies_per_gpu
-    sweep = bs.EnergySweep(n, b, a, "siq", device=dev)
+    sweep = bs.EnergySweep(n, b, a, "siq", device=dev, concurrent=args.energy_concurrent)
     mine = list(range(rank * E, (rank + 1) * E))  # energies of this rank (round robin over 64 = same set)
 
     def step():
@@ -410,7 +410,8 @@ def run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist):
             "data": "synthetic (device splitmix64 generator; energy e = seeds (2e, 2e+1))",
             "config": {"workload": f"cfg5: BASELINE.json configs[{cfg_idx}]", "n_blocks": n, "block": b, "tip": a,
                        "mode": "siq", "energies_per_gpu": E, "energies_per_step": total_e,
-                       "parallelism": f"energy parallel over {world} GPU(s), 2 in-GPU partitions per energy",
+                       "parallelism": f"energy parallel over {world} GPU(s), {sweep.concurrent} energies in flight "
+                                      f"per GPU, 2 in-GPU partitions per energy",
                        "l2": "inputs 28 GiB per energy >> L2"},
             "fp64_tflops_step": tf, "pct_fp64_peak_step": 100.0 * tf / (peak * world), "flops_per_energy": Fx,
             "flops_reference_inventory_per_energy": F,
@@ -451,6 +452,8 @@ def main():
                     help="N>1: partitions per GPU (lanes), plan over N x this many partitions")
     ap.add_argument("--no-other-b", action="store_true",
                     help="skip the general / anti-Hermitian right-hand-side timings")
+    ap.add_argument("--energy-concurrent", type=int, default=None,
+                    help="cfg5: energies in flight per GPU (default: 2 when they fit)")
     ap.add_argument("--energies-per-gpu", type=int, default=8,
                     help="cfg5: energy points per GPU per step (64 energies on 8 GPUs)")
     args = ap.parse_args()
@@ -712,14 +715,16 @@ def main():
                                                            "implementation executes far fewer flops",
                          "executed_over_inventory": executed / F,
                          "algorithmic_over_inventory": algorithmic / F,
-                         # DRAM bytes per launch of this kernel from one ncu --set full capture of all
-                         # its launches in a cfg4-shaped solve (profiles/ncu_zgemm_traffic_r01.json)
-                         "traffic": ncu["dram_bytes_per_launch"] if ncu else None,
+                         # DRAM bytes per launch of this kernel from one ncu --set full capture of its
+                         # launches in the two-lane cfg4-shaped step (profiles/ncu_gemm3m_step_r02.json)
+                         "traffic": ncu["mean"]["dram_bytes"] if ncu else None,
                          "traffic_source": ("ncu --set full, " + ncu["target"]) if ncu else None,
                          # every operand read once + outputs written once, live over this step's launches
                          "compulsory_bytes_per_launch": (prof.gemm_bytes / prof.gemm_launches
                                                          if prof.gemm_launches else None),
-                         "traffic_over_compulsory": ncu["traffic_over_compulsory"] if ncu else None,
+                         "traffic_over_compulsory": (ncu["mean"]["dram_bytes"] / (prof.gemm_bytes / prof.gemm_launches)
+                                                     if ncu and prof.gemm_launches else None),
+                         "ncu_dmma_pct_of_peak_active": ncu["mean"]["dmma_inst_pct_of_peak_active"] if ncu else None,
                          "peak_source": peak_src,
                          # busy share of the instrumented step (rank 0)
                          "share_of_step": prof.gemm_busy_ms / prof_ms if prof_ms else None,

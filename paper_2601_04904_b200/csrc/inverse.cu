@@ -340,6 +340,9 @@ constexpr int kLeafThreads = 256;
 
 constexpr int kT = 32;
 constexpr int kTLD = kT + 2;  // 544-byte rows: conflict-free DMMA fragment loads
+// largest |re| + |im| of a block Gauss-Jordan multiplier accepted without the
+// exact fallback (threshold pivoting with tau ~ 1/16)
+constexpr double kMultMax = 16.0;
 
 // Operand tiles double buffered: the next tile's loads fly while the
 // current one computes (3 buffers, or the addend tile via smem, measured
@@ -487,6 +490,7 @@ struct TileCtx {
   bool keep;        // lookahead tile: also leave the result in S.r for the leaf
   int r_tk;  // column tile whose R = Dinv W[J,K] is cached in S.r
   unsigned long long* trace;  // debug (may be null)
+  int* flag;  // exact-fallback request (growth check, below)
   __device__ int quad(int ti, int tk) const { return 2 * (ti / ntq) + (tk / ntq); }
   __device__ int ext(int t) const { return min(kT, b - (t % ntq) * kT); }  // valid rows / cols of tile t
   __device__ double2* at(const Quad* Q, int ti, int tk) const {
@@ -567,6 +571,19 @@ __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int
     return;
   }
   tile_mma(acc, S.c[buf], tk == p ? S.d : S.r);
+  if (tk == p && ti > p && q == 0) {
+    // Growth check (threshold pivoting): acc = W[I,p] Dinv_p are the
+    // multipliers of rows not yet pivotal (pivot candidates of a full-column
+    // search) against this panel's in-tile pivots.  Partial pivoting keeps
+    // them <= 1; if any exceeds kMultMax the in-tile pivot was small for its
+    // column and the exact full-column partial-pivoting inverse takes over
+    // (same flag as an exactly zero leaf pivot).  Diagonally dominant pivots
+    // (the RGF recursion's) give multipliers << 1.
+    bool big = false;
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn) big |= fabs(acc[jn][0]) + fabs(acc[jn][1]) > kMultMax;
+    if (__syncthreads_or(big) && threadIdx.x == 0) atomicMax(T.flag, 1);
+  }
   if (T.keep) {  // the next leaf reads this tile from shared memory, not back through L2
     __syncthreads();  // every warp is done reading S.r
 #pragma unroll
@@ -677,6 +694,7 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
   TileCtx T;
   T.keep = false;
   T.trace = g.trace;
+  T.flag = g.flag;
   T.b = b;
   T.ntq = ntq;
   T.nt = nt;

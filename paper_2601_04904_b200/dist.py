@@ -489,12 +489,12 @@ def assemble_reduced(coll: Collectives, a, b, plan: PartitionPlan, payload: Boun
     return reduced if isinstance(a, DeviceBta) else reduced.to_host()
 
 
-def solve_reduced(reduced: ReducedSystem, mode: str, counter=None, recursive_parts=None):
+def solve_reduced(reduced: ReducedSystem, mode: str, counter=None, recursive_parts=None, *, _pipe=0):
     """Solve the replicated reduced system (dist.py:507-523) on the GPU."""
     if recursive_parts and reduced.matrix_a.n >= 2 * recursive_parts:
         return dist_solve(reduced.matrix_a, reduced.matrix_b, num_parts=recursive_parts, mode=mode)
     return solve_selected(reduced.matrix_a, reduced.matrix_b if mode == "siq" else None, mode, counter=counter,
-                          _b_symmetry=reduced.b_symmetry)
+                          _b_symmetry=reduced.b_symmetry, _pipe=_pipe)
 
 
 def local_backward(a, b, plan: PartitionPlan, rank: int, factors: LocalFactors, reduced: ReducedSystem,
@@ -636,9 +636,10 @@ class _Lanes:
     thread; the lanes start after, and the caller's stream waits for, all
     work previously queued on the caller's stream."""
 
-    def __init__(self, device, count):
+    def __init__(self, device, count, base=0):
         self.device = device
         self.count = count
+        self.base = base  # lane contexts base .. base + count - 1 (concurrent runners use disjoint lanes)
         self.streams = [torch.cuda.Stream(device) for _ in range(count)]
         # Concurrent chains share the SMs: each block inverse gets fewer CTAs
         # (cfg4, 2 lanes, current sweeps: 32 / 36 / 40 / 44 / 48 / 64 CTAs ->
@@ -659,7 +660,7 @@ class _Lanes:
             try:
                 with torch.cuda.device(self.device), torch.cuda.stream(self.streams[rank]):
                     self.streams[rank].wait_event(start)
-                    ctx = _native.Context.get(self.device.index, lane=rank)
+                    ctx = _native.Context.get(self.device.index, lane=self.base + rank)
                     ctx.set_inverse_grid(self.inverse_grid)
                     ctx.set_aux_avoid_sms(self.avoid_sms)
                     try:
@@ -769,7 +770,7 @@ class InGpuPartitions:
     latency-bound chain of a single sweep leaves idle.  Factor buffers are
     kept between runs for repeated solves of one shape."""
 
-    def __init__(self, shape, mode, parts, device, plan=None, local=None):
+    def __init__(self, shape, mode, parts, device, plan=None, local=None, lane_base=0, pipe=0):
         """``local``: the partition indices this process runs (default: all
         ``parts``, the single-GPU scheme); with a subset -- k partitions per
         GPU of a multi-GPU job -- ``run`` needs a hub that exchanges with the
@@ -780,7 +781,8 @@ class InGpuPartitions:
         self.device = device
         self.plan = plan or plan_partitions(self.n, parts, mode)
         self.local = list(range(parts)) if local is None else list(local)
-        self.lanes = _Lanes(device, len(self.local))
+        self.lanes = _Lanes(device, len(self.local), base=lane_base)
+        self.pipe = pipe  # the reduced solve's context (concurrent runners: disjoint)
         self._factors = [None] * len(self.local)
         self.chunk = None
         self.copy_stream = torch.cuda.Stream(device)  # shared by the partitions' input chunks
@@ -829,7 +831,7 @@ class InGpuPartitions:
         self.reduced = reduced = _assemble(gathered, A, B, plan, tip_sum)
         tm.stop("communication")
         tm.start("reduced")
-        red_sol = solve_reduced(reduced, mode, None, recursive_parts)
+        red_sol = solve_reduced(reduced, mode, None, recursive_parts, _pipe=self.pipe)
         tm.stop("reduced")
         tm.start("backward")
         if out is None:

@@ -40,55 +40,124 @@ def rank_energies(energies, world: int, rank: int):
 class EnergySweep:
     """Solve many energy points of one shape on one GPU with preallocated
     buffers; ``run`` calls ``consume(e, solution)`` after each energy (the
-    solution's device buffers are reused by the next energy)."""
+    solution's device buffers are reused by that pipe's next energy).
+
+    ``concurrent`` = number of energies in flight on the GPU (pipes).  Each
+    pipe owns its input / output buffers, its partition runner (factor
+    buffers) and lane contexts, and runs in its own host thread on its own
+    streams; energies go to the pipes round robin.  The forward sweeps are
+    bound by their Schur chains (latency), the backward sweeps by the tensor
+    pipe (throughput), so a second energy in flight fills the SMs the first
+    one's chains leave idle.  None = 2 when the buffers fit in device memory
+    (config 5: ~84 GiB per pipe), else 1.  With one pipe, the next energy's
+    inputs are generated on a side stream while the current one solves."""
 
     def __init__(self, n: int, b: int, a: int, mode: str = "siq", device=None, partitions=None,
-                 dominance: float = 1.5):
+                 dominance: float = 1.5, concurrent: int | None = None):
         self.n, self.b, self.a, self.mode = n, b, a, mode
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.parts = default_partitions(n) if partitions is None else partitions
         self.dominance = dominance
         fused = mode == "siq"
+        if concurrent is None:
+            concurrent = 2 if self._fits(2) else 1
+        self.concurrent = int(concurrent)
         mk = lambda: DeviceBta.empty(n, b, a, self.device, zero=False)  # noqa: E731
-        self.inputs = [(mk(), mk() if fused else None) for _ in range(2)]
-        self.out = (mk(), mk() if fused else None)
-        self.gen_stream = torch.cuda.Stream(self.device)
-        self._free = [None, None]  # event: input slot no longer read by a solve
+        # one pipe: two input slots (generation overlapped with the solve);
+        # several pipes: one input slot each (the other pipe's solve overlaps it)
+        nin = 2 if self.concurrent == 1 else 1
+        self.pipes = []
+        for _ in range(self.concurrent):
+            self.pipes.append({"inputs": [(mk(), mk() if fused else None) for _ in range(nin)],
+                               "out": (mk(), mk() if fused else None),
+                               "gen": torch.cuda.Stream(self.device), "stream": torch.cuda.Stream(self.device),
+                               "free": [None] * nin})
+        # single-pipe aliases (round-1 attribute names)
+        self.inputs, self.out = self.pipes[0]["inputs"], self.pipes[0]["out"]
+        self.gen_stream = self.pipes[0]["gen"]
 
-    def _generate(self, e: int, slot: int) -> torch.cuda.Event:
-        A, B = self.inputs[slot]
+    def _fits(self, k: int) -> bool:
+        """Device memory for k pipes: inputs + outputs + the partition runner's
+        factors (~5 b x b blocks per diagonal block) + working strips, x 1.1."""
+        n, b, a = self.n, self.b, self.a
+        blocks = 16 * (n * b * b + 2 * (n - 1) * b * b + 2 * n * a * b + a * a)
+        fac = 16 * n * (6 * b * b + 4 * a * b)
+        need = k * (4 * blocks + fac) * 1.1
+        free, _ = torch.cuda.mem_get_info(self.device)
+        return need < free
+
+    def _generate(self, pipe, e: int, slot: int) -> torch.cuda.Event:
+        A, B = pipe["inputs"][slot]
         sa, sb = energy_seeds(e)
-        with torch.cuda.device(self.device), torch.cuda.stream(self.gen_stream):
-            if self._free[slot] is not None:
-                self.gen_stream.wait_event(self._free[slot])
+        g = pipe["gen"]
+        with torch.cuda.device(self.device), torch.cuda.stream(g):
+            if pipe["free"][slot] is not None:
+                g.wait_event(pipe["free"][slot])
             generate_dd_bta_device(self.n, self.b, self.a, sa, self.dominance, out=A)
             if B is not None:
                 hermitianize_device(generate_dd_bta_device(self.n, self.b, self.a, sb, self.dominance, out=B))
             ready = torch.cuda.Event()
-            ready.record(self.gen_stream)
+            ready.record(g)
         return ready
 
+    def _run_pipe(self, p: int, energies, consume, timings, lock):
+        pipe = self.pipes[p]
+        nin = len(pipe["inputs"])
+        main = pipe["stream"]
+        with torch.cuda.device(self.device), torch.cuda.stream(main):
+            main.wait_stream(self._caller)
+            ready = self._generate(pipe, energies[0], 0)
+            for k, e in enumerate(energies):
+                slot = k % nin
+                nxt = None
+                if k + 1 < len(energies) and nin > 1:  # overlap the next energy's inputs with this solve
+                    nxt = self._generate(pipe, energies[k + 1], (k + 1) % nin)
+                main.wait_event(ready)
+                A, B = pipe["inputs"][slot]
+                sol = solve_selected(A, B, self.mode, out=pipe["out"], partitions=self.parts, timings=timings,
+                                     _pipe=p)
+                done = torch.cuda.Event()
+                done.record(main)
+                pipe["free"][slot] = done
+                if consume is not None:
+                    with lock:
+                        consume(e, sol)
+                if k + 1 < len(energies):
+                    ready = nxt if nxt is not None else self._generate(pipe, energies[k + 1], (k + 1) % nin)
+
     def run(self, energies, consume=None, timings=None):
-        """Solve ``energies`` in order; returns the number solved."""
+        """Solve ``energies``; returns the number solved.  With several pipes,
+        ``consume`` is called from the pipes' threads (serialised by a lock),
+        in each pipe's energy order."""
+        import threading
+
         energies = list(energies)
         if not energies:
             return 0
-        main = torch.cuda.current_stream(self.device)
-        ready = self._generate(energies[0], 0)
-        for k, e in enumerate(energies):
-            slot = k & 1
-            if k + 1 < len(energies):  # overlap the next energy's inputs with this solve
-                nxt = self._generate(energies[k + 1], slot ^ 1)
-            main.wait_event(ready)
-            A, B = self.inputs[slot]
-            sol = solve_selected(A, B, self.mode, out=self.out, partitions=self.parts, timings=timings)
-            done = torch.cuda.Event()
-            done.record(main)
-            self._free[slot] = done
-            if consume is not None:
-                consume(e, sol)
-            if k + 1 < len(energies):
-                ready = nxt
+        self._caller = torch.cuda.current_stream(self.device)
+        lock = threading.Lock()
+        k = min(self.concurrent, len(energies))
+        shares = [energies[p::k] for p in range(k)]
+        if k == 1:
+            self._run_pipe(0, shares[0], consume, timings, lock)
+        else:
+            errors = []
+
+            def work(p):
+                try:
+                    self._run_pipe(p, shares[p], consume, None, lock)
+                except BaseException as exc:  # noqa: BLE001 - re-raised below
+                    errors.append(exc)
+
+            threads = [threading.Thread(target=work, args=(p,)) for p in range(k)]
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join()
+            if errors:
+                raise errors[0]
+        for p in range(k):
+            self._caller.wait_stream(self.pipes[p]["stream"])
         return len(energies)
 
 

@@ -67,9 +67,12 @@ def _check_mode(a, b, mode):
     return mode
 
 
-def _ctx_for(x):
+def _ctx_for(x, pipe=0):
+    """Native context of the device holding x (the current device for host
+    inputs); ``pipe`` > 0 (concurrent solves of EnergySweep) selects a lane
+    of its own."""
     dev = x.device.index if isinstance(x, DeviceBta) else None
-    ctx = _native.Context.get(dev)
+    ctx = _native.Context.get(dev, lane=0 if pipe == 0 else 1000 + pipe)
     return ctx, torch.device("cuda", ctx.device)
 
 
@@ -289,7 +292,7 @@ def release_caches() -> None:
 
 def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal_only=False,
                    out=None, workspace=None, partitions=None, _b_symmetry=None, _device_in=None,
-                   _io_events=None) -> SelectedSolution:
+                   _io_events=None, _pipe=0) -> SelectedSolution:
     """Selected inverse of ``a`` and, in fused mode, the selected quadratic
     solution for ``b`` (rgf.py:497-531).  Never mutates its inputs.
 
@@ -312,8 +315,8 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
     parts = default_partitions(n) if partitions is None else int(partitions)
     if parts > 1 and n >= 2 * parts:
         return _solve_partitioned(a, b if fused else None, mode, parts, counter, timings, diagonal_only, out,
-                                  _device_in, _io_events)
-    ctx, device = _ctx_for(a)
+                                  _device_in, _io_events, _pipe)
+    ctx, device = _ctx_for(a, _pipe)
     host = not isinstance(a, DeviceBta)
     A = DeviceBta.empty(n, bs, asz, device, zero=False).copy_from_host(a) if host else a
     B = None
@@ -371,7 +374,8 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
     return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
 
 
-def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, device_in=None, io_events=None):
+def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, device_in=None, io_events=None,
+                       pipe=0):
     """solve_selected through InGpuPartitions (dist.py) with cached buffers.
 
     ``device_in`` (internal, HostEnergySweep): device storage for streamed
@@ -398,10 +402,13 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, 
         B = b if not host else (dev_in[1] if dev_in else DeviceBta.empty(n, bs, asz, device, zero=False))
         if host and not stream_in:
             B.copy_from_host(b)
-    key = (device.index, n, bs, asz, mode, parts)
+    # pipe (internal, EnergySweep concurrency): concurrent solves need their own
+    # runner (factor buffers) and lane contexts
+    key = (device.index, n, bs, asz, mode, parts, pipe)
     runner = _PARTITIONED.get(key)
     if runner is None:
-        runner = _PARTITIONED[key] = InGpuPartitions((n, bs, asz), mode, parts, device)
+        runner = _PARTITIONED[key] = InGpuPartitions((n, bs, asz), mode, parts, device, lane_base=pipe * parts,
+                                                     pipe=pipe)
     dev_out = out if (out is not None and isinstance(out[0], DeviceBta)) else None
     if stream_in or stream_out:
         XA, XB = runner.run(A, B, out=dev_out, host_in=(a, b) if stream_in else None,

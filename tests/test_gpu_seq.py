@@ -78,6 +78,21 @@ def test_block_inverse_needs_pivoting(n):
     assert np.linalg.norm(x @ got - np.eye(n)) / np.sqrt(n) <= 1e-10
 
 
+@pytest.mark.parametrize("n", [64, 96, 512])
+def test_block_inverse_small_in_tile_pivot(n):
+    """A nonsingular block whose leading 32-row tile has only tiny entries in
+    its first columns while rows below hold O(1) ones: pivoting inside the
+    diagonal tile alone would pick a ~1e-12 pivot (growth 1e12); the growth
+    check (block multipliers > 16) hands the block to the exact full-column
+    partial-pivoting inverse -> LAPACK accuracy."""
+    x = crand(n, n)
+    x[:32, :4] *= 1e-12
+    got = bs.block_inverse(x)
+    ref = np.linalg.inv(x)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert np.linalg.norm(x @ got - np.eye(n)) / np.sqrt(n) <= 1e-9
+
+
 def test_block_inverse_singular_reports_row():
     x = np.eye(4, dtype=np.complex128)
     x[2, :] = 0.0
