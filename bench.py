@@ -352,7 +352,8 @@ def run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist):
     import paper_2601_04904_b200 as bs
 
     E = args.energies_per_gpu
-    sweep = bs.EnergySweep(n, b, a, "siq", device=dev, concurrent=args.energy_concurrent)
+    sweep = bs.EnergySweep(n, b, a, "siq", device=dev, concurrent=args.energy_concurrent or 1,
+                           overlap=False if args.no_energy_overlap else None)
     mine = list(range(rank * E, (rank + 1) * E))  # energies of this rank (round robin over 64 = same set)
 
     def step():
@@ -410,8 +411,9 @@ def run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist):
             "data": "synthetic (device splitmix64 generator; energy e = seeds (2e, 2e+1))",
             "config": {"workload": f"cfg5: BASELINE.json configs[{cfg_idx}]", "n_blocks": n, "block": b, "tip": a,
                        "mode": "siq", "energies_per_gpu": E, "energies_per_step": total_e,
-                       "parallelism": f"energy parallel over {world} GPU(s), {sweep.concurrent} energies in flight "
-                                      f"per GPU, 2 in-GPU partitions per energy",
+                       "parallelism": f"energy parallel over {world} GPU(s), 2 in-GPU partitions per energy, "
+                                      + ("energy k+1's forward overlapped with energy k's backward" if sweep.overlap
+                                         else f"{sweep.concurrent} energy pipe(s) per GPU"),
                        "l2": "inputs 28 GiB per energy >> L2"},
             "fp64_tflops_step": tf, "pct_fp64_peak_step": 100.0 * tf / (peak * world), "flops_per_energy": Fx,
             "flops_reference_inventory_per_energy": F,
@@ -453,7 +455,9 @@ def main():
     ap.add_argument("--no-other-b", action="store_true",
                     help="skip the general / anti-Hermitian right-hand-side timings")
     ap.add_argument("--energy-concurrent", type=int, default=None,
-                    help="cfg5: energies in flight per GPU (default: 2 when they fit)")
+                    help="cfg5: independent energy pipes per GPU (default 1)")
+    ap.add_argument("--no-energy-overlap", action="store_true",
+                    help="cfg5: no overlap of energy k+1's forward with energy k's backward")
     ap.add_argument("--energies-per-gpu", type=int, default=8,
                     help="cfg5: energy points per GPU per step (64 energies on 8 GPUs)")
     args = ap.parse_args()

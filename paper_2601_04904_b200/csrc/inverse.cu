@@ -1,6 +1,7 @@
 // Complex128 block inverse (see inverse.cuh).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "inverse.cuh"
 #include "zgemm.cuh"
@@ -52,6 +53,8 @@ struct Leaf32 {
   double2 pan[2][32][kPanLd];         // current sub-panel, double buffered
   double2 prow[kSub][3][kSub];        // pivot rows of the other three sub-panels
   int piv[32];
+  int rowstep[32];                    // warp leaf: step of the sub-panel row i was pivot of, else -1
+  int pstep[kSub];                    // warp leaf: pivot row of each step of the sub-panel
 };
 
 __device__ bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
@@ -153,6 +156,112 @@ __device__ bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
 }
 
 
+// The same elimination with each sub-panel's 8 pivot steps done by ONE warp
+// in registers: lane r holds row r of the 32 x 8 sub-panel, the pivot search
+// is a redux/ballot over the lanes, the pivot row and its reciprocal travel
+// by shuffles -- no shared memory and no CTA barrier inside the 8 steps.
+// Per sub-panel the CTA publishes the whole tile (one barrier), warp 0 runs
+// the steps and writes the sub-panel and its pivots back (one barrier), and
+// every thread applies the sub-panel to its entries of the other columns as
+// the blocked leaf does (x' = zero_rows_P(x) + W x[P], the pivot rows read
+// from the published tile), then a barrier before the next publish.
+// Identical pivots and arithmetic per entry as gj_leaf32 (bitwise equal
+// results up to the order of the lazy-update sums, which is also the same).
+__device__ bool gj_leaf32_warp(Leaf32& L, int n) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int i = t >> 3, cl = t & 7;
+  double2 v[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int c = cl + kSub * s;
+    v[s] = (i < n && c < n) ? L.a[i][c] : make_double2(0.0, 0.0);
+  }
+  bool used = false;  // warp 0: row `lane` already pivotal
+  bool any_zero = false;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int k0 = kSub * s;
+    if (k0 >= n) break;
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) L.a[i][cl + kSub * s2] = v[s2];
+    __syncthreads();
+    const int steps = min(kSub, n - k0);
+    if (warp == 0) {
+      double2 w[kSub];
+#pragma unroll
+      for (int c = 0; c < kSub; ++c) w[c] = L.a[lane][k0 + c];
+      int myj = -1;
+#pragma unroll
+      for (int j = 0; j < kSub; ++j) {
+        if (j >= steps) break;
+        const double2 cv = w[j];
+        const bool cand = lane < n && !used;
+        const unsigned key = cand ? (unsigned)__double2hiint(cabs1(cv)) + 1u : 0u;
+        const double2 rl = crecip_fast(cv);  // speculative: every lane inverts its candidate
+        const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+        const unsigned ball = __ballot_sync(0xffffffffu, cand && key == kmax);
+        const int p = __ffs(ball) - 1;
+        const bool zero = kmax <= 1u;
+        any_zero |= zero;
+        const bool me = lane == p;
+        used |= me;
+        if (me) myj = j;
+        if (lane == 0) {
+          L.piv[k0 + j] = p;
+          L.pstep[j] = p;
+        }
+        const double2 rp = make_double2(__shfl_sync(0xffffffffu, rl.x, p), __shfl_sync(0xffffffffu, rl.y, p));
+        const double2 inv = zero ? make_double2(1.0, 0.0) : rp;
+        const double2 m = cmul(cv, inv);
+        const double2 coef = me ? inv : make_double2(-m.x, -m.y);
+#pragma unroll
+        for (int c = 0; c < kSub; ++c) {
+          // pivot row entry by shuffle (independent across c: the shuffles pipeline)
+          const double2 pr = make_double2(__shfl_sync(0xffffffffu, w[c].x, p), __shfl_sync(0xffffffffu, w[c].y, p));
+          const double bx = me ? 0.0 : w[c].x, by = me ? 0.0 : w[c].y;
+          double2 nv;
+          nv.x = fma(coef.x, pr.x, fma(-coef.y, pr.y, bx));
+          nv.y = fma(coef.x, pr.y, fma(coef.y, pr.x, by));
+          w[c] = c == j ? coef : nv;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kSub; ++c) L.pan[0][lane][c] = w[c];
+      L.rowstep[lane] = myj;
+    }
+    __syncthreads();
+    // lazy update of the other sub-panels: x' = zero_rows_P(x) + W x[P]
+    const int jp = L.rowstep[i];
+    double2 w[kSub];
+#pragma unroll
+    for (int j = 0; j < kSub; ++j) w[j] = L.pan[0][i][j];
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) {
+      if (s2 == s) continue;
+      double2 acc = jp >= 0 ? make_double2(0.0, 0.0) : v[s2];
+#pragma unroll
+      for (int j = 0; j < kSub; ++j) {
+        if (j >= steps) break;
+        const double2 x = L.a[L.pstep[j]][cl + kSub * s2];
+        acc.x = fma(w[j].x, x.x, fma(-w[j].y, x.y, acc.x));
+        acc.y = fma(w[j].x, x.y, fma(w[j].y, x.x, acc.y));
+      }
+      if (i < n && cl + kSub * s2 < n) v[s2] = acc;
+    }
+    if (i < n && cl + k0 < n) v[s] = L.pan[0][i][cl];
+    __syncthreads();  // L.a / L.pan are rewritten by the next sub-panel
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) L.a[i][cl + kSub * s] = v[s];
+  __syncthreads();
+  return __shfl_sync(0xffffffffu, (int)any_zero, 0) != 0;  // warp 0's verdict (thread 0 reports it)
+}
+
+// BSEL_LEAF=8warp selects the round-1 CTA-wide leaf.
+__device__ __forceinline__ bool leaf32(Leaf32& L, int n, bool warp_leaf) {
+  return warp_leaf ? gj_leaf32_warp(L, n) : gj_leaf32(L, n);
+}
+
 // One CTA (256 threads) per matrix, n <= 32.
 __global__ void __launch_bounds__(256)
     leaf_inverse_kernel(const double2* __restrict__ X, int64_t ldx, int64_t sx, double2* __restrict__ Y,
@@ -167,7 +276,7 @@ __global__ void __launch_bounds__(256)
     if (i < n && j < n) L.a[i][j] = X[(int64_t)i * ldx + j];
   }
   __syncthreads();
-  const bool any_zero = gj_leaf32(L, n);
+  const bool any_zero = gj_leaf32_warp(L, n);
   if (tid == 0 && any_zero) atomicMax(flag, 1);
   const double2 (*S)[33] = L.a;
   for (int e = tid; e < 32 * 32; e += 256) {
@@ -433,13 +542,14 @@ __device__ __forceinline__ int acc_col(int jn) { return ((threadIdx.x >> 5) >> 2
 
 // CTA-wide: invert the diagonal tile W[j0:j0+jb, j0:j0+jb] and publish the
 // zero-padded 32 x 32 Dinv to gDp.
-__device__ void leaf_publish(Leaf32& L, const double2* W, int64_t ld, int j0, int jb, double2* gDp, int* flag) {
+__device__ void leaf_publish(Leaf32& L, const double2* W, int64_t ld, int j0, int jb, double2* gDp, int* flag,
+                             bool warp_leaf) {
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int i = e >> 5, j = e & 31;
     L.a[i][j] = (i < jb && j < jb) ? ldcg2(W + (int64_t)(j0 + i) * ld + j0 + j) : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const bool zero = gj_leaf32(L, jb);
+  const bool zero = leaf32(L, jb, warp_leaf);
   if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
   const double2 (*S)[33] = L.a;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
@@ -462,13 +572,14 @@ struct Quad {
 };
 
 // As leaf_publish, with the diagonal tile already in shared memory.
-__device__ void leaf_publish_smem(Leaf32& L, const double2 (*src)[kTLD], int jb, double2* gDp, int* flag) {
+__device__ void leaf_publish_smem(Leaf32& L, const double2 (*src)[kTLD], int jb, double2* gDp, int* flag,
+                                  bool warp_leaf) {
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int i = e >> 5, j = e & 31;
     L.a[i][j] = (i < jb && j < jb) ? src[i][j] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const bool zero = gj_leaf32(L, jb);
+  const bool zero = leaf32(L, jb, warp_leaf);
   if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
   const double2 (*Sx)[33] = L.a;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
@@ -666,6 +777,7 @@ __device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
 struct GjArgs {
   Quad in, out, a, bq;
   int b, nq;
+  int warp_leaf;  // 1: gj_leaf32_warp (default), 0: the CTA-wide leaf (BSEL_LEAF=8warp)
   double2* gD;
   unsigned* barrier;
   int* flag;
@@ -688,7 +800,7 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
   Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0][0]);  // spans x[0] and x[1]
   const int b = g.b, ntq = (b + kT - 1) / kT, nt = g.nq * ntq, ntiles = nt * nt, G = gridDim.x;
   unsigned target = 0;
-  if (blockIdx.x == 0) leaf_publish(L, g.in.p[0], g.in.ld[0], 0, min(kT, b), g.gD, g.flag);
+  if (blockIdx.x == 0) leaf_publish(L, g.in.p[0], g.in.ld[0], 0, min(kT, b), g.gD, g.flag, g.warp_leaf != 0);
   target += G;
   grid_barrier(g.barrier, target);
   TileCtx T;
@@ -721,7 +833,8 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
       T.r_tk = -1;  // S.r now holds the tile, not an R
       __syncthreads();
       stamp(8 * p + 1);
-      leaf_publish_smem(L, S.r, min(kT, b - (p + 1) * kT), g.gD + ((p + 1) & 1) * kT * kT, g.flag);
+      leaf_publish_smem(L, S.r, min(kT, b - (p + 1) * kT), g.gD + ((p + 1) & 1) * kT * kT, g.flag,
+                        g.warp_leaf != 0);
       stamp(8 * p + 2);
     }
     if (G == 1 || blockIdx.x > 0) {
@@ -893,6 +1006,11 @@ Quad quad1(const double2* p, int64_t ld) {
 }
 
 cudaError_t launch_gj(GjArgs& g, int grid, cudaStream_t stream) {
+  static const int warp_leaf = [] {
+    const char* e = getenv("BSEL_LEAF");
+    return (e && std::string(e) == "8warp") ? 0 : 1;
+  }();
+  g.warp_leaf = warp_leaf;
   if ((cudaError_t)cudaMemsetAsync(g.barrier, 0, sizeof(unsigned), stream) != cudaSuccess) return cudaGetLastError();
   // The CTAs wait on one another (grid barrier), so the launch is
   // cooperative: co-residency of the whole grid is guaranteed.  Cooperative

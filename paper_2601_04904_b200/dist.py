@@ -797,6 +797,16 @@ class InGpuPartitions:
         only provide device storage for the couplings and the tip);
         ``host_out`` = (x_a, x_b) host BtaMatrix receiving the solution,
         streamed out behind the backward sweeps."""
+        st = self.run_forward(A, B, hub=hub, recursive_parts=recursive_parts, host_in=host_in)
+        return self.run_backward(st, out=out, host_out=host_out)
+
+    def run_forward(self, A, B, hub=None, recursive_parts=None, host_in=None) -> dict:
+        """Forward half of ``run``: the partitions' eliminations, the exchange
+        and the reduced solve.  Returns the state ``run_backward`` consumes;
+        this runner's factor buffers stay in use until that backward ran
+        (EnergySweep overlaps one energy's backward with the next energy's
+        forward on a second runner).  Blocks the host until the reduced
+        solve is done."""
         plan, parts, mode = self.plan, self.parts, self.mode
         B = B if mode == "siq" else None
         # Chunk of the host transfers (blocks): small enough that the first
@@ -833,16 +843,23 @@ class InGpuPartitions:
         tm.start("reduced")
         red_sol = solve_reduced(reduced, mode, None, recursive_parts, _pipe=self.pipe)
         tm.stop("reduced")
+        return {"A": A, "B": B, "results": results, "reduced": reduced, "red_sol": red_sol, "tm": tm,
+                "counters": counters, "chunk": chunk}
+
+    def run_backward(self, st: dict, out=None, host_out=None):
+        """Backward half of ``run`` (enqueues the back-substitutions; returns
+        without waiting for the GPU)."""
+        A, B, results, tm, loc = st["A"], st["B"], st["results"], st["tm"], self.local
         tm.start("backward")
         if out is None:
             out = (DeviceBta.empty(A.n, A.b, A.a, self.device),
                    DeviceBta.empty(A.n, A.b, A.a, self.device) if B is not None else None)
         io_out = None
         if host_out is not None:
-            io_out = _host_io(chunk, x_a=host_out[0], x_b=host_out[1] if B is not None else None)
+            io_out = _host_io(st["chunk"], x_a=host_out[0], x_b=host_out[1] if B is not None else None)
         errors = self.lanes.run(lambda lane, ctx: local_backward(
-            A, B, plan, loc[lane], results[lane][2], reduced, red_sol, counters[lane], out=out, _ctx=ctx,
-            _sync=io_out))
+            A, B, self.plan, loc[lane], results[lane][2], st["reduced"], st["red_sol"], st["counters"][lane],
+            out=out, _ctx=ctx, _sync=io_out))
         if errors:
             lane, exc = min(errors, key=lambda e: e[0])
             raise WorkerError(loc[lane], exc) from exc

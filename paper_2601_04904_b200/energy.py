@@ -42,26 +42,36 @@ class EnergySweep:
     buffers; ``run`` calls ``consume(e, solution)`` after each energy (the
     solution's device buffers are reused by that pipe's next energy).
 
-    ``concurrent`` = number of energies in flight on the GPU (pipes).  Each
-    pipe owns its input / output buffers, its partition runner (factor
-    buffers) and lane contexts, and runs in its own host thread on its own
-    streams; energies go to the pipes round robin.  The forward sweeps are
-    bound by their Schur chains (latency), the backward sweeps by the tensor
-    pipe (throughput), so a second energy in flight fills the SMs the first
-    one's chains leave idle.  None = 2 when the buffers fit in device memory
-    (config 5: ~84 GiB per pipe), else 1.  With one pipe, the next energy's
-    inputs are generated on a side stream while the current one solves."""
+    Two energies in flight, two ways.  The forward sweeps are bound by their
+    Schur chains (latency), the backward sweeps by the tensor pipe
+    (throughput), so a second energy fills the SMs the first one's chains
+    leave idle:
+
+    * ``overlap`` (default when it fits: config 5 needs ~163 GB): energy
+      k+1's forward runs while energy k's backward does, on a second
+      partition runner, with ONE output set (``_run_overlapped``);
+    * ``concurrent`` = k independent pipes, each with its own input / output
+      buffers, partition runner and lane contexts, in its own host thread on
+      its own streams (energies round robin); needs k full solve footprints,
+      so it only fits for small shapes.
+
+    Otherwise energies solve back to back and the next energy's inputs are
+    generated on a side stream while the current one solves."""
 
     def __init__(self, n: int, b: int, a: int, mode: str = "siq", device=None, partitions=None,
-                 dominance: float = 1.5, concurrent: int | None = None):
+                 dominance: float = 1.5, concurrent: int = 1, overlap: bool | None = None):
         self.n, self.b, self.a, self.mode = n, b, a, mode
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.parts = default_partitions(n) if partitions is None else partitions
         self.dominance = dominance
         fused = mode == "siq"
-        if concurrent is None:
-            concurrent = 2 if self._fits(2) else 1
         self.concurrent = int(concurrent)
+        # overlap: the next energy's forward runs while this energy's backward
+        # does (second partition runner); default when the buffers fit
+        if overlap is None:
+            overlap = self.concurrent == 1 and self.parts > 1 and n >= 2 * self.parts and self._fits_overlap()
+        self.overlap = bool(overlap) and self.parts > 1 and n >= 2 * self.parts
+        self._runners = None
         mk = lambda: DeviceBta.empty(n, b, a, self.device, zero=False)  # noqa: E731
         # one pipe: two input slots (generation overlapped with the solve);
         # several pipes: one input slot each (the other pipe's solve overlaps it)
@@ -76,15 +86,19 @@ class EnergySweep:
         self.inputs, self.out = self.pipes[0]["inputs"], self.pipes[0]["out"]
         self.gen_stream = self.pipes[0]["gen"]
 
-    def _fits(self, k: int) -> bool:
-        """Device memory for k pipes: inputs + outputs + the partition runner's
-        factors (~5 b x b blocks per diagonal block) + working strips, x 1.1."""
+    def _bytes(self):
+        """(one BTA matrix, one partition runner's factors + working strips)."""
         n, b, a = self.n, self.b, self.a
         blocks = 16 * (n * b * b + 2 * (n - 1) * b * b + 2 * n * a * b + a * a)
-        fac = 16 * n * (6 * b * b + 4 * a * b)
-        need = k * (4 * blocks + fac) * 1.1
+        fac = 16 * n * (7 * b * b + 6 * a * b)
+        return blocks, fac
+
+    def _fits_overlap(self) -> bool:
+        """Device memory for the overlapped form: this sweep's two input slots
+        and one output set (allocated below) + a second partition runner."""
+        blocks, fac = self._bytes()
         free, _ = torch.cuda.mem_get_info(self.device)
-        return need < free
+        return (6 * blocks + 2 * fac) * 1.05 < free
 
     def _generate(self, pipe, e: int, slot: int) -> torch.cuda.Event:
         A, B = pipe["inputs"][slot]
@@ -135,6 +149,8 @@ class EnergySweep:
         if not energies:
             return 0
         self._caller = torch.cuda.current_stream(self.device)
+        if self.overlap and self.concurrent == 1:
+            return self._run_overlapped(energies, consume)
         lock = threading.Lock()
         k = min(self.concurrent, len(energies))
         shares = [energies[p::k] for p in range(k)]
@@ -158,6 +174,55 @@ class EnergySweep:
                 raise errors[0]
         for p in range(k):
             self._caller.wait_stream(self.pipes[p]["stream"])
+        return len(energies)
+
+
+    def _run_overlapped(self, energies, consume):
+        """Energy k+1's forward sweeps (chain-bound: the Schur chains leave
+        SMs idle) run while energy k's backward sweeps (tensor-pipe bound)
+        do, on a second partition runner: two energies in flight with one
+        output set.  Per energy: generate into input slot k % 2 (after the
+        backward that read it), forward on runner k % 2, backward into the
+        shared outputs (after the previous energy's outputs were consumed)."""
+        from .dist import InGpuPartitions
+        from .matrix import SelectedSolution
+
+        dev = self.device
+        if self._runners is None:
+            shape = (self.n, self.b, self.a)
+            self._runners = [InGpuPartitions(shape, self.mode, self.parts, dev, lane_base=p * self.parts, pipe=p)
+                             for p in range(2)]
+            self._pstreams = [torch.cuda.Stream(dev) for _ in range(2)]
+        R, S = self._runners, self._pstreams
+        pipe = self.pipes[0]
+        for s_ in S:
+            s_.wait_stream(self._caller)
+
+        def forward(k, ready):
+            with torch.cuda.device(dev), torch.cuda.stream(S[k % 2]):
+                S[k % 2].wait_event(ready)
+                A, B = pipe["inputs"][k % 2]
+                return R[k % 2].run_forward(A, B)
+
+        st = forward(0, self._generate(pipe, energies[0], 0))
+        out_free = None
+        for k, e in enumerate(energies):
+            nxt = self._generate(pipe, energies[k + 1], (k + 1) % 2) if k + 1 < len(energies) else None
+            with torch.cuda.device(dev), torch.cuda.stream(S[k % 2]):
+                if out_free is not None:
+                    S[k % 2].wait_event(out_free)
+                R[k % 2].run_backward(st, out=self.out)
+                done = torch.cuda.Event()
+                done.record(S[k % 2])
+            pipe["free"][k % 2] = done
+            if nxt is not None:
+                st = forward(k + 1, nxt)  # overlaps this backward on the GPU
+            if consume is not None:
+                done.synchronize()
+                consume(e, SelectedSolution(x_a=self.out[0], x_b=self.out[1], mode=self.mode))
+            out_free = done
+        for s_ in S:
+            self._caller.wait_stream(s_)
         return len(energies)
 
 

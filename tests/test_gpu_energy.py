@@ -89,3 +89,22 @@ def test_concurrent_energies_match_individual_solves(parts):
         B = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=sb))
         ref = bs.solve_selected(A, B, "siq", partitions=parts)
         assert xa.equals_exact(bs.to_host(ref.x_a)) and xb.equals_exact(bs.to_host(ref.x_b))
+
+
+def test_overlapped_energies_match_individual_solves():
+    """EnergySweep overlap: energy k+1's forward runs during energy k's
+    backward (second partition runner, one output set); every energy's
+    solution bit-identical to its single solve."""
+    n, b, a = 70, 16, 8
+    sweep = bs.EnergySweep(n, b, a, "siq", overlap=True)
+    assert sweep.overlap
+    got = {}
+    sweep.run([3, 0, 5, 1, 2], consume=lambda e, sol: got.__setitem__(
+        e, (bs.to_host(sol.x_a), bs.to_host(sol.x_b))))
+    assert sorted(got) == [0, 1, 2, 3, 5]
+    for e, (xa, xb) in got.items():
+        sa, sb = bs.energy_seeds(e)
+        A = bs.generate_dd_bta_device(n, b, a, seed=sa)
+        B = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=sb))
+        ref = bs.solve_selected(A, B, "siq")
+        assert xa.equals_exact(bs.to_host(ref.x_a)) and xb.equals_exact(bs.to_host(ref.x_b))
