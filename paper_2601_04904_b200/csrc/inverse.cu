@@ -257,7 +257,7 @@ __device__ bool gj_leaf32_warp(Leaf32& L, int n) {
   return __shfl_sync(0xffffffffu, (int)any_zero, 0) != 0;  // warp 0's verdict (thread 0 reports it)
 }
 
-// BSEL_LEAF=8warp selects the round-1 CTA-wide leaf.
+// BSEL_LEAF=warp selects the warp-resident leaf (experiment, slower).
 __device__ __forceinline__ bool leaf32(Leaf32& L, int n, bool warp_leaf) {
   return warp_leaf ? gj_leaf32_warp(L, n) : gj_leaf32(L, n);
 }
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256)
     if (i < n && j < n) L.a[i][j] = X[(int64_t)i * ldx + j];
   }
   __syncthreads();
-  const bool any_zero = gj_leaf32_warp(L, n);
+  const bool any_zero = gj_leaf32(L, n);
   if (tid == 0 && any_zero) atomicMax(flag, 1);
   const double2 (*S)[33] = L.a;
   for (int e = tid; e < 32 * 32; e += 256) {
@@ -777,7 +777,7 @@ __device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
 struct GjArgs {
   Quad in, out, a, bq;
   int b, nq;
-  int warp_leaf;  // 1: gj_leaf32_warp (default), 0: the CTA-wide leaf (BSEL_LEAF=8warp)
+  int warp_leaf;  // 0: the CTA-wide leaf (default), 1: gj_leaf32_warp (BSEL_LEAF=warp)
   double2* gD;
   unsigned* barrier;
   int* flag;
@@ -1006,9 +1006,12 @@ Quad quad1(const double2* p, int64_t ld) {
 }
 
 cudaError_t launch_gj(GjArgs& g, int grid, cudaStream_t stream) {
+  // The warp-resident leaf (gj_leaf32_warp, BSEL_LEAF=warp) measured SLOWER:
+  // 22.6 vs 11.0 us per 32x32 leaf, 484 vs 304 us per 512 inverse
+  // (tools/inv_micro, profiles/inverse_leaf_r02.md) -- the CTA-wide leaf stays.
   static const int warp_leaf = [] {
     const char* e = getenv("BSEL_LEAF");
-    return (e && std::string(e) == "8warp") ? 0 : 1;
+    return (e && std::string(e) == "warp") ? 1 : 0;
   }();
   g.warp_leaf = warp_leaf;
   if ((cudaError_t)cudaMemsetAsync(g.barrier, 0, sizeof(unsigned), stream) != cudaSuccess) return cudaGetLastError();
