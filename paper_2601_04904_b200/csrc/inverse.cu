@@ -493,7 +493,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target)
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-      if (v < target) __nanosleep(64);
+#ifdef BSEL_BARRIER_SLEEP
+      if (v < target) __nanosleep(BSEL_BARRIER_SLEEP);
+#endif
     } while (v < target);
     __threadfence();
   }
@@ -573,7 +575,7 @@ struct Quad {
 
 // As leaf_publish, with the diagonal tile already in shared memory.
 __device__ void leaf_publish_smem(Leaf32& L, const double2 (*src)[kTLD], int jb, double2* gDp, int* flag,
-                                  bool warp_leaf) {
+                                  bool warp_leaf, double2 (*dsmem)[kTLD] = nullptr) {
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int i = e >> 5, j = e & 31;
     L.a[i][j] = (i < jb && j < jb) ? src[i][j] : make_double2(0.0, 0.0);
@@ -584,10 +586,10 @@ __device__ void leaf_publish_smem(Leaf32& L, const double2 (*src)[kTLD], int jb,
   const double2 (*Sx)[33] = L.a;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int r = e >> 5, k = e & 31;
-    if (r < jb && k < jb)
-      gDp[r * kT + L.piv[k]] = Sx[L.piv[r]][k];
-    else
-      gDp[r * kT + k] = make_double2(0.0, 0.0);
+    const int c = (r < jb && k < jb) ? L.piv[k] : k;
+    const double2 v = (r < jb && k < jb) ? Sx[L.piv[r]][k] : make_double2(0.0, 0.0);
+    gDp[r * kT + c] = v;
+    if (dsmem) dsmem[r][c] = v;  // the publishing CTA keeps its copy (no reload through L2)
   }
   __syncthreads();
 }
@@ -822,7 +824,9 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
     // every leaf (the last one was factored during panel ntq-2) has reported
     T.skip_c = T.final_ && g.nq == 2 && *reinterpret_cast<volatile int*>(g.flag) != 0;
     T.r_tk = -1;
-    load_tile(S.d, g.gD + (p & 1) * kT * kT, kT, kT, kT);
+    // CTA 0 (with other CTAs updating the tiles) already holds Dinv_p in
+    // S.d: it factored the leaf itself (lookahead) and kept the result
+    if (!(blockIdx.x == 0 && G > 1 && p > 0)) load_tile(S.d, g.gD + (p & 1) * kT * kT, kT, kT, kT);
     __syncthreads();
     const int sp = (p + 1 < ntq) ? (p + 1) * nt + (p + 1) : -1;
     if (blockIdx.x == 0) stamp(8 * p + 0);
@@ -833,8 +837,10 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
       T.r_tk = -1;  // S.r now holds the tile, not an R
       __syncthreads();
       stamp(8 * p + 1);
+      // S.d is free once the lookahead tile is done (CTA 0 updates no other
+      // tiles when G > 1): keep Dinv_{p+1} there for the next panel
       leaf_publish_smem(L, S.r, min(kT, b - (p + 1) * kT), g.gD + ((p + 1) & 1) * kT * kT, g.flag,
-                        g.warp_leaf != 0);
+                        g.warp_leaf != 0, G > 1 ? S.d : nullptr);
       stamp(8 * p + 2);
     }
     if (G == 1 || blockIdx.x > 0) {

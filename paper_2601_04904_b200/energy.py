@@ -314,12 +314,12 @@ class HostEnergySweep:
         in_free = [None, None]  # event: solve no longer reads the input slot
         out_free = [None, None]  # event: D2H of the output slot finished
         # The partitioned solve streams host inputs in behind its forward
-        # sweeps: with out_slots=1 the first energy uses that (no
-        # unoverlapped fill), and the second energy's load starts once the
-        # first's inputs are in.  With out_slots=2 (device outputs) the
-        # streamed first energy measured 8.5 s at config 4 instead of ~1.1 s
-        # (tools/e2e_probe.py; next round), so it is loaded whole.
-        stream_first = (self.parts > 1 and self.n >= 2 * self.parts and self.out is None
+        # sweeps: the first energy uses that (no unoverlapped fill), and the
+        # second energy's load starts once the first's inputs are in.  (Round
+        # 1 measured 8.5 s for a streamed first energy with device outputs:
+        # solve_selected copied the caller's device outputs to pageable host
+        # memory for host inputs -- fixed in rgf.py.)
+        stream_first = (self.parts > 1 and self.n >= 2 * self.parts
                         and os.environ.get("BSEL_SWEEP_STREAM_FIRST", "1") != "0")
         self.done_events = []
         ready = None if stream_first else self._load(inputs[0], 0, None)

@@ -367,10 +367,11 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
             XB.copy_to_host(hxb, non_blocking=True)
         torch.cuda.current_stream(device).synchronize()
         return SelectedSolution(x_a=hxa, x_b=hxb if fused else None, mode=mode)
-    if host:
+    if host and not (out is not None and isinstance(out[0], DeviceBta)):
         from .device import to_host
 
         return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if fused else None, mode=mode)
+    # device outputs given by the caller stay on the device (host inputs or not)
     return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
 
 
@@ -448,8 +449,11 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, 
             XB.copy_to_host(hxb, non_blocking=True)
         torch.cuda.current_stream(device).synchronize()
         return SelectedSolution(x_a=hxa, x_b=hxb if fused else None, mode=mode)
-    if host:
+    if host and dev_out is None:
         from .device import to_host
 
         return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if fused else None, mode=mode)
+    # device outputs given by the caller stay on the device (host inputs or not): a
+    # round-1 bug copied them to pageable host memory here (the "8.5 s streamed first
+    # energy" of HostEnergySweep with two output slots)
     return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
