@@ -678,9 +678,12 @@ def main():
                          f"value = the faster",
                "all_cores_ms": pr["all_cores_ms"], "one_thread_ms": pr["one_thread_ms"], "host": host_info()}
         full = os.path.join(ROOT, "profiles", "cpu_protocol_r02.json")
-        if os.path.exists(full):
+        try:
             with open(full) as fh:
                 cpu["full_protocol"] = {k: v for k, v in json.load(fh).items() if k in ("value_ms", "fit", "host")}
+            cpu["full_protocol"]["source"] = "profiles/cpu_protocol_r02.json (tools/cpu_protocol.py on this pool)"
+        except (OSError, ValueError):
+            pass
 
     if rank == 0:
         line = {

@@ -58,7 +58,7 @@ def main():
     best = min(out["fit"], key=lambda k: out["fit"][k]["extrapolated_ms"])
     out["value_ms"] = out["fit"][best]["extrapolated_ms"]
     out["value_threads"] = int(best)
-    print(json.dumps(out))
+    bench.emit(out)  # bench.py routes fd 1 to stderr; emit() writes to the real stdout
 
 
 if __name__ == "__main__":
