@@ -447,6 +447,14 @@ constexpr int kLeafThreads = 256;
 // rewrote them since this SM may have cached them in L1.
 // ---------------------------------------------------------------------------
 
+// grid-barrier poll back-off in ns (0 = spin)
+#ifndef BSEL_BARRIER_SLEEP
+#define BSEL_BARRIER_SLEEP 64
+#endif
+// DMMA accumulator sets per tile product (2: even / odd k steps, half-length chains)
+#ifndef BSEL_TILE_ACC
+#define BSEL_TILE_ACC 2
+#endif
 constexpr int kT = 32;
 constexpr int kTLD = kT + 2;  // 544-byte rows: conflict-free DMMA fragment loads
 // largest |re| + |im| of a block Gauss-Jordan multiplier accepted without the
@@ -493,7 +501,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target)
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-#ifdef BSEL_BARRIER_SLEEP
+#if BSEL_BARRIER_SLEEP > 0
       if (v < target) __nanosleep(BSEL_BARRIER_SLEEP);
 #endif
     } while (v < target);
@@ -519,8 +527,12 @@ __device__ __forceinline__ void tile_mma(double (&acc)[4][2], const double2 (*sA
   const int kc0 = (lane & 3) >> 1, part = lane & 1;
   const int comp = (lane & 1) ^ ((lane >> 2) & 1);
   const int col0 = nh * 16 + ((lane >> 2) >> 1);
+  // two independent accumulator sets (even / odd k steps): the latency-bound
+  // tiles of the inverse (lookahead tile, panel updates) see half-length
+  // DMMA dependency chains
+  double acc2[4][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc2[j][0] = acc2[j][1] = 0.0;
 #pragma unroll 4
   for (int kk = 0; kk < kT / 2; ++kk) {
     const int kc = 2 * kk + kc0;
@@ -531,11 +543,14 @@ __device__ __forceinline__ void tile_mma(double (&acc)[4][2], const double2 (*sA
       double bf = Brow[(col0 + jn * 4) * 2 + comp];
       int hi = __double2hiint(bf) ^ (int)maskB;
       bf = __hiloint2double(hi, __double2loint(bf));
+      double(&c)[2] = (BSEL_TILE_ACC > 1 && (kk & 1)) ? acc2[jn] : acc[jn];
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                   : "+d"(acc[jn][0]), "+d"(acc[jn][1])
+                   : "+d"(c[0]), "+d"(c[1])
                    : "d"(af), "d"(bf));
     }
   }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] += acc2[j][0], acc[j][1] += acc2[j][1];
 }
 
 // Warp-tile coordinates of acc[jn]: row, col inside the 32 x 32 tile.
