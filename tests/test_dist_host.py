@@ -275,3 +275,115 @@ def test_host_payload_wire_roundtrip():
         for x, y in zip(getattr(p, f), getattr(q, f)):
             np.testing.assert_array_equal(x, y)
     assert q.nbytes() == p.nbytes() == 16 * 2 * (4 * 9 + 4 * 6)
+
+
+def test_payload_wire_format_interoperates_with_the_reference():
+    """Our BoundaryPayload bytes parse with the reference's from_bytes and
+    the reference's bytes parse with ours (dist.py:41-131 wire format; our
+    trailing sym_flags word is ignored by the reference)."""
+    import sys
+    if not os.path.isdir(os.path.join(REF, "btasel")):
+        pytest.skip("reference not installed")
+    sys.path.insert(0, REF)
+    try:
+        from btasel.dist import BoundaryPayload as RefPayload
+    finally:
+        sys.path.remove(REF)
+    from paper_2601_04904_b200.dist import BoundaryPayload
+    rng = np.random.default_rng(3)
+    c = lambda r, k: rng.standard_normal((r, k)) + 1j * rng.standard_normal((r, k))  # noqa: E731
+    ref = RefPayload(rank=1, kind="middle", diag=[c(3, 3), c(3, 3)], coupling=[c(3, 3), c(3, 3)],
+                     arrow_row=[c(2, 3), c(2, 3)], arrow_col=[c(3, 2), c(3, 2)])
+    ours = BoundaryPayload.from_bytes(ref.to_bytes())
+    assert ours.summary() == ref.summary() and ours.sym_flags == 3 and not ours.fused
+    back = RefPayload.from_bytes(ours.to_bytes())
+    assert back.summary() == ref.summary()
+    for f in ("diag", "coupling", "arrow_row", "arrow_col"):
+        for x, y in zip(getattr(ref, f), getattr(back, f)):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_owned_slices_merge_cover_the_pattern():
+    """owned_slices (the reference's local_backward slice form, dist.py:551-560)
+    of every rank merge into the full solution; every pattern block owned once."""
+    import torch
+    from paper_2601_04904_b200 import DeviceBta, plan_partitions
+    from paper_2601_04904_b200.dist import merge_slices, owned_slices, _slices_from_bytes, _slices_to_bytes
+    n, b, a = 12, 2, 1
+    full = {k: torch.randn(s, dtype=torch.complex128) for k, s in
+            {"diag": (n, b, b), "lower": (n - 1, b, b), "upper": (n - 1, b, b), "arrow_row": (n, a, b),
+             "arrow_col": (n, b, a), "tip": (a, a)}.items()}
+    X = DeviceBta(n, b, a, full)
+    plan = plan_partitions(n, 3, "siq")
+    slices = [_slices_from_bytes(_slices_to_bytes(owned_slices((X, X), plan, r)), True) for r in range(3)]
+    owned = {}
+    for sl in slices:
+        for kind in ("diag", "lower", "upper", "arrow_row", "arrow_col"):
+            for g in sl["x_a"][kind]:
+                assert (kind, g) not in owned
+                owned[(kind, g)] = True
+    assert len(owned) == 3 * n + 2 * (n - 1)
+    sol = merge_slices(n, b, a, "siq", slices)
+    for kind, t in full.items():
+        got = np.stack(getattr(sol.x_a, kind)) if kind != "tip" else sol.x_a.tip
+        np.testing.assert_array_equal(got, t.numpy())
+
+
+def _rankhub_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as tdist
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2601_04904_b200 import TorchCollectives
+        from paper_2601_04904_b200.dist import BoundaryPayload, _RankHub
+        b, a, k = 3, 2, 2
+        coll = TorchCollectives()
+        hub = _RankHub(coll, k)
+        pays, deltas = [], []
+        for j in range(k):
+            p = rank * k + j
+            kind = "first" if p == 0 else ("last" if p == world * k - 1 else "middle")
+            nb = 1 if kind != "middle" else 2
+            pay = BoundaryPayload(rank=p, kind=kind, b=b, a=a, fused=False)
+            val = lambda r, c, s: torch.full((r, c), complex(p, s), dtype=torch.complex128)  # noqa: E731
+            pay.diag = [val(b, b, i) for i in range(nb)]
+            pay.arrow_row = [val(a, b, 10 + i) for i in range(nb)]
+            pay.arrow_col = [val(b, a, 20 + i) for i in range(nb)]
+            if kind == "middle":
+                pay.coupling = [val(b, b, 30), val(b, b, 31)]
+            pays.append(pay)
+            deltas.append(torch.full((1, a, a), complex(p + 1, 0), dtype=torch.complex128))
+        got = hub.all_gather_all(pays)
+        tip = hub.all_reduce_all(deltas)
+        q.put((rank, [(g.rank, g.kind, len(g.diag), complex(g.diag[0][0, 0])) for g in got],
+               complex(tip[0, 0, 0]), [e.kind for e in coll.trace]))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc(), None, None))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_rank_hub_k_partitions_per_rank_gloo():
+    """_RankHub (k partitions per rank): ONE all_gather brings every
+    partition's payload in plan order, the tip deltas sum to the same value on
+    every rank; trace = one all_gather + one all_reduce."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_rankhub_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=240) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, got, tip, kinds in res:
+        assert not isinstance(got, str), got
+        assert [g[0] for g in got] == [0, 1, 2, 3]
+        assert [g[1] for g in got] == ["first", "middle", "middle", "last"]
+        assert [g[2] for g in got] == [1, 2, 2, 1]
+        assert [g[3] for g in got] == [complex(p, 0) for p in range(4)]
+        assert tip == complex(1 + 2 + 3 + 4, 0)
+        assert kinds == ["all_gather", "all_reduce"]
