@@ -451,9 +451,10 @@ constexpr int kLeafThreads = 256;
 #ifndef BSEL_BARRIER_SLEEP
 #define BSEL_BARRIER_SLEEP 64
 #endif
-// DMMA accumulator sets per tile product (2: even / odd k steps, half-length chains)
+// DMMA accumulator sets per tile product (2: even / odd k steps, half-length
+// chains -- measured neutral-to-slower in the cfg4 step, profiles/sweeps_r02.md)
 #ifndef BSEL_TILE_ACC
-#define BSEL_TILE_ACC 2
+#define BSEL_TILE_ACC 1
 #endif
 constexpr int kT = 32;
 constexpr int kTLD = kT + 2;  // 544-byte rows: conflict-free DMMA fragment loads

@@ -31,6 +31,16 @@ int aux_ctas() {
   }();
   return cap;
 }
+// BSEL_AUX_AFTER_CHAIN=1: a step's aux levels start after BOTH chain
+// products (not after f): the chain's second product then runs without the
+// step's own aux level competing for the SMs (experiment).
+bool aux_after_chain() {
+  static const bool on = [] {
+    const char* e = getenv("BSEL_AUX_AFTER_CHAIN");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
 }  // namespace
 
 bool fwd_backward_products() {
@@ -111,9 +121,10 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     Level L(sA);
     L.out(f).mm(+1, st.Lk, N, S, N);
     L.flush();
-    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
+    if (!aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     L.out(st.ad_j).add(+1, st.ad_j).mm(-1, f, N, st.Uk, N);
     L.flush();
+    if (aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
   }
   // Aux: A-side arrow/tip updates and the B side in three levels.  The
   // reference's quadratic updates (rgf.py:257-280) are re-associated so each
@@ -181,9 +192,10 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     Level L(sA);
     L.out(fn).mm(+1, st.L, N, S, N);
     L.flush();
-    cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
+    if (!aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     L.out(st.ad_n).add(+1, st.ad_n).mm(-1, fn, N, st.U, N);
     L.flush();
+    if (aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
   }
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
   Level L(sB, kTileAuto, aux_ctas());
