@@ -235,6 +235,17 @@ int bsel_generate_dd_bta(bsel_context_t* ctx, const bsel_bta_t* out, uint64_t se
                          bsel_status_t* st);
 /* hermitianize (matrix.py:337-354) in place: m <- (m + m^H)/2 on the pattern. */
 int bsel_hermitianize(bsel_context_t* ctx, const bsel_bta_t* m, bsel_status_t* st);
+/* Boundary publication over peer memory (the distributed scheme's all_gather,
+ * dist.py:436, as one kernel of NVLink P2P stores): copy nblocks (<= 16)
+ * device blocks src[i] of elems[i] complex elements to complex offset
+ * dst_off[i] of EVERY destination buffer dst[d] (ndst <= 8: the group's
+ * symmetric-memory receive buffers, this rank's included, mapped into this
+ * process), plus the 4-double slot header at complex offset hdr_off.  The
+ * caller orders it with a device-side group barrier before the receivers
+ * read.  Replaces: collectives.py:136-158 ThreadCollectives.all_gather
+ * (TorchCollectives(symmetric=True)).                                      */
+int bsel_publish(bsel_context_t* ctx, const void* const* src, const int64_t* elems, const int64_t* dst_off,
+                 int nblocks, void* const* dst, int ndst, int64_t hdr_off, const double* hdr, bsel_status_t* st);
 /* Number of CUDA kernels this library has launched in this process.        */
 uint64_t bsel_kernel_launches(void);
 

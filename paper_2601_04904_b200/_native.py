@@ -41,6 +41,7 @@ EXPORTS = (
     "bsel_local_backward",
     "bsel_generate_dd_bta",
     "bsel_hermitianize",
+    "bsel_publish",
     "bsel_kernel_launches",
     "bsel_profile_begin",
     "bsel_profile_end",
@@ -211,6 +212,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         sig["bsel_local_backward"] = ([vp, pb, pb, lf, pb, pb, pb, pb, i64, i64, i32, pb, pb, ts, st], i32)
         sig["bsel_generate_dd_bta"] = ([vp, ctypes.POINTER(Bta), ctypes.c_uint64, ctypes.c_double, st], i32)
         sig["bsel_hermitianize"] = ([vp, ctypes.POINTER(Bta), st], i32)
+        sig["bsel_publish"] = ([vp, vp, vp, vp, i32, vp, i32, i64, vp, st], i32)
         sig["bsel_kernel_launches"] = ([], ctypes.c_uint64)
         sig["bsel_profile_begin"] = ([], i32)
         sig["bsel_profile_end"] = ([ctypes.POINTER(Profile)], i32)

@@ -75,9 +75,19 @@ class Collectives:
 
 
 class TorchCollectives(Collectives):
-    """torch.distributed transport; the process group must be initialised."""
+    """torch.distributed transport; the process group must be initialised.
 
-    def __init__(self, group=None):
+    ``symmetric`` (default: env ``BSEL_SYMM_EXCHANGE=1``, NCCL groups only):
+    the boundary all_gather is one kernel of NVLink peer stores
+    (``bsel_publish``) into symmetric-memory receive buffers (torch
+    ``_symmetric_memory``), bracketed by device-side group barriers, instead
+    of pack + NCCL ``all_gather_into_tensor``.  If the symmetric rendezvous
+    fails on any rank, every rank keeps the NCCL path (agreed by one
+    all_reduce)."""
+
+    def __init__(self, group=None, symmetric=None):
+        import os
+
         import torch.distributed as dist
 
         if not dist.is_initialized():
@@ -88,6 +98,73 @@ class TorchCollectives(Collectives):
         self.world_size = dist.get_world_size(group)
         self.trace: list[TraceEvent] = []
         self._round = 0
+        if symmetric is None:
+            symmetric = os.environ.get("BSEL_SYMM_EXCHANGE", "0") == "1"
+        self.symmetric = bool(symmetric) and dist.get_backend(group) == "nccl" and self.world_size <= 8
+        self._symm = {}
+        self.exchange_impl = "nccl all_gather"
+
+    def _symm_get(self, slot: int):
+        """Receive buffer (world x slot float64) in symmetric memory, its
+        handle and the peers' mapped buffer pointers; None if unavailable."""
+        st = self._symm.get(slot)
+        if st is not None:
+            return st
+        import ctypes
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ok, err = 1, None
+        try:
+            import torch.distributed._symmetric_memory as symm
+
+            grp = self.group or self._dist.group.WORLD
+            if hasattr(symm, "enable_symm_mem_for_group"):
+                symm.enable_symm_mem_for_group(grp.group_name)
+            buf = symm.empty(self.world_size * slot, dtype=torch.float64, device=dev)
+            hdl = symm.rendezvous(buf, grp)
+            ptrs = (ctypes.c_void_p * self.world_size)(*[int(p) for p in hdl.buffer_ptrs])
+        except Exception as exc:  # noqa: BLE001 - decided collectively below
+            ok, err = 0, exc
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        self._dist.all_reduce(flag, op=self._dist.ReduceOp.MIN, group=self.group)
+        if not int(flag.item()):
+            self.symmetric = False
+            import warnings
+
+            warnings.warn(f"symmetric-memory exchange unavailable ({err}); using NCCL all_gather")
+            return None
+        st = self._symm[slot] = (buf, hdl, ptrs)
+        self.exchange_impl = "bsel_publish: NVLink peer stores into symmetric memory"
+        return st
+
+    def _symm_all_gather(self, payload):
+        import ctypes
+
+        from . import _native
+        from .dist import _KIND_CODES
+
+        slot = payload.slot_elems()
+        st = self._symm_get(slot)
+        if st is None:
+            return None
+        buf, hdl, ptrs = st
+        w = self.world_size
+        hdl.barrier(channel=0)  # every rank consumed the previous exchange
+        blocks = payload.slot_blocks()
+        base = self.rank * (slot // 2)  # complex offset of this rank's slot
+        nb = len(blocks)
+        src = (ctypes.c_void_p * max(nb, 1))(*[t.data_ptr() for t, _ in blocks])
+        elems = (ctypes.c_int64 * max(nb, 1))(*[t.numel() for t, _ in blocks])
+        offs = (ctypes.c_int64 * max(nb, 1))(*[base + off for _, off in blocks])
+        hdr = (ctypes.c_double * 4)(float(payload.rank), float(_KIND_CODES[payload.kind]), float(len(payload.diag)),
+                                    float(payload.sym_flags))
+        ctx = _native.Context.get(torch.cuda.current_device())
+        ctx.bind_stream()
+        ctx.call("bsel_publish", src, elems, offs, nb, ptrs, w, base, hdr)
+        hdl.barrier(channel=0)  # every slot written everywhere
+        allp = buf.view(w, slot)
+        hdrs = allp[:, :4].cpu().tolist()
+        return [payload.unpack(allp[r], rank=r, header=hdrs[r]) for r in range(w)]
 
     def _record(self, kind, payloads):
         self.trace.append(TraceEvent(kind=kind, round_id=self._round, payloads=payloads))
@@ -129,7 +206,12 @@ class TorchCollectives(Collectives):
           runs over NCCL;
         * tensors / numpy arrays of identical shape on all ranks."""
         on_dev = getattr(payload, "on_device", None)
-        if hasattr(payload, "pack") and (on_dev is None or on_dev()):
+        out = None
+        if self.symmetric and hasattr(payload, "slot_blocks") and on_dev is not None and on_dev():
+            out = self._symm_all_gather(payload)
+        if out is not None:
+            pass
+        elif hasattr(payload, "pack") and (on_dev is None or on_dev()):
             flat = payload.pack()
             allp = self.gather_tensor(flat)
             hdrs = allp[:, :4].cpu().tolist()

@@ -601,6 +601,16 @@ int bsel_hermitianize(bsel_context_t* ctx, const bsel_bta_t* m, bsel_status_t* s
   });
 }
 
+int bsel_publish(bsel_context_t* ctx, const void* const* src, const int64_t* elems, const int64_t* dst_off,
+                 int nblocks, void* const* dst, int ndst, int64_t hdr_off, const double* hdr, bsel_status_t* st) {
+  return guarded(st, [&] {
+    if (!ctx || (nblocks > 0 && (!src || !elems || !dst_off)) || !dst || !hdr) throw ArgError("NULL argument");
+    cuda_check(launch_publish(reinterpret_cast<const double2* const*>(src), elems, dst_off, nblocks,
+                              reinterpret_cast<double2* const*>(dst), ndst, hdr_off, hdr, ctx->impl->stream()),
+               "publish");
+  });
+}
+
 uint64_t bsel_kernel_launches(void) { return launch_count(); }
 
 int bsel_profile_begin(void) {

@@ -115,6 +115,10 @@ cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cf
 // The 3-multiplication bulk-async kernel (zgemm3m.cu) behind launch_gemm_batch.
 cudaError_t launch_gemm_batch_3m(GemmBatch& batch, cudaStream_t stream, int tile_cfg);
 
+// Boundary publication to peers' symmetric-memory buffers (publish.cu).
+cudaError_t launch_publish(const double2* const* src, const int64_t* elems, const int64_t* dst_off, int nblocks,
+                           double2* const* dst, int ndst, int64_t hdr_off, const double* hdr, cudaStream_t s);
+
 // Number of SMs of the current device (cached).
 int device_sm_count();
 

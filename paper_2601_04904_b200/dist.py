@@ -199,6 +199,18 @@ class BoundaryPayload:
     def slot_elems(self) -> int:
         return 4 + sum(2 * 2 * r * c for _, (r, c) in self._layout())  # 2 blocks per field
 
+    def slot_blocks(self) -> list:
+        """(block tensor, complex offset within the slot) of every block, in
+        ``pack``'s layout (header = the first 2 complex)."""
+        out, off = [], 2
+        for name, (r, c) in self._layout():
+            for j in range(2):
+                lst = getattr(self, name)
+                if j < len(lst):
+                    out.append((lst[j], off))
+                off += r * c
+        return out
+
     def pack(self) -> torch.Tensor:
         dev = self.diag[0].device
         out = torch.zeros(self.slot_elems(), dtype=torch.float64, device=dev)

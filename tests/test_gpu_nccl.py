@@ -225,3 +225,52 @@ def test_reference_dist_over_nccl(world, n, b, a):
         assert tb is None, tb
         assert kinds[:2] == ["all_gather", "all_reduce"]  # + the output gather_to_root round
     assert res[0][1] is True
+
+
+def _symm_rank(rank, world, port, n, b, a, q):
+    """Boundary exchange by NVLink peer stores into symmetric memory
+    (TorchCollectives(symmetric=True), bsel_publish) vs the NCCL all_gather:
+    bit-identical solutions, one all_gather + one all_reduce per solve."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        import paper_2601_04904_b200 as bs
+        dA = bs.generate_dd_bta_device(n, b, a, seed=0)
+        dB = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=1))
+        ref = [t.clone() for X in bs.DistSolver(dA, dB, "siq", world, rank, dev).solve() for t in X.tensors().values()]
+        coll = bs.TorchCollectives(symmetric=True)
+        s = bs.DistSolver(dA, dB, "siq", world, rank, dev, transport=coll)
+        for _ in range(3):  # the receive buffer is reused across solves
+            got = [t for X in s.solve() for t in X.tensors().values()]
+            torch.cuda.synchronize()
+            same = all(torch.equal(x, y) for x, y in zip(got, ref))
+        kinds = [e.kind for e in coll.trace]
+        dist.barrier()
+        q.put((rank, same, kinds, coll.exchange_impl, None))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, None, None, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,n,b,a", [(2, 16, 64, 16), (4, 24, 48, 8)])
+def test_symmetric_memory_exchange(world, n, b, a):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_symm_rank, args=(r, world, port, n, b, a, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+    for rank, same, kinds, impl, tb in res:
+        assert tb is None, tb
+        assert "bsel_publish" in impl, impl
+        assert same
+        assert kinds == ["all_gather", "all_reduce"] * 3
