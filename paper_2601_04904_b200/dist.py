@@ -1111,9 +1111,11 @@ def _solve_as_rank(a, b, plan, coll, mode, counter, timings, recursive_parts):
     return merge_slices(A.n, A.b, A.a, mode, [_slices_from_bytes(bl, fused) for bl in blobs])
 
 
-# SMs the forward's throughput GEMM levels leave to a single lane's chain
-# (measured, n=512 one lane: forward 343 -> 322 ms with 32; 16 and 48 worse)
-AUX_AVOID_SMS = int(os.environ.get("BSEL_AUX_AVOID_SMS", "32"))
+# SMs the forward's throughput GEMM levels leave to a single lane's chain.
+# Round 1 (real-embedding GEMM): 32 helped (n=512 one lane: forward 343 ->
+# 322 ms).  Round 2 (persistent 3M TMA GEMM): 0 is best (2 GPUs 496 vs 520 ms,
+# 4 GPUs 352 vs 369 ms; profiles/sweeps_r02.md).
+AUX_AVOID_SMS = int(os.environ.get("BSEL_AUX_AVOID_SMS", "0"))
 
 
 class _RankHub:
@@ -1162,7 +1164,9 @@ class DistSolver:
         # (default: the reference's plan, partition.py:52-90)
         self.plan = plan_partitions(A.n, world * self.k, mode, costs=plan_costs)
         self.rank = rank
-        self.coll = transport or TorchCollectives()
+        # the bench / production path publishes boundaries by NVLink peer stores
+        # into symmetric memory (BSEL_SYMM_EXCHANGE=0: NCCL all_gather)
+        self.coll = transport or TorchCollectives(symmetric=os.environ.get("BSEL_SYMM_EXCHANGE", "1") != "0")
         self.out = (DeviceBta.empty(A.n, A.b, A.a, device),
                     DeviceBta.empty(A.n, A.b, A.a, device) if self.B is not None else None)
         self._fac = None
