@@ -55,6 +55,46 @@ NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_gemm3m_step_r02.json")
 METRIC = "ms per energy point, fused BTA SI+SQ at 1/2/4/8 B200; % FP64 TC peak"
 
 
+def gemm_rate_by_phase(path):
+    """The GEMM kernel's executed rate per phase from the per-launch timeline
+    of the profiled step (BSEL_PROFILE_DUMP: kind, stream, start, end,
+    algorithmic flops, executed flops): forward = until the last block
+    inverse ends, backward = after.  Rate = executed flops of the phase's
+    GEMM launches / union of their spans."""
+    try:
+        rows = []
+        with open(path) as fh:
+            for line in fh:
+                p = line.strip().split(",")
+                if len(p) >= 6:
+                    rows.append((int(p[0]), float(p[2]), float(p[3]), float(p[4]), float(p[5])))
+        os.remove(path)
+    except OSError:
+        return None
+    if not rows:
+        return None
+    inv_end = max((r[2] for r in rows if r[0] == 1), default=None)
+    if inv_end is None:
+        return None
+    out = {}
+    for name, sel in (("forward", lambda r: r[2] <= inv_end), ("backward", lambda r: r[1] >= inv_end)):
+        g = sorted((r for r in rows if r[0] == 0 and sel(r)), key=lambda r: r[1])
+        busy, c0, c1 = 0.0, None, None
+        for r in g:
+            if c1 is None or r[1] > c1:
+                if c1 is not None:
+                    busy += c1 - c0
+                c0, c1 = r[1], r[2]
+            else:
+                c1 = max(c1, r[2])
+        if c1 is not None:
+            busy += c1 - c0
+        ex = sum(r[4] for r in g)
+        out[name] = {"gemm_busy_ms": round(busy, 2), "gemm_executed_tflops": ex / (busy * 1e-3) / 1e12 if busy else None,
+                     "gemm_launches": len(g)}
+    return out
+
+
 def flops_seq(n, b, a, mode="siq"):
     """Reference sequential op inventory (8 real flops per complex MAC, 8N^3
     per inverse), summed from the per-step tables (kernels.record_sweep)."""
@@ -581,6 +621,10 @@ def main():
     # launch spans (busy time) and its rate = its algorithmic flops / busy time.
     prof = _native.Profile()
     lib = _native.load_library()
+    import tempfile
+
+    dump = os.path.join(tempfile.gettempdir(), f"bsel_timeline_{os.getpid()}.csv")
+    os.environ.setdefault("BSEL_PROFILE_DUMP", dump)  # read by the library at its first profile_end
     lib.bsel_profile_begin()
     pstart, pend = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pstart.record()
@@ -588,6 +632,7 @@ def main():
     pend.record()
     lib.bsel_profile_end(prof)
     prof_ms = pstart.elapsed_time(pend)
+    by_phase = gemm_rate_by_phase(os.environ["BSEL_PROFILE_DUMP"])
     peak, peak_src = fp64_peak_tflops()
     ncu = None
     if os.path.exists(NCU_TRAFFIC_FILE):
@@ -712,6 +757,12 @@ def main():
                                            "real-embedding kernel for small products: 8MNK) of all its launches in "
                                            "one instrumented step / union of their CUDA-event spans (busy time)",
                          "frac_executed": (gemm_tflops / peak) if gemm_tflops else None,
+                         # the same rate per phase (rank 0's profiled step): in the backward the GEMM
+                         # is the bottleneck; the forward is bound by the Schur chains (block inverses)
+                         "by_phase": by_phase,
+                         "frac_executed_backward": (by_phase["backward"]["gemm_executed_tflops"] / peak
+                                                    if by_phase and by_phase["backward"]["gemm_executed_tflops"]
+                                                    else None),
                          "achieved_algorithmic": gemm_tflops_alg,
                          "achieved_algorithmic_basis": "8MNK per complex product (the reference's counting) over "
                                                        "the same busy time; exceeds the DMMA peak by up to 4/3 "

@@ -434,7 +434,7 @@ ProfileTotals profile_end() {
   // Spans relative to the base event; busy time = union of the spans of one
   // kind (launches of concurrent streams overlap).
   std::vector<std::pair<float, float>> spans[2];
-  // BSEL_PROFILE_DUMP=path: every launch as "kind,stream,start_ms,end_ms,flops" (timeline analysis)
+  // BSEL_PROFILE_DUMP=path: every launch as "kind,stream,start_ms,end_ms,flops,exec_flops" (timeline analysis)
   static const char* dump_path = getenv("BSEL_PROFILE_DUMP");
   FILE* dump = dump_path ? fopen(dump_path, "w") : nullptr;
   for (size_t i = 0; i < g_prof_used; ++i) {
@@ -445,7 +445,8 @@ ProfileTotals profile_end() {
     const int kind = g_prof[i].kind == 0 ? 0 : 1;
     spans[kind].emplace_back(s0, s1);
     if (dump)
-      fprintf(dump, "%d,%p,%.4f,%.4f,%.6g\n", kind, (void*)g_prof[i].stream, s0, s1, g_prof[i].flops);
+      fprintf(dump, "%d,%p,%.4f,%.4f,%.6g,%.6g\n", kind, (void*)g_prof[i].stream, s0, s1, g_prof[i].flops,
+              g_prof[i].exec_flops);
     if (kind == 0) {
       ++t.gemm_launches;
       t.gemm_flops += g_prof[i].flops;

@@ -29,7 +29,7 @@ bs.solve_selected(A, Bm, mode, partitions=parts, timings=t)
 lib.bsel_profile_end(prof)
 print("phases ms", {k: round(v * 1e3, 1) for k, v in t.items()})
 rows = [line.strip().split(",") for line in open(path)]
-rows = [(int(k), s, float(a), float(b), float(f)) for k, s, a, b, f in rows]
+rows = [(int(r[0]), r[1], float(r[2]), float(r[3]), float(r[4])) for r in rows]
 streams = {}
 for k, s, a, b, f in rows:
     streams.setdefault(s, []).append((a, b, k, f))
