@@ -84,15 +84,19 @@ __device__ bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
       const int k = k0 + j;
       const double2 cv = L.pan[buf][lane][j];  // column k, row `lane`
       const bool cand = lane < n && !((used >> lane) & 1u);
-      const unsigned key = cand ? (unsigned)__double2hiint(cabs1(cv)) + 1u : 0u;
+      // Pivot key in integer ops only (no FP64 latency on the search): the
+      // max-norm max(|re|, |im|) from the sign-cleared high words (monotone
+      // for non-negative doubles), 5 low bits traded for the row so that ONE
+      // redux.max yields the pivot row (lowest row among near-equal keys).
+      const unsigned mag = max((unsigned)__double2hiint(cv.x) & 0x7fffffffu, (unsigned)__double2hiint(cv.y) & 0x7fffffffu);
+      const unsigned key = cand ? (((mag >> 5) + 1u) << 5) | (31u - (unsigned)lane) : 0u;
       // Off the critical path: every lane inverts its own candidate while the
       // search runs; the pivot's reciprocal is then one shuffle away.
       const double2 rl = crecip_fast(cv);
       const double2 ci = make_double2(__shfl_sync(0xffffffffu, cv.x, i), __shfl_sync(0xffffffffu, cv.y, i));
       const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
-      const unsigned ball = __ballot_sync(0xffffffffu, cand && key == kmax);
-      const int p = __ffs(ball) - 1;
-      const bool zero = kmax <= 1u;  // all candidates zero (or subnormal): let the exact path decide
+      const int p = 31 - (int)(kmax & 31u);
+      const bool zero = (kmax >> 5) <= 1u;  // all candidates zero (or subnormal): let the exact path decide
       any_zero |= zero;
       used |= 1u << p;
       if (p == i) jp = j;
