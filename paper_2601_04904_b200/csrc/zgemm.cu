@@ -526,7 +526,7 @@ cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cf
   }();
   if (tile_cfg == kTile4m64 || tile_cfg == kTile4m32) {
     tile_cfg = tile_cfg == kTile4m64 ? kTile64 : kTile32;
-  } else if (tile_cfg >= kTile3m64 && tile_cfg <= kTile3m32) {
+  } else if (tile_cfg >= kTile3m64 && tile_cfg <= kTile3m6432k32) {
     return launch_gemm_batch_3m(batch, stream, tile_cfg);
   } else if (mode != 4) {
     bool big = true;

@@ -107,7 +107,8 @@ struct GemmBatch {
 // partitions' k = 3 back-substitution, measured best there.
 enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3,
                      // forced kernel variants (microbenchmarks / A-B tests)
-                     kTile3m64 = 10, kTile3m6432 = 11, kTile3m32 = 12, kTile4m64 = 20, kTile4m32 = 21 };
+                     kTile3m64 = 10, kTile3m6432 = 11, kTile3m32 = 12, kTile3m64k32 = 13, kTile3m6432k32 = 14,
+                     kTile4m64 = 20, kTile4m32 = 21 };
 
 // Launch one grouped batch on `stream`.  Problems with M==0 or N==0 are
 // dropped.  Returns cudaSuccess or the launch error.

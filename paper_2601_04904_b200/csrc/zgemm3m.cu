@@ -76,6 +76,10 @@ using C3_64 = Cfg3<64, 64, 16, 2, 4, 4, 1>;
 using C3_6432 = Cfg3<64, 32, 16, 2, 2, 4, 2>;
 // 32x32 tiles, 4 consumer warps of 16x16, BK 16 x 4 stages (small / chain levels).
 using C3_32 = Cfg3<32, 32, 16, 2, 2, 4, 3>;
+// BK 32 variants (half the barrier round trips per flop); 64x32 / BK 32 is the default for levels
+// that fill a wave (launch_gemm_batch_3m)
+using C3_64_K32 = Cfg3<64, 64, 32, 2, 4, 3, 1>;
+using C3_6432_K32 = Cfg3<64, 32, 32, 2, 2, 2, 2>;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -638,7 +642,7 @@ cudaError_t launch3(GemmBatch& batch, cudaStream_t stream) {
 }  // namespace
 
 // Variant selection (tile counts of the launch).  BSEL_GEMM3M_CFG forces one:
-// 64 (64x64), 6432 (64x32), 32 (32x32).
+// 64 (64x64), 6432 (64x32), 643232 (64x32, BK 32), 32 (32x32).
 cudaError_t launch_gemm_batch_3m(GemmBatch& batch, cudaStream_t stream, int tile_cfg) {
   static const int forced = [] {
     const char* e = getenv("BSEL_GEMM3M_CFG");
@@ -648,6 +652,8 @@ cudaError_t launch_gemm_batch_3m(GemmBatch& batch, cudaStream_t stream, int tile
   if (tile_cfg == kTile3m64) cfg = 64;
   if (tile_cfg == kTile3m6432) cfg = 6432;
   if (tile_cfg == kTile3m32) cfg = 32;
+  if (tile_cfg == kTile3m64k32) return launch3<C3_64_K32>(batch, stream);
+  if (tile_cfg == kTile3m6432k32) return launch3<C3_6432_K32>(batch, stream);
   if (!cfg) {
     int64_t t64 = 0, t6432 = 0;
     for (int i = 0; i < batch.nproblems; ++i) {
@@ -657,17 +663,24 @@ cudaError_t launch_gemm_batch_3m(GemmBatch& batch, cudaStream_t stream, int tile
     }
     const int64_t sms = device_sm_count();
     const int64_t wide = tile_cfg == kTileAutoWide ? 128 : 2 * sms;
+    // 64x32 tiles with BK 32 (2 CTAs/SM) whenever they fill one wave: on the
+    // concurrent backward levels they beat 64x64 (43.1 vs 41.9 TFLOP/s
+    // algorithmic, 3 streams) and match it on 1024^3 (35.9 vs 35.8);
+    // profiles/gemm3m_micro_r02b.json.  Fewer tiles: 32x32.
+    (void)t64;
+    (void)wide;
     if (tile_cfg == kTile32)
       cfg = 32;
-    else if (tile_cfg == kTile64 || t64 >= wide)
+    else if (tile_cfg == kTile64)
       cfg = 64;
     else if (t6432 >= sms)
-      cfg = 6432;
+      cfg = 643232;
     else
       cfg = 32;
   }
   if (cfg == 64) return launch3<C3_64>(batch, stream);
   if (cfg == 6432) return launch3<C3_6432>(batch, stream);
+  if (cfg == 643232) return launch3<C3_6432_K32>(batch, stream);
   return launch3<C3_32>(batch, stream);
 }
 

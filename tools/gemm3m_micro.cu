@@ -241,14 +241,14 @@ int main(int argc, char** argv) {
     return flops(b0) * reps / ms / 1e9;
   };
   printf("{\"unit\": \"algorithmic TFLOP/s (8MNK)\"");
-  const int cfgs[] = {kTile4m64, kTile4m32, kTile3m64, kTile3m6432, kTile3m32, kTileAuto};
-  const char* cn[] = {"4m64", "4m32", "3m64", "3m6432", "3m32", "auto3m"};
+  const int cfgs[] = {kTile4m64, kTile4m32, kTile3m64, kTile3m6432, kTile3m32, kTileAuto, kTile3m64k32,
+                      kTile3m6432k32};
+  const char* cn[] = {"4m64", "4m32", "3m64", "3m6432", "3m32", "auto3m", "3m64k32", "3m6432k32"};
+  const int ncfg = 8;
   for (auto& l : lv) {
     const int reps = 20;
     printf(",\n \"%s\": {", l.name.c_str());
-    for (int c = 0; c < 6; ++c) {
-      if (l.b.p[0].lower_only && (cfgs[c] == kTile3m6432)) {
-      }
+    for (int c = 0; c < ncfg; ++c) {
       printf("%s\"%s\": %.2f", c ? ", " : "", cn[c], timeit(l.b, cfgs[c], reps));
     }
     if (!l.b.p[0].lower_only) printf(", \"cublas\": %.2f", cublas_time(l.b, reps));
@@ -281,7 +281,7 @@ int main(int argc, char** argv) {
   cudaStream_t cs[3];
   for (auto& x : cs) cudaStreamCreate(&x);
   for (int li = 0; li < 3; ++li) {
-    for (int c = 0; c < 6; ++c) {
+    for (int c = 0; c < ncfg; ++c) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
