@@ -532,13 +532,17 @@ __device__ __forceinline__ void tile_mma(double (&acc)[4][2], const double2 (*sA
   const int kc0 = (lane & 3) >> 1, part = lane & 1;
   const int comp = (lane & 1) ^ ((lane >> 2) & 1);
   const int col0 = nh * 16 + ((lane >> 2) >> 1);
-  // two independent accumulator sets (even / odd k steps): the latency-bound
-  // tiles of the inverse (lookahead tile, panel updates) see half-length
-  // DMMA dependency chains
-  double acc2[4][2];
+  // BSEL_TILE_ACC independent accumulator sets (k steps round robin): the
+  // latency-bound tiles of the inverse (lookahead tile, panel updates) see
+  // dependent DMMA chains of 16 / BSEL_TILE_ACC steps (the DMMA dependent
+  // latency is ~90 ns on B200, tools/inv_micro lookahead trace)
+  constexpr int NA = BSEL_TILE_ACC;
+  double accs[NA][4][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc2[j][0] = acc2[j][1] = 0.0;
-#pragma unroll 4
+  for (int q = 0; q < NA; ++q)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) accs[q][j][0] = accs[q][j][1] = 0.0;
+#pragma unroll
   for (int kk = 0; kk < kT / 2; ++kk) {
     const int kc = 2 * kk + kc0;
     const double af = A[kc * 2 + part];
@@ -548,14 +552,19 @@ __device__ __forceinline__ void tile_mma(double (&acc)[4][2], const double2 (*sA
       double bf = Brow[(col0 + jn * 4) * 2 + comp];
       int hi = __double2hiint(bf) ^ (int)maskB;
       bf = __hiloint2double(hi, __double2loint(bf));
-      double(&c)[2] = (BSEL_TILE_ACC > 1 && (kk & 1)) ? acc2[jn] : acc[jn];
+      double(&c)[2] = accs[kk % NA][jn];
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                    : "+d"(c[0]), "+d"(c[1])
                    : "d"(af), "d"(bf));
     }
   }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j][0] += acc2[j][0], acc[j][1] += acc2[j][1];
+  for (int j = 0; j < 4; ++j) {
+    acc[j][0] = accs[0][j][0];
+    acc[j][1] = accs[0][j][1];
+#pragma unroll
+    for (int q = 1; q < NA; ++q) acc[j][0] += accs[q][j][0], acc[j][1] += accs[q][j][1];
+  }
 }
 
 // Warp-tile coordinates of acc[jn]: row, col inside the 32 x 32 tile.
@@ -690,6 +699,11 @@ __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int
   }
   if (is.has_x) {  // R = Dinv . W[J,K]
     tile_mma(acc, S.d, S.x[buf]);
+    if (T.trace && T.keep && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+      T.trace[16 * T.p + 12] = v;
+    }
     __syncthreads();  // previous readers of S.r are done
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) S.r[orow][acc_col(jn)] = make_double2(acc[jn][0], acc[jn][1]);
@@ -739,6 +753,13 @@ __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int
 template <int B>
 __device__ __forceinline__ void gj_stage(PinvSmem& S, TileCtx& T, int t, int tn, int t1, int t0,
                                          const TileIssue& cur, TileIssue& nxt, int& issued_r_tk) {
+  const bool lk = T.trace && T.keep && blockIdx.x == 0 && threadIdx.x == 0;  // debug: lookahead phases
+  auto gt = [] {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+  };
+  if (lk) T.trace[16 * T.p + 8] = gt();
   if (tn < t1) {
     nxt = issue_tile(S, T, tn, B ^ 1, issued_r_tk);
     inv_cp_wait<1>();
@@ -746,14 +767,16 @@ __device__ __forceinline__ void gj_stage(PinvSmem& S, TileCtx& T, int t, int tn,
     inv_cp_wait<0>();
   }
   __syncthreads();
+  if (lk) T.trace[16 * T.p + 9] = gt();
   const bool tr = T.trace && blockIdx.x == 1 && threadIdx.x == 0 && t == t0;  // debug stamps
   unsigned long long g0 = 0, g1 = 0;
   if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   compute_tile(S, T, t, B, cur);
   __syncthreads();  // slot B is refilled by the next stage's issue
+  if (lk) T.trace[16 * T.p + 10] = gt();
   if (tr) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
-    T.trace[8 * T.p + 6] = g0, T.trace[8 * T.p + 7] = g1;
+    T.trace[16 * T.p + 6] = g0, T.trace[16 * T.p + 7] = g1;
   }
 }
 
@@ -767,6 +790,11 @@ __device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
   int issued_r_tk = T.r_tk;
   __syncthreads();  // smem buffers free (previous panel / leaf)
   TileIssue a, b;
+  if (T.trace && T.keep && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    T.trace[16 * T.p + 11] = v;
+  }
   a = issue_tile(S, T, t, 0, issued_r_tk);
   b.has_x = false;
   while (true) {
@@ -849,30 +877,30 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
     if (!(blockIdx.x == 0 && G > 1 && p > 0)) load_tile(S.d, g.gD + (p & 1) * kT * kT, kT, kT, kT);
     __syncthreads();
     const int sp = (p + 1 < ntq) ? (p + 1) * nt + (p + 1) : -1;
-    if (blockIdx.x == 0) stamp(8 * p + 0);
+    if (blockIdx.x == 0) stamp(16 * p + 0);
     if (blockIdx.x == 0 && sp >= 0) {
       T.keep = true;
       gj_tiles(S, T, sp, sp + 1, -1);
       T.keep = false;
       T.r_tk = -1;  // S.r now holds the tile, not an R
       __syncthreads();
-      stamp(8 * p + 1);
+      stamp(16 * p + 1);
       // S.d is free once the lookahead tile is done (CTA 0 updates no other
       // tiles when G > 1): keep Dinv_{p+1} there for the next panel
       leaf_publish_smem(L, S.r, min(kT, b - (p + 1) * kT), g.gD + ((p + 1) & 1) * kT * kT, g.flag,
                         g.warp_leaf != 0, G > 1 ? S.d : nullptr);
-      stamp(8 * p + 2);
+      stamp(16 * p + 2);
     }
     if (G == 1 || blockIdx.x > 0) {
       const int chunk = (ntiles + workers - 1) / workers;
       const int t0 = wid * chunk, t1 = min(ntiles, t0 + chunk);
       gj_tiles(S, T, t0, t1, G == 1 ? -1 : sp);
     }
-    if (blockIdx.x == 0) stamp(8 * p + 3);
-    if (blockIdx.x == 1) stamp(8 * p + 4);
+    if (blockIdx.x == 0) stamp(16 * p + 3);
+    if (blockIdx.x == 1) stamp(16 * p + 4);
     target += G;
     grid_barrier(g.barrier, target);
-    if (blockIdx.x == 1) stamp(8 * p + 5);
+    if (blockIdx.x == 1) stamp(16 * p + 5);
     T.Wc = T.Wn;
   }
 }

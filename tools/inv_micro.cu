@@ -80,19 +80,21 @@ int main() {
     if (n == 512) {
       const int nt = n / 32;
       unsigned long long* tr;
-      cudaMalloc(&tr, 8 * nt * 8);
-      cudaMemset(tr, 0, 8 * nt * 8);
+      cudaMalloc(&tr, 16 * nt * 8);
+      cudaMemset(tr, 0, 16 * nt * 8);
       bsel::g_inverse_trace = tr;
       bsel::launch_block_inverse(X, n, Y, n, n, W, flag, nullptr, 0, s);
       cudaStreamSynchronize(s);
       bsel::g_inverse_trace = nullptr;
-      std::vector<unsigned long long> h(8 * nt);
-      cudaMemcpy(h.data(), tr, 8 * nt * 8, cudaMemcpyDeviceToHost);
+      std::vector<unsigned long long> h(16 * nt);
+      cudaMemcpy(h.data(), tr, 16 * nt * 8, cudaMemcpyDeviceToHost);
       unsigned long long t0 = h[0];
       for (int p = 0; p < nt; ++p) {
-        auto d = [&](int k) { return h[8 * p + k] ? (double)(h[8 * p + k] - t0) / 1e3 : -1.0; };
+        auto d = [&](int k) { return h[16 * p + k] ? (double)(h[16 * p + k] - t0) / 1e3 : -1.0; };
         printf("panel %2d: cta0 start %7.2f  tile %7.2f  leaf %7.2f  atbar %7.2f | cta1 first-tile %7.2f..%7.2f done %7.2f  past-bar %7.2f us\n",
                p, d(0), d(1), d(2), d(3), d(6), d(7), d(4), d(5));
+        printf("          lookahead: issue %7.2f  stage-begin %7.2f  landed %7.2f  R-done %7.2f  tile-done %7.2f\n",
+               d(11), d(8), d(9), d(12), d(10));
       }
     }
     cudaFree(X); cudaFree(Y); cudaFree(W); cudaFree(flag);
