@@ -382,6 +382,44 @@ def dist_e2e(args, solver, A, B, n, world, rank, dev, dist):
                     "solution blocks streamed out behind the backward; max over ranks"}
 
 
+def cfg5_side_measurement(args, dev):
+    """BASELINE configs[4] (energy sweep, n=256, b=1024, a=256) at N=1 as a
+    side key of the default line: the cfg4 buffers are released first, then
+    1 warm-up + args.cfg5_energies timed energies through EnergySweep
+    (overlapped energies when they fit), device-timed ms per energy."""
+    import gc
+
+    import torch
+
+    import paper_2601_04904_b200 as bs
+
+    try:
+        bs.release_caches()
+        gc.collect()
+        torch.cuda.empty_cache()
+        n, b, a, idx = WORKLOADS["cfg5"]
+        sweep = bs.EnergySweep(n, b, a, "siq", device=dev)
+        sweep.run([0])
+        torch.cuda.synchronize()
+        k = max(2, args.cfg5_energies)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        sweep.run(list(range(1, k + 1)))
+        e.record()
+        torch.cuda.synchronize()
+        out = {"workload": f"cfg5: BASELINE.json configs[{idx}]", "n_blocks": n, "block": b, "tip": a,
+               "ms_per_energy": s.elapsed_time(e) / k, "energies": k,
+               "mode": "energy k+1's forward overlapped with energy k's backward" if sweep.overlap
+               else "energies back to back",
+               "note": "energies e = generator seeds (2e, 2e+1), generated on the device; device-timed"}
+        del sweep
+        gc.collect()
+        torch.cuda.empty_cache()
+        return out
+    except Exception as exc:  # noqa: BLE001 - a side key must not lose the main line
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
 def run_energy_sweep(args, n, b, a, cfg_idx, world, rank, local, dev, dist):
     """Config 5: energy-point sweep, energy parallel across ranks (weak
     scaling: ``--energies-per-gpu`` energies per GPU per step, no
@@ -494,6 +532,8 @@ def main():
                     help="N>1: partitions per GPU (lanes), plan over N x this many partitions")
     ap.add_argument("--no-other-b", action="store_true",
                     help="skip the general / anti-Hermitian right-hand-side timings")
+    ap.add_argument("--no-cfg5", action="store_true", help="N=1: skip the config-5 side measurement")
+    ap.add_argument("--cfg5-energies", type=int, default=4, help="N=1: timed energies of the config-5 side key")
     ap.add_argument("--energy-concurrent", type=int, default=None,
                     help="cfg5: independent energy pipes per GPU (default 1)")
     ap.add_argument("--no-energy-overlap", action="store_true",
@@ -730,6 +770,12 @@ def main():
         except (OSError, ValueError):
             pass
 
+    # ---- config 5 side measurement (N=1): the energy sweep's ms per energy -
+    cfg5 = None
+    if world == 1 and not args.no_cfg5:
+        A = B = XA = XB = ws = None  # noqa: F841 - release the cfg4 device buffers first
+        cfg5 = cfg5_side_measurement(args, dev)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
@@ -801,6 +847,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "input_generation_s": t_gen,
+            "config5": cfg5,
         }
         emit(line)
     if dist:

@@ -223,11 +223,20 @@ class BtaMatrix:
 
 @dataclass
 class SelectedSolution:
-    """Pattern-restricted solution containers (matrix.py:166-185)."""
+    """Pattern-restricted solution containers (matrix.py:166-185).
+
+    ``algorithm`` (not in the reference; informational): which scheme
+    produced the solution -- "rgf" (the sequential sweeps, rgf.py) or
+    "partitions=k" (the paper's partitioned scheme, dist.py, with k
+    partitions: solve_selected's default for n >= 64 runs 2 of them
+    concurrently on one GPU; ``partitions=1`` or BSEL_PARTITIONS=1 selects
+    the sequential sweeps).  OpCounter always receives the reference's
+    sequential inventory."""
 
     x_a: object
     x_b: object | None
     mode: str
+    algorithm: str = "rgf"
 
     def __post_init__(self):
         if self.mode not in MODES:

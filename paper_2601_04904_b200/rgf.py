@@ -281,7 +281,13 @@ def _pinned(m) -> bool:
 def default_partitions(n: int) -> int:
     """Partitions used by ``solve_selected(partitions=None)``: the 2-partition
     scheme run concurrently on one GPU once the chain is long enough to
-    matter (measured on config 4: 2050 vs 2366 ms per energy point)."""
+    matter (config 4: 784 vs 978 ms per energy point); BSEL_PARTITIONS
+    overrides (1 = always the sequential RGF sweeps)."""
+    import os
+
+    env = os.environ.get("BSEL_PARTITIONS")
+    if env:
+        return max(1, int(env))
     return 2 if n >= 64 else 1
 
 
@@ -431,7 +437,8 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, 
             timings["forward"] = ph["forward"] + ph["communication"] + ph["reduced"]
             timings["backward"] = ph["backward"]
         torch.cuda.current_stream(device).synchronize()
-        return SelectedSolution(x_a=host_out[0], x_b=host_out[1] if fused else None, mode=mode)
+        return SelectedSolution(x_a=host_out[0], x_b=host_out[1] if fused else None, mode=mode,
+                                algorithm=f"partitions={parts}")
     if diagonal_only:
         for X in (XA, XB) if fused else (XA,):
             X.lower.zero_()
@@ -448,12 +455,13 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, 
         if fused:
             XB.copy_to_host(hxb, non_blocking=True)
         torch.cuda.current_stream(device).synchronize()
-        return SelectedSolution(x_a=hxa, x_b=hxb if fused else None, mode=mode)
+        return SelectedSolution(x_a=hxa, x_b=hxb if fused else None, mode=mode, algorithm=f"partitions={parts}")
     if host and dev_out is None:
         from .device import to_host
 
-        return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if fused else None, mode=mode)
+        return SelectedSolution(x_a=to_host(XA), x_b=to_host(XB) if fused else None, mode=mode,
+                                algorithm=f"partitions={parts}")
     # device outputs given by the caller stay on the device (host inputs or not): a
     # round-1 bug copied them to pageable host memory here (the "8.5 s streamed first
     # energy" of HostEnergySweep with two output slots)
-    return SelectedSolution(x_a=XA, x_b=XB, mode=mode)
+    return SelectedSolution(x_a=XA, x_b=XB, mode=mode, algorithm=f"partitions={parts}")

