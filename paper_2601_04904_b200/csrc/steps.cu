@@ -31,6 +31,17 @@ int aux_ctas() {
   }();
   return cap;
 }
+// Tile configuration of the chain's two products (BSEL_CHAIN_TILE: auto
+// (default), 6432 = 64x32 / BK 32, 64, 32) -- experiment knob.
+int chain_tile() {
+  static const int cfg = [] {
+    const char* e = getenv("BSEL_CHAIN_TILE");
+    const int v = e ? atoi(e) : 0;
+    return v == 6432 ? (int)kTile3m6432k32 : v == 64 ? (int)kTile3m64 : v == 32 ? (int)kTile3m32 : (int)kTileAuto;
+  }();
+  return cfg;
+}
+
 // BSEL_AUX_AFTER_CHAIN=1: a step's aux levels start after BOTH chain
 // products (not after f): the chain's second product then runs without the
 // step's own aux level competing for the SMs (experiment).
@@ -118,7 +129,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
   } else {
     ctx.invert(st.ad_i, st.S, order, index, sA);
-    Level L(sA);
+    Level L(sA, chain_tile());
     L.out(f).mm(+1, st.Lk, N, S, N);
     L.flush();
     if (!aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
@@ -189,7 +200,7 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
   } else {
     ctx.invert(st.ad_i, st.S, order, index, sA);
-    Level L(sA);
+    Level L(sA, chain_tile());
     L.out(fn).mm(+1, st.L, N, S, N);
     L.flush();
     if (!aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");

@@ -448,7 +448,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // `rw` from slot lookup to kernel launch).
 class TmaTable {
  public:
-  static constexpr uint32_t kCap = 1u << 18;  // 32 MiB of descriptors per device
+  static constexpr uint32_t kMaxCap = 1u << 18;  // 32 MiB of descriptors per device
+  // BSEL_TMA_TABLE_CAP (>= 64) shrinks the table (tests exercise the reset path)
+  static uint32_t cap() {
+    static const uint32_t c = [] {
+      const char* e = getenv("BSEL_TMA_TABLE_CAP");
+      const long v = e ? atol(e) : 0;
+      return v >= 64 && v < (long)kMaxCap ? (uint32_t)v : kMaxCap;
+    }();
+    return c;
+  }
 
   static TmaTable& current() {
     static std::mutex mu;
@@ -464,8 +473,8 @@ class TmaTable {
     if (dev_) return cudaSuccess;
     if (!encode_fn()) return cudaErrorNotSupported;
     cudaError_t e;
-    if ((e = cudaMalloc(&dev_, (size_t)kCap * 128)) != cudaSuccess) return e;
-    if ((e = cudaHostAlloc(&host_, (size_t)kCap * 128, cudaHostAllocDefault)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&dev_, (size_t)cap() * 128)) != cudaSuccess) return e;
+    if ((e = cudaHostAlloc(&host_, (size_t)cap() * 128, cudaHostAllocDefault)) != cudaSuccess) return e;
     return cudaStreamCreateWithFlags(&up_, cudaStreamNonBlocking);
   }
 
@@ -523,7 +532,7 @@ class TmaTable {
         *id = next_ - (uint32_t)pending_.size() + (uint32_t)j;
         return cudaSuccess;
       }
-    if (next_ == kCap) {
+    if (next_ == cap()) {
       *full = true;
       pending_.clear();
       return cudaSuccess;

@@ -345,3 +345,30 @@ def test_solution_reports_the_scheme():
     assert bs.solve_selected(A, B, partitions=1).algorithm == "rgf"
     dA, dB = bs.to_device(A), bs.to_device(B)
     assert bs.solve_selected(dA, dB).algorithm == "partitions=2"
+
+
+def test_tma_descriptor_table_reset_path():
+    """The 3M GEMM's TMA descriptor table restarts when it fills (device sync,
+    slots reused): with a 64-slot table a config-3-shaped solve (thousands of
+    distinct operand blocks) refills it many times and must reproduce the
+    default-table result bit for bit."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_2601_04904_b200 as bs; "
+            "A = bs.generate_dd_bta_device(24, 128, 32, seed=0); "
+            "B = bs.hermitianize_device(bs.generate_dd_bta_device(24, 128, 32, seed=1)); "
+            "s = bs.solve_selected(A, B); x = bs.to_host(s.x_b); "
+            "np.save(sys.argv[1], np.concatenate([x.stacked()[k].ravel() for k in ('diag', 'lower', 'arrow_row')]))"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        outs = []
+        for cap in ("64", ""):
+            env = dict(os.environ, BSEL_TMA_TABLE_CAP=cap)
+            path = os.path.join(d, f"x{cap or 'full'}.npy")
+            r = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True,
+                               timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+        np.testing.assert_array_equal(outs[0], outs[1])
