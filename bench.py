@@ -533,7 +533,7 @@ def main():
     ap.add_argument("--no-other-b", action="store_true",
                     help="skip the general / anti-Hermitian right-hand-side timings")
     ap.add_argument("--no-cfg5", action="store_true", help="N=1: skip the config-5 side measurement")
-    ap.add_argument("--cfg5-energies", type=int, default=4, help="N=1: timed energies of the config-5 side key")
+    ap.add_argument("--cfg5-energies", type=int, default=6, help="N=1: timed energies of the config-5 side key")
     ap.add_argument("--energy-concurrent", type=int, default=None,
                     help="cfg5: independent energy pipes per GPU (default 1)")
     ap.add_argument("--no-energy-overlap", action="store_true",
@@ -774,6 +774,7 @@ def main():
     cfg5 = None
     if world == 1 and not args.no_cfg5:
         A = B = XA = XB = ws = None  # noqa: F841 - release the cfg4 device buffers first
+        hA = hB = hXA = hXB = None  # noqa: F841 - and the 69 GB of pinned host buffers of the e2e leg
         cfg5 = cfg5_side_measurement(args, dev)
 
     if rank == 0:
