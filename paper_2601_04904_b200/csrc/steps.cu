@@ -110,7 +110,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
       L.flush();
     }
     cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
-    Level LB(sB, kTileAuto, aux_ctas());
+    Level LB(sB, kTileAutoFwd, aux_ctas());
     LB.avoid_sms(ctx.aux_avoid_sms(), ctx.aux_counter());
     LB.out(t2).mm(+1, S, N, st.ac_i, N);
     LB.out(st.ar_j).add(+1, st.ar_j).mm(-1, st.ar_i, N, t1, N);
@@ -146,7 +146,7 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   //   -g BC_i - BR_i g^H + p g^H    = g k - BR_i g^H
   // which also removes the reference's serial chain w -> S_B -> v -> Bd.
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
-  Level L(sB, kTileAuto, aux_ctas());
+  Level L(sB, kTileAutoFwd, aux_ctas());
   L.avoid_sms(ctx.aux_avoid_sms(), ctx.aux_counter());
   L.out(g).mm(+1, st.ar_i, N, S, N);
   L.out(w).mm(+1, S, N, st.bd_i, N);
@@ -209,7 +209,7 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
     if (aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
   }
   cuda_check(cudaStreamWaitEvent(sB, ring_a_event(ctx, slot), 0), "wait A");
-  Level L(sB, kTileAuto, aux_ctas());
+  Level L(sB, kTileAutoFwd, aux_ctas());
   L.avoid_sms(ctx.aux_avoid_sms(), ctx.aux_counter());
   L.out(fr).mm(+1, st.fill_r, N, S, N);
   L.out(g).mm(+1, st.ar_i, N, S, N);

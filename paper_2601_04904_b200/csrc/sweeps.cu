@@ -287,7 +287,7 @@ void bt_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const FactorsDev
       // v L^H - t1 BU = L S_B L^H - t1 BU = t1 (Bd t1^H - BU): two levels,
       // one product fewer than rgf.py:113-118.
       Mat w = ctx.tmp(r + 1, b, b), q = F.elim_q ? F.EQ(i) : ctx.tmp(r + 2, b, b), sb = F.SB(i);
-      Level L(sB);
+      Level L(sB, kTileAutoFwd);
       L.out(w).mm(+1, S, N, B->D(i), N);
       L.out(q).add(-1, B->U(i)).mm(+1, B->D(i), N, t1, H);
       L.flush();

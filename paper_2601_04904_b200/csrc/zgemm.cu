@@ -537,7 +537,7 @@ cudaError_t launch_gemm_batch(GemmBatch& batch, cudaStream_t stream, int tile_cf
     }
     if (mode == 3 || big) return launch_gemm_batch_3m(batch, stream, tile_cfg);
   }
-  if (tile_cfg == kTileAuto || tile_cfg == kTileAutoWide) {
+  if (tile_cfg == kTileAuto || tile_cfg == kTileAutoWide || tile_cfg == kTileAutoFwd) {
     int64_t tiles64 = 0;
     for (int i = 0; i < w; ++i)
       tiles64 += (int64_t)((batch.p[i].M + 63) / 64) * ((batch.p[i].N + 63) / 64);

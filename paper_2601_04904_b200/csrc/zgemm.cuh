@@ -104,8 +104,10 @@ struct GemmBatch {
 // Tile configurations (complex tile BM x BN).
 // kTileAuto: 64x64 tiles once a launch has >= 2 waves of them; kTileAutoWide:
 // already from 128 of them (BSEL_GEMM_MIN_TILES64_WIDE): the middle
-// partitions' k = 3 back-substitution, measured best there.
-enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3,
+// partitions' k = 3 back-substitution, measured best there.  kTileAutoFwd:
+// the forward sweeps' aux levels, which run beside the Schur chain (3M tile
+// policy without the BK 32 variant, zgemm3m.cu).
+enum TileCfg : int { kTile64 = 0, kTile32 = 1, kTileAuto = 2, kTileAutoWide = 3, kTileAutoFwd = 4,
                      // forced kernel variants (microbenchmarks / A-B tests)
                      kTile3m64 = 10, kTile3m6432 = 11, kTile3m32 = 12, kTile3m64k32 = 13, kTile3m6432k32 = 14,
                      kTile4m64 = 20, kTile4m32 = 21 };

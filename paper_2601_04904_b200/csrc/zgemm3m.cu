@@ -671,18 +671,21 @@ cudaError_t launch_gemm_batch_3m(GemmBatch& batch, cudaStream_t stream, int tile
       t6432 += (int64_t)((P.M + 63) / 64) * ((P.N + 31) / 32);
     }
     const int64_t sms = device_sm_count();
-    const int64_t wide = tile_cfg == kTileAutoWide ? 128 : 2 * sms;
-    // 64x32 tiles with BK 32 (2 CTAs/SM) whenever they fill one wave: on the
-    // concurrent backward levels they beat 64x64 (43.1 vs 41.9 TFLOP/s
-    // algorithmic, 3 streams) and match it on 1024^3 (35.9 vs 35.8);
-    // profiles/gemm3m_micro_r02b.json.  Fewer tiles: 32x32.
-    (void)t64;
-    (void)wide;
     if (tile_cfg == kTile32)
       cfg = 32;
     else if (tile_cfg == kTile64)
       cfg = 64;
+    else if (tile_cfg == kTileAutoFwd)
+      // Forward aux levels share the SMs with the Schur chain (block inverse
+      // + two chain products on the priority stream): the BK 16 variants,
+      // 64x64 from two waves.  With the BK 32 tiles here the single-lane
+      // chain of a 2-GPU rank ran 328 vs 274 ms (profiles/sweeps_r02.md).
+      cfg = t64 >= 2 * sms ? 64 : t6432 >= sms ? 6432 : 32;
     else if (t6432 >= sms)
+      // 64x32 tiles with BK 32 (2 CTAs/SM) whenever they fill one wave: on
+      // the concurrent backward levels they beat 64x64 (43.1 vs 41.9 TFLOP/s
+      // algorithmic, 3 streams) and match it on 1024^3 (35.9 vs 35.8);
+      // profiles/gemm3m_micro_r02b.json.
       cfg = 643232;
     else
       cfg = 32;
