@@ -55,7 +55,7 @@ NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_gemm3m_step_r02.json")
 METRIC = "ms per energy point, fused BTA SI+SQ at 1/2/4/8 B200; % FP64 TC peak"
 
 
-def gemm_rate_by_phase(path):
+def gemm_rate_by_phase(path, keep=False):
     """The GEMM kernel's executed rate per phase from the per-launch timeline
     of the profiled step (BSEL_PROFILE_DUMP: kind, stream, start, end,
     algorithmic flops, executed flops): forward = until the last block
@@ -68,7 +68,8 @@ def gemm_rate_by_phase(path):
                 p = line.strip().split(",")
                 if len(p) >= 6:
                     rows.append((int(p[0]), float(p[2]), float(p[3]), float(p[4]), float(p[5])))
-        os.remove(path)
+        if not keep:
+            os.remove(path)
     except OSError:
         return None
     if not rows:
@@ -672,7 +673,7 @@ def main():
     pend.record()
     lib.bsel_profile_end(prof)
     prof_ms = pstart.elapsed_time(pend)
-    by_phase = gemm_rate_by_phase(os.environ["BSEL_PROFILE_DUMP"])
+    by_phase = gemm_rate_by_phase(os.environ["BSEL_PROFILE_DUMP"], keep=os.environ["BSEL_PROFILE_DUMP"] != dump)
     peak, peak_src = fp64_peak_tflops()
     ncu = None
     if os.path.exists(NCU_TRAFFIC_FILE):

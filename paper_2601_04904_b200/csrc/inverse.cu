@@ -1,5 +1,6 @@
 // Complex128 block inverse (see inverse.cuh).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <string>
 
@@ -47,6 +48,12 @@ __device__ __forceinline__ double2 crecip_fast(double2 z) {
 // register bitmask.  Input in a (rows/cols < n); on return a holds S with
 // inv(A)[r][piv[k]] = S[piv[r]][k].
 constexpr int kSub = 8;               // sub-panel width
+// BSEL_LEAF_UNROLL: unroll factor of a sub-panel's pivot steps (code size:
+// fully unrolled, the leaf is ~7k instructions per call site)
+#ifndef BSEL_LEAF_UNROLL
+#define BSEL_LEAF_UNROLL 2
+#endif
+constexpr int kLeafUnroll = BSEL_LEAF_UNROLL;
 constexpr int kPanLd = kSub + 1;      // padded: column reads hit 8 distinct bank groups
 struct Leaf32 {
   double2 a[32][33];                  // input, then (after the elimination) the result S
@@ -57,7 +64,15 @@ struct Leaf32 {
   int pstep[kSub];                    // warp leaf: pivot row of each step of the sub-panel
 };
 
-__device__ bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
+#ifndef BSEL_LEAF_NOINLINE
+#define BSEL_LEAF_NOINLINE 0
+#endif
+#if BSEL_LEAF_NOINLINE
+__device__ __noinline__
+#else
+__device__
+#endif
+bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
   const int t = threadIdx.x, lane = t & 31;
   const int i = t >> 3, cl = t & 7;
   double2 v[4];
@@ -78,7 +93,7 @@ __device__ bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
     __syncthreads();
     const int steps = min(kSub, n - k0);
     int jp = -1;  // this row's step within the sub-panel if it was chosen as a pivot row
-#pragma unroll
+#pragma unroll kLeafUnroll
     for (int j = 0; j < kSub; ++j) {
       if (j >= steps) break;
       const int k = k0 + j;
@@ -159,112 +174,6 @@ __device__ bool gj_leaf32(Leaf32& L, int n, long long* trace = nullptr) {
   return any_zero;
 }
 
-
-// The same elimination with each sub-panel's 8 pivot steps done by ONE warp
-// in registers: lane r holds row r of the 32 x 8 sub-panel, the pivot search
-// is a redux/ballot over the lanes, the pivot row and its reciprocal travel
-// by shuffles -- no shared memory and no CTA barrier inside the 8 steps.
-// Per sub-panel the CTA publishes the whole tile (one barrier), warp 0 runs
-// the steps and writes the sub-panel and its pivots back (one barrier), and
-// every thread applies the sub-panel to its entries of the other columns as
-// the blocked leaf does (x' = zero_rows_P(x) + W x[P], the pivot rows read
-// from the published tile), then a barrier before the next publish.
-// Identical pivots and arithmetic per entry as gj_leaf32 (bitwise equal
-// results up to the order of the lazy-update sums, which is also the same).
-__device__ bool gj_leaf32_warp(Leaf32& L, int n) {
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int i = t >> 3, cl = t & 7;
-  double2 v[4];
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int c = cl + kSub * s;
-    v[s] = (i < n && c < n) ? L.a[i][c] : make_double2(0.0, 0.0);
-  }
-  bool used = false;  // warp 0: row `lane` already pivotal
-  bool any_zero = false;
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int k0 = kSub * s;
-    if (k0 >= n) break;
-#pragma unroll
-    for (int s2 = 0; s2 < 4; ++s2) L.a[i][cl + kSub * s2] = v[s2];
-    __syncthreads();
-    const int steps = min(kSub, n - k0);
-    if (warp == 0) {
-      double2 w[kSub];
-#pragma unroll
-      for (int c = 0; c < kSub; ++c) w[c] = L.a[lane][k0 + c];
-      int myj = -1;
-#pragma unroll
-      for (int j = 0; j < kSub; ++j) {
-        if (j >= steps) break;
-        const double2 cv = w[j];
-        const bool cand = lane < n && !used;
-        const unsigned key = cand ? (unsigned)__double2hiint(cabs1(cv)) + 1u : 0u;
-        const double2 rl = crecip_fast(cv);  // speculative: every lane inverts its candidate
-        const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
-        const unsigned ball = __ballot_sync(0xffffffffu, cand && key == kmax);
-        const int p = __ffs(ball) - 1;
-        const bool zero = kmax <= 1u;
-        any_zero |= zero;
-        const bool me = lane == p;
-        used |= me;
-        if (me) myj = j;
-        if (lane == 0) {
-          L.piv[k0 + j] = p;
-          L.pstep[j] = p;
-        }
-        const double2 rp = make_double2(__shfl_sync(0xffffffffu, rl.x, p), __shfl_sync(0xffffffffu, rl.y, p));
-        const double2 inv = zero ? make_double2(1.0, 0.0) : rp;
-        const double2 m = cmul(cv, inv);
-        const double2 coef = me ? inv : make_double2(-m.x, -m.y);
-#pragma unroll
-        for (int c = 0; c < kSub; ++c) {
-          // pivot row entry by shuffle (independent across c: the shuffles pipeline)
-          const double2 pr = make_double2(__shfl_sync(0xffffffffu, w[c].x, p), __shfl_sync(0xffffffffu, w[c].y, p));
-          const double bx = me ? 0.0 : w[c].x, by = me ? 0.0 : w[c].y;
-          double2 nv;
-          nv.x = fma(coef.x, pr.x, fma(-coef.y, pr.y, bx));
-          nv.y = fma(coef.x, pr.y, fma(coef.y, pr.x, by));
-          w[c] = c == j ? coef : nv;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < kSub; ++c) L.pan[0][lane][c] = w[c];
-      L.rowstep[lane] = myj;
-    }
-    __syncthreads();
-    // lazy update of the other sub-panels: x' = zero_rows_P(x) + W x[P]
-    const int jp = L.rowstep[i];
-    double2 w[kSub];
-#pragma unroll
-    for (int j = 0; j < kSub; ++j) w[j] = L.pan[0][i][j];
-#pragma unroll
-    for (int s2 = 0; s2 < 4; ++s2) {
-      if (s2 == s) continue;
-      double2 acc = jp >= 0 ? make_double2(0.0, 0.0) : v[s2];
-#pragma unroll
-      for (int j = 0; j < kSub; ++j) {
-        if (j >= steps) break;
-        const double2 x = L.a[L.pstep[j]][cl + kSub * s2];
-        acc.x = fma(w[j].x, x.x, fma(-w[j].y, x.y, acc.x));
-        acc.y = fma(w[j].x, x.y, fma(w[j].y, x.x, acc.y));
-      }
-      if (i < n && cl + kSub * s2 < n) v[s2] = acc;
-    }
-    if (i < n && cl + k0 < n) v[s] = L.pan[0][i][cl];
-    __syncthreads();  // L.a / L.pan are rewritten by the next sub-panel
-  }
-#pragma unroll
-  for (int s = 0; s < 4; ++s) L.a[i][cl + kSub * s] = v[s];
-  __syncthreads();
-  return __shfl_sync(0xffffffffu, (int)any_zero, 0) != 0;  // warp 0's verdict (thread 0 reports it)
-}
-
-// BSEL_LEAF=warp selects the warp-resident leaf (experiment, slower).
-__device__ __forceinline__ bool leaf32(Leaf32& L, int n, bool warp_leaf) {
-  return warp_leaf ? gj_leaf32_warp(L, n) : gj_leaf32(L, n);
-}
 
 // One CTA (256 threads) per matrix, n <= 32.
 __global__ void __launch_bounds__(256)
@@ -515,6 +424,38 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target)
   __syncthreads();
 }
 
+// Dataflow flags (epoch-tagged u64, never reset): spin until *p >= target.
+// Bounded: a flag that never arrives traps (a launch error) instead of
+// hanging the GPU.
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Publish a flag after the CTA's stores (callers: __syncthreads, then one
+// thread): the release store is cumulative over the stores the barrier
+// ordered before it (a preceding __threadfence, or fence.acq_rel + relaxed
+// store, measured the same).
+__device__ __forceinline__ void publish_flag(unsigned long long* p, unsigned long long v) { st_release(p, v); }
+// Poll back-off: 32 ns (0 / 256 ns and relaxed polling with one final
+// acquire measured the same, tools/build_sweep.sh).
+__device__ __noinline__ void wait_ge_slow(const unsigned long long* p, unsigned long long target) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire(p) < target) {
+    __nanosleep(32);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) __trap();  // 4 s: a lost flag, not a slow peer
+  }
+}
+__device__ __forceinline__ void wait_ge(const unsigned long long* p, unsigned long long target) {
+  if (ld_acquire(p) < target) wait_ge_slow(p, target);
+}
+
 // Load a kT x kT tile (rows x cols valid, zero elsewhere) into smem.
 __device__ __forceinline__ void load_tile(double2 (*dst)[kTLD], const double2* src, int64_t ld, int rows, int cols) {
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
@@ -573,14 +514,13 @@ __device__ __forceinline__ int acc_col(int jn) { return ((threadIdx.x >> 5) >> 2
 
 // CTA-wide: invert the diagonal tile W[j0:j0+jb, j0:j0+jb] and publish the
 // zero-padded 32 x 32 Dinv to gDp.
-__device__ void leaf_publish(Leaf32& L, const double2* W, int64_t ld, int j0, int jb, double2* gDp, int* flag,
-                             bool warp_leaf) {
+__device__ void leaf_publish(Leaf32& L, const double2* W, int64_t ld, int j0, int jb, double2* gDp, int* flag) {
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int i = e >> 5, j = e & 31;
     L.a[i][j] = (i < jb && j < jb) ? ldcg2(W + (int64_t)(j0 + i) * ld + j0 + j) : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const bool zero = leaf32(L, jb, warp_leaf);
+  const bool zero = gj_leaf32(L, jb);
   if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
   const double2 (*S)[33] = L.a;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
@@ -604,13 +544,19 @@ struct Quad {
 
 // As leaf_publish, with the diagonal tile already in shared memory.
 __device__ void leaf_publish_smem(Leaf32& L, const double2 (*src)[kTLD], int jb, double2* gDp, int* flag,
-                                  bool warp_leaf, double2 (*dsmem)[kTLD] = nullptr) {
+                                  double2 (*dsmem)[kTLD] = nullptr, long long* trace = nullptr) {
+  if (trace && threadIdx.x == 0) {
+    trace[12] = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace[16]));
+  }
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int i = e >> 5, j = e & 31;
     L.a[i][j] = (i < jb && j < jb) ? src[i][j] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const bool zero = leaf32(L, jb, warp_leaf);
+  if (trace && threadIdx.x == 0) trace[13] = clock64();
+  const bool zero = gj_leaf32(L, jb, trace);
+  if (trace && threadIdx.x == 0) trace[14] = clock64();
   if (threadIdx.x == 0 && zero) atomicMax(flag, 1);
   const double2 (*Sx)[33] = L.a;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
@@ -621,6 +567,10 @@ __device__ void leaf_publish_smem(Leaf32& L, const double2 (*src)[kTLD], int jb,
     if (dsmem) dsmem[r][c] = v;  // the publishing CTA keeps its copy (no reload through L2)
   }
   __syncthreads();
+  if (trace && threadIdx.x == 0) {
+    trace[15] = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace[17]));
+  }
 }
 
 struct TileCtx {
@@ -678,6 +628,7 @@ __device__ __forceinline__ TileIssue issue_tile(PinvSmem& S, const TileCtx& T, i
 }
 
 // Compute output tile t from buffer `buf` (its loads have landed).
+template <bool DF>
 __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int buf, const TileIssue& is) {
   const int tk = t / T.nt, ti = t % T.nt, p = T.p;
   const int ib = T.ext(ti), kb = T.ext(tk);
@@ -737,7 +688,7 @@ __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int
     for (int jn = 0; jn < 4; ++jn)
       S.r[orow][acc_col(jn)] = make_double2(is.w[jn].x - acc[jn][0], is.w[jn].y - acc[jn][1]);
   }
-  if (skip) return;
+  if (skip || (DF && T.keep)) return;  // dataflow: the lookahead tile lives in S.r only
 #pragma unroll
   for (int jn = 0; jn < 4; ++jn) {
     const int oc = acc_col(jn);
@@ -750,7 +701,7 @@ __device__ __forceinline__ void compute_tile(PinvSmem& S, TileCtx& T, int t, int
 // loads into slot B ^ 1, compute t.  B is a template constant so the two
 // in-flight TileIssue register sets never have to be copied (a copy would
 // wait for the in-flight epilogue loads).
-template <int B>
+template <int B, bool DF = false>
 __device__ __forceinline__ void gj_stage(PinvSmem& S, TileCtx& T, int t, int tn, int t1, int t0,
                                          const TileIssue& cur, TileIssue& nxt, int& issued_r_tk) {
   const bool lk = T.trace && T.keep && blockIdx.x == 0 && threadIdx.x == 0;  // debug: lookahead phases
@@ -771,7 +722,7 @@ __device__ __forceinline__ void gj_stage(PinvSmem& S, TileCtx& T, int t, int tn,
   const bool tr = T.trace && blockIdx.x == 1 && threadIdx.x == 0 && t == t0;  // debug stamps
   unsigned long long g0 = 0, g1 = 0;
   if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
-  compute_tile(S, T, t, B, cur);
+  compute_tile<DF>(S, T, t, B, cur);
   __syncthreads();  // slot B is refilled by the next stage's issue
   if (lk) T.trace[16 * T.p + 10] = gt();
   if (tr) {
@@ -783,6 +734,7 @@ __device__ __forceinline__ void gj_stage(PinvSmem& S, TileCtx& T, int t, int tn,
 // Output tiles [t0, t1) of the Gauss-Jordan update of panel p (tile `skip`
 // excluded), software pipelined: the operands of the next tile stream in
 // (cp.async, double buffered) while the current one computes.
+template <bool DF = false>
 __device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
   auto next = [&](int t) { ++t; return t == skip ? t + 1 : t; };
   int t = t0 == skip ? t0 + 1 : t0;
@@ -799,13 +751,68 @@ __device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
   b.has_x = false;
   while (true) {
     int tn = next(t);
-    gj_stage<0>(S, T, t, tn, t1, t0, a, b, issued_r_tk);
+    gj_stage<0, DF>(S, T, t, tn, t1, t0, a, b, issued_r_tk);
     if (tn >= t1) break;
     t = tn;
     tn = next(t);
-    gj_stage<1>(S, T, t, tn, t1, t0, b, a, issued_r_tk);
+    gj_stage<1, DF>(S, T, t, tn, t1, t0, b, a, issued_r_tk);
     if (tn >= t1) break;
     t = tn;
+  }
+}
+
+// Dataflow variant of gj_tiles: the tiles of [t0, t1) (minus `skip`) in two
+// passes -- first the "hot" ones (row / column p+1 and the tile (p+2, p+2):
+// the sources of the next panel and of CTA 0's next lookahead tile), then the
+// rest -- one software pipeline across both passes.  After the last hot tile
+// ONE fence publishes all hot tiles' ready flags (ver[t] = done).  Positions
+// k in [0, 2 len): pass k / len, tile t0 + k % len.
+__device__ void gj_tiles_df(PinvSmem& S, TileCtx& T, int t0, int t1, int skip, unsigned long long* ver,
+                            unsigned long long done) {
+  const int len = t1 - t0, p = T.p, nt = T.nt;
+  auto hot = [&](int t) {
+    const int tk = t / nt, ti = t % nt;
+    return ti == p + 1 || tk == p + 1 || (ti == p + 2 && tk == p + 2);
+  };
+  auto tile = [&](int k) { return t0 + (k >= len ? k - len : k); };
+  auto next = [&](int k) {  // next position whose tile belongs to its pass
+    for (++k; k < 2 * len; ++k) {
+      const int t = tile(k);
+      if (t != skip && hot(t) == (k < len)) break;
+    }
+    return k;
+  };
+  int k = next(-1);
+  if (k >= 2 * len) return;
+  const bool flags = ver != nullptr;
+  int issued_r_tk = T.r_tk;
+  __syncthreads();  // smem buffers free (previous panel)
+  TileIssue a, b;
+  a = issue_tile(S, T, tile(k), 0, issued_r_tk);
+  b.has_x = false;
+  auto publish_hot = [&](int kk, int kn) {  // after the last hot tile: flags of every hot tile
+    if (flags && kk < len && kn >= len && threadIdx.x == 0) {
+      bool first = true;
+      for (int t = t0; t < t1; ++t)
+        if (t != skip && hot(t)) {
+          if (first) publish_flag(ver + t, done);  // orders every hot tile's stores
+          else st_release(ver + t, done);
+          first = false;
+        }
+    }
+  };
+  constexpr int kNone = 1 << 30;
+  while (true) {
+    int kn = next(k);
+    gj_stage<0, true>(S, T, tile(k), kn < 2 * len ? tile(kn) : kNone, kNone, -1, a, b, issued_r_tk);
+    publish_hot(k, kn);
+    if (kn >= 2 * len) break;
+    k = kn;
+    kn = next(k);
+    gj_stage<1, true>(S, T, tile(k), kn < 2 * len ? tile(kn) : kNone, kNone, -1, b, a, issued_r_tk);
+    publish_hot(k, kn);
+    if (kn >= 2 * len) break;
+    k = kn;
   }
 }
 
@@ -827,12 +834,41 @@ __device__ void gj_tiles(PinvSmem& S, TileCtx& T, int t0, int t1, int skip) {
 struct GjArgs {
   Quad in, out, a, bq;
   int b, nq;
-  int warp_leaf;  // 0: the CTA-wide leaf (default), 1: gj_leaf32_warp (BSEL_LEAF=warp)
   double2* gD;
   unsigned* barrier;
   int* flag;
   unsigned long long* trace;
+  unsigned long long* stats;  // BSEL_INV_STATS: phase totals (ns) over all launches, may be null
 };
+
+#if BSEL_INV_STATS
+#define LEAF_TRACE_DECL __shared__ long long s_leaf_tr[18];
+#define LEAF_TRACE (g.stats ? s_leaf_tr : nullptr)
+#define LEAF_TRACE_ACC                                                              \
+  if (g.stats && threadIdx.x == 0)                                                  \
+    for (int q = 0; q < 4; ++q) {                                                   \
+      atomicAdd(g.stats + kStSteps, (unsigned long long)(s_leaf_tr[3 * q + 1] - s_leaf_tr[3 * q])); \
+      atomicAdd(g.stats + kStLazy, (unsigned long long)(s_leaf_tr[3 * q + 2] - s_leaf_tr[3 * q + 1])); \
+      if (q == 0) {                                                                 \
+        atomicAdd(g.stats + kStPro, (unsigned long long)(s_leaf_tr[13] - s_leaf_tr[12])); \
+        atomicAdd(g.stats + kStCore, (unsigned long long)(s_leaf_tr[14] - s_leaf_tr[13])); \
+        atomicAdd(g.stats + kStEpi, (unsigned long long)(s_leaf_tr[15] - s_leaf_tr[14])); \
+        atomicAdd(g.stats + kStLeafNs, (unsigned long long)(s_leaf_tr[17] - s_leaf_tr[16])); \
+      }                                                                             \
+    }
+#else
+#define LEAF_TRACE_DECL
+#define LEAF_TRACE nullptr
+#define LEAF_TRACE_ACC
+#endif
+// Build with -DBSEL_INV_STATS=1 and run with BSEL_INV_STATS=1: slots (summed over launches, globaltimer ns): CTA 0 per panel
+// lookahead tile / leaf / wait at the barrier, CTA 1 tile updates / wait,
+// whole kernel (CTA 0 first stamp -> exit), launches, panels.
+#ifndef BSEL_INV_STATS
+#define BSEL_INV_STATS 0
+#endif
+enum InvStat { kStLook = 0, kStLeaf, kStWait0, kStTiles1, kStWait1, kStKernel, kStLaunches, kStPanels, kStPub, kStCoLoc, kStSteps, kStLazy, kStPro, kStCore, kStEpi, kStLeafNs,
+               kStSm = 16, kStN = kStSm + 256 };
 
 __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_constant__ GjArgs g) {
   // trace (debug, may be null): per panel p, [8p+0] CTA0 start, [+1] after the
@@ -845,12 +881,36 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
       g.trace[slot] = t;
     }
   };
+  auto now = [] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+#if BSEL_INV_STATS
+  const bool st = g.stats && threadIdx.x == 0 && blockIdx.x < 2;
+#else
+  constexpr bool st = false;  // instrumentation compiled out (it costs registers)
+#endif
+  unsigned long long st_t = st ? now() : 0;
+  auto lap = [&](int slot) {  // time since the previous lap into `slot`
+    if (st) {
+      const unsigned long long t = now();
+      atomicAdd(g.stats + slot, t - st_t);
+      st_t = t;
+    }
+  };
+  if (st && blockIdx.x == 0) {
+    atomicAdd(g.stats + kStKernel, 0ull - st_t);
+    atomicAdd(g.stats + kStLaunches, 1ull);
+    atomicAdd(g.stats + kStPanels, (unsigned long long)((g.b + kT - 1) / kT));
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
   Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0][0]);  // spans x[0] and x[1]
+  LEAF_TRACE_DECL
   const int b = g.b, ntq = (b + kT - 1) / kT, nt = g.nq * ntq, ntiles = nt * nt, G = gridDim.x;
   unsigned target = 0;
-  if (blockIdx.x == 0) leaf_publish(L, g.in.p[0], g.in.ld[0], 0, min(kT, b), g.gD, g.flag, g.warp_leaf != 0);
+  if (blockIdx.x == 0) leaf_publish(L, g.in.p[0], g.in.ld[0], 0, min(kT, b), g.gD, g.flag);
   target += G;
   grid_barrier(g.barrier, target);
   TileCtx T;
@@ -878,6 +938,7 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
     __syncthreads();
     const int sp = (p + 1 < ntq) ? (p + 1) * nt + (p + 1) : -1;
     if (blockIdx.x == 0) stamp(16 * p + 0);
+    lap(blockIdx.x == 0 ? kStWait0 : kStWait1);
     if (blockIdx.x == 0 && sp >= 0) {
       T.keep = true;
       gj_tiles(S, T, sp, sp + 1, -1);
@@ -885,11 +946,14 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
       T.r_tk = -1;  // S.r now holds the tile, not an R
       __syncthreads();
       stamp(16 * p + 1);
+      lap(kStLook);
       // S.d is free once the lookahead tile is done (CTA 0 updates no other
       // tiles when G > 1): keep Dinv_{p+1} there for the next panel
       leaf_publish_smem(L, S.r, min(kT, b - (p + 1) * kT), g.gD + ((p + 1) & 1) * kT * kT, g.flag,
-                        g.warp_leaf != 0, G > 1 ? S.d : nullptr);
+                        G > 1 ? S.d : nullptr, LEAF_TRACE);
+      LEAF_TRACE_ACC
       stamp(16 * p + 2);
+      lap(kStLeaf);
     }
     if (G == 1 || blockIdx.x > 0) {
       const int chunk = (ntiles + workers - 1) / workers;
@@ -898,20 +962,240 @@ __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_cons
     }
     if (blockIdx.x == 0) stamp(16 * p + 3);
     if (blockIdx.x == 1) stamp(16 * p + 4);
+    if (blockIdx.x == 1) lap(kStTiles1);
     target += G;
     grid_barrier(g.barrier, target);
     if (blockIdx.x == 1) stamp(16 * p + 5);
     T.Wc = T.Wn;
   }
+  lap(blockIdx.x == 0 ? kStWait0 : kStWait1);
+  if (st && blockIdx.x == 0) atomicAdd(g.stats + kStKernel, st_t);
 }
 
+
+// ---------------------------------------------------------------------------
+// Dataflow persistent Gauss-Jordan (nq = 1, the chain's block inverse): the
+// per-panel grid barrier of persistent_gj_kernel replaced by ready flags.
+//
+// Measured (BSEL_INV_STATS, b = 512): with the barrier every panel costs
+// max(CTA 0's lookahead tile + leaf, the slowest worker's tiles) + barrier;
+// under the concurrent GEMM levels the workers' tiles (22 us per panel on
+// one GPU with two lanes) and the leaf path (20 us) alternate as the
+// slower side, and neither overlaps the other's panel.  Here:
+//  * CTA 0 runs ahead: lookahead tile (p+1, p+1) (its three source tiles'
+//    flags), leaf, publish Dinv_{p+1} into its own slot (one slot per
+//    panel: no reuse), flag dv = p + 2 -- it never waits for the bulk of
+//    panel p.
+//  * Workers (fixed tile ranges) start panel p once Dinv_p is out, wait per
+//    tile for the flags of its two foreign source tiles (row-panel (p, K),
+//    column-panel (I, p)), do their "hot" tiles (the next panel's sources)
+//    first and publish them with one fence, then the rest.
+//  * Three rotating n x n buffers (panel p reads R(p) = W(p-1), writes
+//    W(p); the last panel writes Y, R(0) = X).  W(p) reuses W(p-3)'s
+//    buffer, last read during panel p-2: a worker starts panel p only when
+//    every worker has reported panel p-2 done (per-CTA progress flags; CTA
+//    0's reads of R(p-2) precede its publication of Dinv_p).
+// Flags are u64 = epoch * 256 + version (epoch: a process-wide launch
+// counter) in a zero-initialised sync area at the start of the workspace,
+// so they are never reset.
+// ---------------------------------------------------------------------------
+constexpr int kSyncTiles = 4096;  // (2048 / kT)^2 tile flags: b <= 2048
+constexpr int kSyncCtas = 256;
+constexpr int64_t kSyncElems = (kSyncTiles + 1 + kSyncCtas + 1) / 2;  // in double2 units
+
+struct DfArgs {
+  unsigned long long* stats;  // BSEL_INV_STATS (instrumented builds), may be null
+  Quad in, y, s1, s2;  // nq = 1 quads (p[0], ld[0])
+  double2* dinv;       // ntq slots of kT x kT
+  unsigned long long* ver;   // tile flags [nt * nt]
+  unsigned long long* dv;    // Dinv_p published: *dv >= base + p + 1
+  unsigned long long* prog;  // per-CTA progress: panel p done -> base + p + 1
+  unsigned long long base;   // epoch * 256
+  int b;
+  int* flag;
+};
+
+__global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_constant__ DfArgs g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
+  Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0][0]);  // spans x[0] and x[1]
+  LEAF_TRACE_DECL
+  const int b = g.b, nt = (b + kT - 1) / kT, ntiles = nt * nt, G = gridDim.x;
+  const unsigned long long base = g.base;
+  // instrumentation (-DBSEL_INV_STATS=1): CTA 0 source waits / lookahead /
+  // leaf, CTA 1 wait phase / tiles (the InvStat slots)
+#if BSEL_INV_STATS
+  const bool st = g.stats && threadIdx.x == 0 && blockIdx.x < 2;
+#else
+  constexpr bool st = false;
+#endif
+  unsigned long long st_t = 0;
+  auto lap = [&](int slot) {
+    if (st) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (slot >= 0) atomicAdd(g.stats + slot, t - st_t);
+      st_t = t;
+    }
+  };
+  lap(-1);
+#if BSEL_INV_STATS
+  if (g.stats && threadIdx.x == 0) {  // CTAs per SM of this launch (co-location check)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    atomicAdd(g.stats + kStSm + (smid & 255), 1ull);
+    if (blockIdx.x == 0) atomicExch(g.stats + kStCoLoc, (unsigned long long)smid);
+  }
+#endif
+  if (st && blockIdx.x == 0) {
+    atomicAdd(g.stats + kStKernel, 0ull - st_t);
+    atomicAdd(g.stats + kStLaunches, 1ull);
+    atomicAdd(g.stats + kStPanels, (unsigned long long)((g.b + kT - 1) / kT));
+  }
+  // W(p): the last panel writes Y, earlier ones rotate backwards over Y, s1, s2
+  auto wbuf = [&](int p) -> const Quad* {
+    const int r = (nt - 1 - p) % 3;
+    return r == 0 ? &g.y : r == 1 ? &g.s1 : &g.s2;
+  };
+  TileCtx T;
+  T.trace = nullptr;
+  T.flag = g.flag;
+  T.b = b;
+  T.ntq = nt;
+  T.nt = nt;
+  T.skip_c = false;
+  if (blockIdx.x == 0) {
+    // ---- CTA 0: leaf 0, then per panel the lookahead tile + leaf ----
+    leaf_publish(L, g.in.p[0], g.in.ld[0], 0, min(kT, b), g.dinv, g.flag);
+    // keep Dinv_0 in S.d for the first lookahead
+    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) S.d[e >> 5][e & 31] = ldcg2(g.dinv + e);
+    __syncthreads();
+    if (threadIdx.x == 0) publish_flag(g.dv, base + 1);
+    lap(kStLeaf);
+    for (int p = 0; p + 1 < nt; ++p) {
+      T.p = p;
+      T.j0 = p * kT;
+      T.jb = min(kT, b - T.j0);
+      T.final_ = false;
+      T.Wc = p == 0 ? &g.in : wbuf(p - 1);
+      T.Wn = wbuf(p);
+      T.r_tk = -1;
+      T.keep = true;
+      const int sp = (p + 1) * nt + (p + 1);
+      // sources of the lookahead tile at version p (panel 0 reads the input):
+      // (p+1, p+1), row-panel (p, p+1), column-panel (p+1, p)
+      if (p > 0 && threadIdx.x < 3) {
+        const int src = threadIdx.x == 0 ? sp : threadIdx.x == 1 ? (p + 1) * nt + p : p * nt + (p + 1);
+        wait_ge(g.ver + src, base + p);
+      }
+      __syncthreads();
+      lap(kStWait0);
+      gj_tiles<true>(S, T, sp, sp + 1, -1);
+      T.keep = false;
+      __syncthreads();
+      lap(kStLook);
+      leaf_publish_smem(L, S.r, min(kT, b - (p + 1) * kT), g.dinv + (int64_t)(p + 1) * kT * kT, g.flag,
+                        S.d, LEAF_TRACE);
+      LEAF_TRACE_ACC
+      lap(kStLeaf);
+      if (threadIdx.x == 0) publish_flag(g.dv, base + p + 2);
+      lap(kStPub);
+    }
+    if (st) atomicAdd(g.stats + kStKernel, st_t);
+    return;
+  }
+  // ---- workers: fixed tile ranges ----
+  const int workers = G - 1, wid = blockIdx.x - 1;
+  const int chunk = (ntiles + workers - 1) / workers;
+  const int t0 = min(ntiles, wid * chunk), t1 = min(ntiles, t0 + chunk);
+  for (int p = 0; p < nt; ++p) {
+    const int sp = (p + 1 < nt) ? (p + 1) * nt + (p + 1) : -1;
+    // One wait phase per panel (each flag polled by one thread, released to
+    // the CTA by the barrier): W(p) reuses the buffer read during panel p-2
+    // (every CTA must be past it); Dinv_p; the source tiles of this range at
+    // version p -- column-panel (ti, p) per tile, row-panel (p, tk) per column.
+    const int tid = threadIdx.x;
+    // (CTA 0 has no progress flag: Dinv_p -- waited for below -- is published
+    // after its lookahead of panel p-1, i.e. after its reads of R(p-2))
+    if (p >= 2 && tid > 0 && tid < G) wait_ge(g.prog + tid, base + p - 1);
+    if (tid == 255) wait_ge(g.dv, base + p + 1);
+    if (p > 0 && tid >= 128 && tid < 160) {
+      for (int j = tid - 128; j < t1 - t0; j += 32) {
+        const int t = t0 + j, tk = t / nt, ti = t % nt;
+        if (ti != p && t != sp) wait_ge(g.ver + p * nt + ti, base + p);
+        // (also when the column's first tile here is the skipped lookahead
+        // tile: the column's other tiles form R from (p, tk))
+        if ((j == 0 || ti == 0) && tk != p) wait_ge(g.ver + tk * nt + p, base + p);
+      }
+    }
+    __syncthreads();
+    load_tile(S.d, g.dinv + (int64_t)p * kT * kT, kT, kT, kT);
+    __syncthreads();
+    if (blockIdx.x == 1) lap(kStWait1);
+    T.p = p;
+    T.j0 = p * kT;
+    T.jb = min(kT, b - T.j0);
+    T.final_ = p == nt - 1;
+    T.Wc = p == 0 ? &g.in : wbuf(p - 1);
+    T.Wn = wbuf(p);
+    T.r_tk = -1;
+    T.keep = false;
+    gj_tiles_df(S, T, t0, t1, sp, T.final_ ? nullptr : g.ver, base + p + 1);
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(g.prog + blockIdx.x, base + p + 1);
+    if (blockIdx.x == 1) lap(kStTiles1);
+  }
+}
 }  // namespace
 
 // work: n*n ping-pong buffer (also the exact fallback's scratch), then the
 // published Dinv tiles (2 x kT*kT, double-buffered) and the grid-barrier counter.
 unsigned long long* g_inverse_trace = nullptr;
 
-int64_t block_inverse_workspace(int n) { return (int64_t)n * n + 2 * kT * kT + 1; }
+namespace {
+// BSEL_INV_STATS=1: per-phase totals of every persistent inverse of the
+// process, printed to stderr at exit (one buffer per process, device 0 of
+// the first launch; the analysis tool, not a product path).
+unsigned long long* inverse_stats() {
+  static unsigned long long* buf = [] {
+    const char* e = getenv("BSEL_INV_STATS");
+    unsigned long long* p = nullptr;
+    if (!(e && atoi(e) != 0)) return p;
+    if (cudaMallocManaged(&p, kStN * sizeof(unsigned long long)) != cudaSuccess) return (unsigned long long*)nullptr;
+    memset(p, 0, kStN * sizeof(unsigned long long));
+    atexit([] {
+      unsigned long long* q = inverse_stats();
+      if (!q || cudaDeviceSynchronize() != cudaSuccess) return;
+      const double n = q[kStLaunches] ? (double)q[kStLaunches] : 1.0;
+      int multi = 0, used = 0;
+      for (int k = 0; k < 256; ++k) used += q[kStSm + k] > 0, multi += q[kStSm + k] > q[kStLaunches];
+      fprintf(stderr, "[inverse stats] leaf per launch: pivot steps %.0f kcycles, lazy updates %.0f kcycles | "
+              "prologue %.0f, core %.0f, epilogue %.0f kcycles; leaf_publish_smem %.1f us (globaltimer)\n",
+              q[kStSteps] / n / 1e3, q[kStLazy] / n / 1e3, q[kStPro] / n / 1e3, q[kStCore] / n / 1e3,
+              q[kStEpi] / n / 1e3, q[kStLeafNs] / n / 1e3);
+      fprintf(stderr, "[inverse stats] SMs used %d, SMs hosting > 1 CTA per launch on average %d, CTA0's last SM %llu "
+              "hosted %.2f CTAs per launch\n", used, multi, q[kStCoLoc], q[kStSm + (q[kStCoLoc] & 255)] / n);
+      fprintf(stderr,
+              "[inverse stats] launches %llu panels/launch %.1f | per launch us: kernel %.1f | CTA0 lookahead %.1f "
+              "leaf %.1f wait %.1f publish %.1f | CTA1 tiles %.1f wait %.1f\n",
+              q[kStLaunches], q[kStPanels] / n, q[kStKernel] / n / 1e3, q[kStLook] / n / 1e3, q[kStLeaf] / n / 1e3,
+              q[kStWait0] / n / 1e3, q[kStPub] / n / 1e3, q[kStTiles1] / n / 1e3, q[kStWait1] / n / 1e3);
+    });
+    return p;
+  }();
+  return buf;
+}
+}  // namespace
+
+// Layout: [sync area: kSyncElems (zero at allocation, epoch-tagged flags of
+// the dataflow kernel)][scratch].  Scratch: dataflow kernel s1, s2 (n x n
+// each) + Dinv slots (ntq x kT x kT); barrier kernel: n x n ping-pong, 2 Dinv
+// tiles, barrier counter; exact fallback: n x n.
+int64_t block_inverse_workspace(int n) {
+  const int64_t ntq = (n + kT - 1) / kT;
+  return kSyncElems + std::max<int64_t>(2 * (int64_t)n * n + ntq * kT * kT, (int64_t)n * n + 2 * kT * kT + 1);
+}
+
 
 namespace {
 // CTAs of the persistent inverse.  Default 64: fewer CTAs become co-resident
@@ -938,6 +1222,55 @@ int coop_grid_limit() {
       per_sm = 0;
     return coop ? per_sm * device_sm_count() : 0;
   });
+}
+
+Quad quad1(const double2* p, int64_t ld) {
+  Quad q{};
+  q.p[0] = const_cast<double2*>(p);
+  q.ld[0] = ld;
+  return q;
+}
+
+// BSEL_INV_DATAFLOW=0 selects the barrier kernel for the block inverse
+// (A/B experiments); default: the dataflow kernel.
+bool dataflow_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BSEL_INV_DATAFLOW");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+std::atomic<unsigned long long> g_inverse_epoch{0};
+
+cudaError_t launch_dataflow(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n, double2* sync,
+                            double2* scratch, int* flag, int grid, cudaStream_t stream) {
+  const cudaError_t attr = per_device([] {
+    return cudaFuncSetAttribute(dataflow_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(PinvSmem));
+  });
+  if (attr != cudaSuccess) return attr;
+  const int ntq = (n + kT - 1) / kT;
+  DfArgs g{};
+  g.in = quad1(const_cast<double2*>(X), ldx);
+  g.y = quad1(Y, ldy);
+  g.s1 = quad1(scratch, n);
+  g.s2 = quad1(scratch + (int64_t)n * n, n);
+  g.dinv = scratch + 2 * (int64_t)n * n;
+  unsigned long long* f = reinterpret_cast<unsigned long long*>(sync);
+  g.ver = f;
+  g.dv = f + kSyncTiles;
+  g.prog = f + kSyncTiles + 1;
+  g.base = (g_inverse_epoch.fetch_add(1) + 1) << 8;
+  g.b = n;
+  g.flag = flag;
+  g.stats = inverse_stats();
+  (void)ntq;
+  void* args[] = {(void*)&g};
+  const cudaError_t err =
+      cudaLaunchCooperativeKernel((const void*)dataflow_gj_kernel, grid, 256, args, sizeof(PinvSmem), stream);
+  count_launch();
+  return err;
 }
 }  // namespace
 
@@ -1052,22 +1385,12 @@ cudaError_t levels_inverse(const double2* X, int64_t ldx, double2* Y, int64_t ld
 }  // namespace
 
 namespace {
-Quad quad1(const double2* p, int64_t ld) {
-  Quad q{};
-  q.p[0] = const_cast<double2*>(p);
-  q.ld[0] = ld;
-  return q;
-}
 
 cudaError_t launch_gj(GjArgs& g, int grid, cudaStream_t stream) {
-  // The warp-resident leaf (gj_leaf32_warp, BSEL_LEAF=warp) measured SLOWER:
-  // 22.6 vs 11.0 us per 32x32 leaf, 484 vs 304 us per 512 inverse
-  // (tools/inv_micro, profiles/inverse_leaf_r02.md) -- the CTA-wide leaf stays.
-  static const int warp_leaf = [] {
-    const char* e = getenv("BSEL_LEAF");
-    return (e && std::string(e) == "warp") ? 1 : 0;
-  }();
-  g.warp_leaf = warp_leaf;
+  // (A warp-resident leaf measured 2x slower -- 22.6 vs 11.0 us per 32x32
+  // leaf, profiles/inverse_leaf_r02.md -- and was removed in round 2: its
+  // runtime switch tripled the kernels' code.)
+  g.stats = inverse_stats();
   if ((cudaError_t)cudaMemsetAsync(g.barrier, 0, sizeof(unsigned), stream) != cudaSuccess) return cudaGetLastError();
   // The CTAs wait on one another (grid barrier), so the launch is
   // cooperative: co-residency of the whole grid is guaranteed.  Cooperative
@@ -1119,9 +1442,19 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
                                  unsigned long long key, cudaStream_t stream, int grid_req) {
   if (n <= 0) return cudaSuccess;
   cudaError_t err;
+  double2* sync = work;
+  work += kSyncElems;
   const int panels = (n + kLeaf - 1) / kLeaf;
   const int limit = coop_grid_limit();
   if (panels > 1 && limit > 0) {
+    int grid = panels * panels < limit ? panels * panels : limit;
+    const int cap = grid_req > 0 ? grid_req : inverse_grid_cap();
+    if (grid > cap) grid = cap;
+    if (dataflow_enabled() && grid >= 2 && grid <= kSyncCtas && panels * panels <= kSyncTiles) {
+      err = launch_dataflow(X, ldx, Y, ldy, n, sync, work, flag, grid, stream);
+      if (err != cudaSuccess) return err;
+      goto fallback;
+    }
     GjArgs g{};
     g.in = quad1(X, ldx);
     g.out = g.a = quad1(Y, ldy);
@@ -1132,14 +1465,12 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     g.barrier = reinterpret_cast<unsigned*>(g.gD + 2 * kT * kT);
     g.flag = flag;
     g.trace = g_inverse_trace;
-    int grid = panels * panels < limit ? panels * panels : limit;
-    const int cap = grid_req > 0 ? grid_req : inverse_grid_cap();
-    if (grid > cap) grid = cap;
     err = launch_gj(g, grid, stream);
   } else {
     err = levels_inverse(X, ldx, Y, ldy, n, work, flag, stream);
   }
   if (err != cudaSuccess) return err;
+fallback:
   // Exact fallback (no-op unless a leaf met an exactly zero pivot).
   const size_t smem = (size_t)n * (2 * sizeof(double2) + 2 * sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
@@ -1149,7 +1480,7 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
   return cudaGetLastError();
 }
 
-int64_t schur_step_workspace(int b) { return 6 * (int64_t)b * b + 2 * kT * kT + 1; }
+int64_t schur_step_workspace(int b) { return kSyncElems + 6 * (int64_t)b * b + 2 * kT * kT + 1; }
 
 bool schur_step_supported(int b) { return b > kLeaf && coop_grid_limit() > 0; }
 
@@ -1160,6 +1491,7 @@ cudaError_t launch_schur_step(const double2* D, int64_t ldd, const double2* U, i
                               int grid_req) {
   if (!schur_step_supported(b)) return cudaErrorInvalidValue;
   const int64_t bb = (int64_t)b * b;
+  work += kSyncElems;  // the sync area belongs to the dataflow inverse
   double2* w = work;  // w0..w3 (B buffer), wc (A's C quadrant), wh (H if none given)
   if (!H) H = w + 5 * bb, ldh = b;
   GjArgs g{};

@@ -25,6 +25,8 @@ constexpr int kLeaf = 32;
 extern unsigned long long* g_inverse_trace;
 
 // Workspace (complex elements) needed by launch_block_inverse for one n x n.
+// It must be ZERO when first used (its head holds the dataflow kernel's
+// epoch-tagged ready flags, which are never reset).
 int64_t block_inverse_workspace(int n);
 
 // Y = inv(X) for one n x n matrix (X untouched, Y must not alias X).

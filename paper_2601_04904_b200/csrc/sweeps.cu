@@ -99,6 +99,9 @@ double2* Context::inv_work(int64_t elems) {
     cuda_check(cudaStreamSynchronize(chain_), "sync before realloc");
     if (inv_work_) cudaFree(inv_work_);
     cuda_check(cudaMalloc(&inv_work_, (size_t)elems * sizeof(double2)), "inverse workspace");
+    // the inverse's sync area (epoch-tagged flags, never reset) starts at zero
+    cuda_check(cudaMemset(inv_work_, 0, (size_t)elems * sizeof(double2)), "inverse workspace init");
+    cuda_check(cudaDeviceSynchronize(), "inverse workspace init");
     inv_work_elems_ = elems;
   }
   return inv_work_;

@@ -187,6 +187,23 @@ def _quadratic_residual(A, B, XA, XB, chunk=64):
     return worst
 
 
+def test_dataflow_inverse_two_lanes_stress():
+    """The chain's block inverse is a dataflow kernel (per-tile ready flags,
+    no grid barrier).  Two concurrent lanes (partitions=2, two inverses in
+    flight, the bench path) repeatedly vs the sequential sweeps: a missed
+    dependency shows up as a large error, not rounding (a race of this kind
+    gave 3e-9 identity residuals on the full config 4 before it was fixed)."""
+    n, b, a = 40, 512, 128
+    A = bs.generate_dd_bta_device(n, b, a, seed=5)
+    B = bs.hermitianize_device(bs.generate_dd_bta_device(n, b, a, seed=6))
+    ref = bs.solve_selected(A, B, "siq", partitions=1)
+    ra, rb = bs.to_host(ref.x_a), bs.to_host(ref.x_b)
+    for _ in range(4):
+        got = bs.solve_selected(A, B, "siq", partitions=2)
+        assert max_block_rel_err(bs.to_host(got.x_a), ra) <= 1e-12
+        assert max_block_rel_err(bs.to_host(got.x_b), rb) <= 1e-12
+
+
 @pytest.mark.parametrize("parts", [2, 1])
 def test_config4_full_bench_inputs_dense_free(parts):
     """The exact bench.py workload (n=1024, b=512, a=256, seeds 0/1, B

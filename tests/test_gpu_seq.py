@@ -57,13 +57,22 @@ def test_zgemm_general_alpha_beta_and_counter():
         bs.block_multiply_acc(None, crand(3, 4), crand(5, 2))
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 64, 100, 256, 512])
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 64, 100, 256, 512, 1000, 1024])
 def test_block_inverse_dd(n):
     x = crand(n, n) + np.diag(3.0 * n * np.ones(n))
     got = bs.block_inverse(x)
     res = np.linalg.norm(x @ got - np.eye(n)) / np.sqrt(n)
     assert res <= 1e-13
     np.testing.assert_allclose(got, np.linalg.inv(x), rtol=1e-11, atol=1e-14)
+
+
+def test_block_inverse_repeated_sizes():
+    """The dataflow inverse's ready flags are epoch-tagged and never reset:
+    back-to-back launches of different sizes on one workspace stay exact."""
+    for n in (512, 96, 512, 1000, 64, 512):
+        x = crand(n, n) + np.diag(3.0 * n * np.ones(n))
+        got = bs.block_inverse(x)
+        np.testing.assert_allclose(got, np.linalg.inv(x), rtol=1e-11, atol=1e-14)
 
 
 @pytest.mark.parametrize("n", [2, 7, 40, 96])

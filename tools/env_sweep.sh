@@ -3,7 +3,7 @@
 #   tools/env_sweep.sh "BSEL_SCHUR=1" "BSEL_LANE_INV_GRID=48" ...
 # One line per variant: value (ms) and forward / backward phases.
 for v in "" "$@"; do
-  out=$(env $v timeout 400 python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e --no-other-b --no-seq 2>/dev/null)
+  out=$(env $v timeout 400 python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e --no-other-b --no-seq --no-cfg5 2>/dev/null)
   echo "$out" | python -c "
 import json,sys
 try:

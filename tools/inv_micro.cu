@@ -47,6 +47,7 @@ int main() {
     cudaMalloc(&X, (size_t)n * n * 16);
     cudaMalloc(&Y, (size_t)n * n * 16);
     cudaMalloc(&W, (size_t)bsel::block_inverse_workspace(n) * 16);
+    cudaMemset(W, 0, (size_t)bsel::block_inverse_workspace(n) * 16);
     cudaMalloc(&flag, 4);
     cudaMemset(flag, 0, 4);
     fill<<<(n * n + 255) / 256, 256>>>(X, n, 7);
@@ -62,6 +63,7 @@ int main() {
     cudaMalloc(&X, (size_t)n * n * 16);
     cudaMalloc(&Y, (size_t)n * n * 16);
     cudaMalloc(&W, (size_t)bsel::block_inverse_workspace(n) * 16);
+    cudaMemset(W, 0, (size_t)bsel::block_inverse_workspace(n) * 16);
     cudaMalloc(&flag, 4);
     cudaMemset(flag, 0, 4);
     fill<<<(n * n + 255) / 256, 256>>>(X, n, 7);
