@@ -386,6 +386,8 @@ struct PinvSmem {
 };
 
 static_assert(sizeof(Leaf32) <= sizeof(PinvSmem::x), "leaf scratch must fit in PinvSmem::x");
+static_assert(2048 * (2 * sizeof(double2) + 2 * sizeof(int)) <= sizeof(PinvSmem),
+              "the dataflow kernel's in-kernel exact fallback (n <= 2048) must fit its shared memory");
 
 __device__ __forceinline__ void inv_cp16(void* smem, const void* gmem, bool pred) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -1013,6 +1015,8 @@ struct DfArgs {
   unsigned long long base;   // epoch * 256
   int b;
   int* flag;
+  unsigned long long* status;  // exact fallback (in-kernel): singular -> atomicMin(status, key)
+  unsigned long long key;
 };
 
 __global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_constant__ DfArgs g) {
@@ -1101,6 +1105,18 @@ __global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_consta
       if (threadIdx.x == 0) publish_flag(g.dv, base + p + 2);
       lap(kStPub);
     }
+    // Exact fallback in-kernel (no separate launch per inverse: under the
+    // concurrent GEMM levels a 1024-thread fallback CTA waited for an SM on
+    // every chain step).  Once every worker is past its last panel (growth
+    // flags are raised during the panels, the last one wrote Y), a flagged
+    // inverse is recomputed from X by full-column partial pivoting.
+    if (threadIdx.x >= 1 && threadIdx.x < G) wait_ge(g.prog + threadIdx.x, base + nt);
+    __syncthreads();
+    int fl;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(fl) : "l"(g.flag) : "memory");
+    if (fl == 1 && exact_gj(g.in.p[0], g.in.ld[0], g.y.p[0], g.y.ld[0], b, g.s1.p[0], g.flag, g.status, g.key) &&
+        threadIdx.x == 0)
+      *g.flag = 0;
     if (st) atomicAdd(g.stats + kStKernel, st_t);
     return;
   }
@@ -1243,8 +1259,18 @@ bool dataflow_enabled() {
 
 std::atomic<unsigned long long> g_inverse_epoch{0};
 
+// BSEL_INV_DF_COOP=1: cooperative launch of the dataflow kernel (experiment).
+bool dataflow_coop() {
+  static const bool on = [] {
+    const char* e = getenv("BSEL_INV_DF_COOP");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
 cudaError_t launch_dataflow(const double2* X, int64_t ldx, double2* Y, int64_t ldy, int n, double2* sync,
-                            double2* scratch, int* flag, int grid, cudaStream_t stream) {
+                            double2* scratch, int* flag, unsigned long long* status, unsigned long long key,
+                            int grid, cudaStream_t stream) {
   const cudaError_t attr = per_device([] {
     return cudaFuncSetAttribute(dataflow_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(PinvSmem));
@@ -1264,11 +1290,18 @@ cudaError_t launch_dataflow(const double2* X, int64_t ldx, double2* Y, int64_t l
   g.base = (g_inverse_epoch.fetch_add(1) + 1) << 8;
   g.b = n;
   g.flag = flag;
+  g.status = status;
+  g.key = key;
   g.stats = inverse_stats();
   (void)ntq;
-  void* args[] = {(void*)&g};
-  const cudaError_t err =
-      cudaLaunchCooperativeKernel((const void*)dataflow_gj_kernel, grid, 256, args, sizeof(PinvSmem), stream);
+  cudaError_t err;
+  if (dataflow_coop()) {
+    void* args[] = {(void*)&g};
+    err = cudaLaunchCooperativeKernel((const void*)dataflow_gj_kernel, grid, 256, args, sizeof(PinvSmem), stream);
+  } else {
+    dataflow_gj_kernel<<<grid, 256, sizeof(PinvSmem), stream>>>(g);
+    err = cudaGetLastError();
+  }
   count_launch();
   return err;
 }
@@ -1451,9 +1484,9 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     const int cap = grid_req > 0 ? grid_req : inverse_grid_cap();
     if (grid > cap) grid = cap;
     if (dataflow_enabled() && grid >= 2 && grid <= kSyncCtas && panels * panels <= kSyncTiles) {
-      err = launch_dataflow(X, ldx, Y, ldy, n, sync, work, flag, grid, stream);
-      if (err != cudaSuccess) return err;
-      goto fallback;
+      // the exact fallback runs inside the dataflow kernel (n <= 2048: its
+      // n * 40 B of shared memory fit the kernel's)
+      return launch_dataflow(X, ldx, Y, ldy, n, sync, work, flag, status, key, grid, stream);
     }
     GjArgs g{};
     g.in = quad1(X, ldx);
@@ -1470,7 +1503,6 @@ cudaError_t launch_block_inverse(const double2* X, int64_t ldx, double2* Y, int6
     err = levels_inverse(X, ldx, Y, ldy, n, work, flag, stream);
   }
   if (err != cudaSuccess) return err;
-fallback:
   // Exact fallback (no-op unless a leaf met an exactly zero pivot).
   const size_t smem = (size_t)n * (2 * sizeof(double2) + 2 * sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
