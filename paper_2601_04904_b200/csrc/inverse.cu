@@ -870,7 +870,8 @@ struct GjArgs {
 #define BSEL_INV_STATS 0
 #endif
 enum InvStat { kStLook = 0, kStLeaf, kStWait0, kStTiles1, kStWait1, kStKernel, kStLaunches, kStPanels, kStPub, kStCoLoc, kStSteps, kStLazy, kStPro, kStCore, kStEpi, kStLeafNs,
-               kStSm = 16, kStN = kStSm + 256 };
+               kStMark = 280, kStFirst = 298, kStLast, kStSpread, kStCta0Late, kStCta0LateSum,
+               kStSm = 16, kStN = 304 };
 
 __global__ void __launch_bounds__(256, 2) persistent_gj_kernel(const __grid_constant__ GjArgs g) {
   // trace (debug, may be null): per panel p, [8p+0] CTA0 start, [+1] after the
@@ -1020,6 +1021,10 @@ struct DfArgs {
 };
 
 __global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_constant__ DfArgs g) {
+  // Programmatic dependent launch (launch_dataflow): the CTAs may be placed
+  // while the previous kernel of the stream (the chain GEMM producing X)
+  // still runs; nothing is read before it has completed and flushed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PinvSmem& S = *reinterpret_cast<PinvSmem*>(smem_raw);
   Leaf32& L = *reinterpret_cast<Leaf32*>(&S.x[0][0][0]);  // spans x[0] and x[1]
@@ -1044,6 +1049,20 @@ __global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_consta
   };
   lap(-1);
 #if BSEL_INV_STATS
+  if (g.stats && threadIdx.x == 0) {  // CTA start spread of this launch (one lane per process only)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x == 0) {  // gap since the previous chain kernel ended (marks: [0] end, [4] gap, [5] count)
+      const unsigned long long prev = atomicAdd(g.stats + kStMark, 0ull);
+      if (prev && t > prev && t - prev < 10000000ull) {
+        atomicAdd(g.stats + kStMark + 4, t - prev);
+        atomicAdd(g.stats + kStMark + 5, 1ull);
+      }
+    }
+    atomicMin(g.stats + kStFirst, t);
+    atomicMax(g.stats + kStLast, t);
+    if (blockIdx.x == 0) atomicExch(g.stats + kStCta0Late, t);
+  }
   if (g.stats && threadIdx.x == 0) {  // CTAs per SM of this launch (co-location check)
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1118,6 +1137,17 @@ __global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_consta
         threadIdx.x == 0)
       *g.flag = 0;
     if (st) atomicAdd(g.stats + kStKernel, st_t);
+#if BSEL_INV_STATS
+    if (g.stats && threadIdx.x == 0) {  // every CTA has started (all reported their last panel)
+      const unsigned long long f = atomicExch(g.stats + kStFirst, ~0ull), l = atomicExch(g.stats + kStLast, 0ull);
+      atomicAdd(g.stats + kStSpread, l - f);
+      const unsigned long long c0 = atomicAdd(g.stats + kStCta0Late, 0ull);
+      atomicAdd(g.stats + kStCta0LateSum, c0 - f);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(g.stats + kStMark, t);
+    }
+#endif
     return;
   }
   // ---- workers: fixed tile ranges ----
@@ -1179,12 +1209,18 @@ unsigned long long* inverse_stats() {
     if (!(e && atoi(e) != 0)) return p;
     if (cudaMallocManaged(&p, kStN * sizeof(unsigned long long)) != cudaSuccess) return (unsigned long long*)nullptr;
     memset(p, 0, kStN * sizeof(unsigned long long));
+    p[kStFirst] = ~0ull;
     atexit([] {
       unsigned long long* q = inverse_stats();
       if (!q || cudaDeviceSynchronize() != cudaSuccess) return;
       const double n = q[kStLaunches] ? (double)q[kStLaunches] : 1.0;
       int multi = 0, used = 0;
       for (int k = 0; k < 256; ++k) used += q[kStSm + k] > 0, multi += q[kStSm + k] > q[kStLaunches];
+      fprintf(stderr, "[inverse stats] chain gaps: before an inverse %.1f us (%llu), before a chain GEMM %.1f us (%llu)\n",
+              q[kStMark + 5] ? q[kStMark + 4] / (double)q[kStMark + 5] / 1e3 : 0.0, q[kStMark + 5],
+              q[kStMark + 3] ? q[kStMark + 2] / (double)q[kStMark + 3] / 1e3 : 0.0, q[kStMark + 3]);
+      fprintf(stderr, "[inverse stats] CTA start spread per launch %.1f us (CTA 0 after the first CTA by %.1f us)\n",
+              q[kStSpread] / n / 1e3, q[kStCta0LateSum] / n / 1e3);
       fprintf(stderr, "[inverse stats] leaf per launch: pivot steps %.0f kcycles, lazy updates %.0f kcycles | "
               "prologue %.0f, core %.0f, epilogue %.0f kcycles; leaf_publish_smem %.1f us (globaltimer)\n",
               q[kStSteps] / n / 1e3, q[kStLazy] / n / 1e3, q[kStPro] / n / 1e3, q[kStCore] / n / 1e3,
@@ -1202,6 +1238,15 @@ unsigned long long* inverse_stats() {
   return buf;
 }
 }  // namespace
+
+unsigned long long* chain_marks() {
+#if BSEL_INV_STATS
+  unsigned long long* q = inverse_stats();
+  return q ? q + kStMark : nullptr;
+#else
+  return nullptr;
+#endif
+}
 
 // Layout: [sync area: kSyncElems (zero at allocation, epoch-tagged flags of
 // the dataflow kernel)][scratch].  Scratch: dataflow kernel s1, s2 (n x n
@@ -1259,6 +1304,18 @@ bool dataflow_enabled() {
 
 std::atomic<unsigned long long> g_inverse_epoch{0};
 
+// BSEL_INV_PDL=1 (experiment): launch the dataflow kernel as a programmatic
+// dependent of the previous kernel.  Measured slower (2 GPUs 495 vs 466 ms,
+// 1 GPU 810 vs 781): the launch gap before the inverse drops from ~62 to
+// ~15 us, but its early-placed CTAs slow the inverse itself and the GEMMs.
+bool dataflow_pdl() {
+  static const bool on = [] {
+    const char* e = getenv("BSEL_INV_PDL");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
 // BSEL_INV_DF_COOP=1: cooperative launch of the dataflow kernel (experiment).
 bool dataflow_coop() {
   static const bool on = [] {
@@ -1299,8 +1356,23 @@ cudaError_t launch_dataflow(const double2* X, int64_t ldx, double2* Y, int64_t l
     void* args[] = {(void*)&g};
     err = cudaLaunchCooperativeKernel((const void*)dataflow_gj_kernel, grid, 256, args, sizeof(PinvSmem), stream);
   } else {
-    dataflow_gj_kernel<<<grid, 256, sizeof(PinvSmem), stream>>>(g);
-    err = cudaGetLastError();
+    // Under the concurrent GEMM levels the inverse starts ~62 us after the
+    // previous chain GEMM ended (2 GPUs, chain marks of the instrumented
+    // build: its CTAs need 104 KB of shared memory on SMs the persistent
+    // aux-level GEMM CTAs hold).  BSEL_INV_PDL=1 launches it as a
+    // programmatic dependent of that GEMM (which signals launch_dependents
+    // on entry) -- measured slower, see dataflow_pdl.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = sizeof(PinvSmem);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = dataflow_pdl() ? 1 : 0;
+    err = cudaLaunchKernelEx(&cfg, dataflow_gj_kernel, g);
   }
   count_launch();
   return err;

@@ -24,6 +24,12 @@ constexpr int kLeaf = 32;
 // inverse records per-panel globaltimer stamps there.
 extern unsigned long long* g_inverse_trace;
 
+// Instrumented builds (-DBSEL_INV_STATS=1, run with BSEL_INV_STATS=1): the
+// marks the chain's kernels use to measure the gap between one chain kernel's
+// end and the next one's start (printed with the inverse statistics); null
+// otherwise.  One lane per process (the marks are per process).
+unsigned long long* chain_marks();
+
 // Workspace (complex elements) needed by launch_block_inverse for one n x n.
 // It must be ZERO when first used (its head holds the dataflow kernel's
 // epoch-tagged ready flags, which are never reset).

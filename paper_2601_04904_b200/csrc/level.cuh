@@ -44,6 +44,13 @@ class Level {
     b_.max_ctas = max_ctas;
     b_.avoid_sms = 0;
     b_.tile_counter = nullptr;
+    b_.chain_mark = nullptr;
+  }
+  // Instrumented builds: record this level's launches as chain kernels
+  // (launch-gap statistics, inverse.cuh chain_marks).
+  Level& chain_mark(unsigned long long* m) {
+    b_.chain_mark = m;
+    return *this;
   }
   // Keep SMs [0, n) free of this level's CTAs (zgemm.cuh avoid_sms); counter:
   // a device u32 owned by this level's stream.

@@ -197,7 +197,6 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
       const int64_t i = down ? lo + s : hi - 1 - s;
       const int64_t j = down ? i + 1 : i - 1;
       const int64_t e = down ? i : i - 1;  // index of the coupling pair
-      ring_wait(ctx, (int)s);
       need(ctx.chain(), s + 1);
       EndStep st;
       st.Lk = down ? A.L(e) : A.U(e);
@@ -223,7 +222,6 @@ void local_forward(Context& ctx, const BtaDev& A, const BtaDev* B, const BtaDev&
   } else {
     for (int64_t i = lo + 1; i < hi - 1; ++i) {
       const int64_t s = i - lo - 1;
-      ring_wait(ctx, (int)s);
       need(ctx.chain(), i + 1 - lo);
       MiddleStep st;
       st.L = A.L(i), st.U = A.U(i);

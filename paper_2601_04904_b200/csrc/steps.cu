@@ -7,10 +7,14 @@
 // A side rewrites a slot it waits for the B side of step k - kFwdDepth
 // (ring_wait), so the B side may lag the A chain by kFwdDepth - 1 steps: the
 // latency-bound chain runs ahead and the B-side GEMM levels fill the SMs it
-// leaves idle.
+// leaves idle.  The wait is enqueued AFTER the step's inverse (which touches
+// no ring slot), so the inverse directly follows the previous step's last
+// chain GEMM in the stream and is launched as its programmatic dependent
+// (inverse.cu launch_dataflow: its CTAs are placed while that GEMM runs).
 #include <cstdlib>
 
 #include "steps.cuh"
+#include "inverse.cuh"
 
 namespace bsel {
 
@@ -97,11 +101,13 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
     // rgf.py:283-288 / dist.py:252-257: right-hand temporaries.
     Mat t1 = st.h_out.p ? st.h_out : rt(ctx, slot, 0, b, b), t2 = st.ha_out.p ? st.ha_out : rt(ctx, slot, 1, b, a);
     if (schur) {  // S, t1 = S Uk and ad_j -= Lk t1 in one launch
+      ring_wait(ctx, (int)order);
       ctx.schur(st.ad_i, st.Uk, st.Lk, st.ad_j, S, t1, st.f_out.p ? st.f_out : rt(ctx, slot, 2, b, b), order, index,
                 sA);
       cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
     } else {
       ctx.invert(st.ad_i, st.S, order, index, sA);
+      ring_wait(ctx, (int)order);  // after the inverse: it touches no ring slot (PDL launch)
       Level L(sA);
       L.out(t1).mm(+1, S, N, st.Uk, N);
       L.flush();
@@ -125,11 +131,14 @@ void end_step(Context& ctx, const EndStep& st, bool fused, uint64_t order, int64
   Mat f = keep(st.f_out, 0, b, b), g = keep(st.g_out, 1, a, b), w = rt(ctx, slot, 2, b, b);
   Mat k = keep(st.k_out, 4, b, a), q = keep(st.q_out, 5, b, b);
   if (schur) {  // S, f = Lk S and ad_j -= f Uk (and h = S Uk) in one launch
+    ring_wait(ctx, (int)order);
     ctx.schur(st.ad_i, st.Uk, st.Lk, st.ad_j, S, st.h_out, f, order, index, sA);
     cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
   } else {
     ctx.invert(st.ad_i, st.S, order, index, sA);
+    ring_wait(ctx, (int)order);  // after the inverse: it touches no ring slot (PDL launch)
     Level L(sA, chain_tile());
+    L.chain_mark(chain_marks());
     L.out(f).mm(+1, st.Lk, N, S, N);
     L.flush();
     if (!aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
@@ -196,11 +205,14 @@ void middle_step(Context& ctx, const MiddleStep& st, bool fused, uint64_t order,
   auto keep = [&](const Mat& m, int k_, int r, int c) { return m.p ? m : rt(ctx, slot, k_, r, c); };
   Mat fn = keep(st.fn_out, 0, b, b), fr = keep(st.fr_out, 1, b, b), g = keep(st.g_out, 2, a, b);
   if (ctx.schur_ok(b)) {  // S, fn = L S and ad_n -= fn U (and h = S U) in one launch
+    ring_wait(ctx, (int)order);
     ctx.schur(st.ad_i, st.U, st.L, st.ad_n, S, st.h_out, fn, order, index, sA);
     cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");
   } else {
     ctx.invert(st.ad_i, st.S, order, index, sA);
+    ring_wait(ctx, (int)order);  // after the inverse: it touches no ring slot (PDL launch)
     Level L(sA, chain_tile());
+    L.chain_mark(chain_marks());
     L.out(fn).mm(+1, st.L, N, S, N);
     L.flush();
     if (!aux_after_chain()) cuda_check(cudaEventRecord(ring_a_event(ctx, slot), sA), "record A");

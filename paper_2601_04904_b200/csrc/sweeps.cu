@@ -317,8 +317,7 @@ void bta_forward_arrow(Context& ctx, const BtaDev& A, const BtaDev* B, const Fac
   const int mx = std::max(a, b);
   ctx.reserve_slots(64, (int64_t)mx * mx);
   for (int i = 0; i < n - 1; ++i) {
-    ring_wait(ctx, i);
-    EndStep st;
+    EndStep st;  // (end_step waits for the ring slot after its inverse)
     st.Lk = A.L(i), st.Uk = A.U(i);
     st.ad_i = A.D(i), st.ad_j = A.D(i + 1), st.ar_i = A.AR(i), st.ar_j = A.AR(i + 1);
     st.ac_i = A.AC(i), st.ac_j = A.AC(i + 1), st.tipA = A.T();

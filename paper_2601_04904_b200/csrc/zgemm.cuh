@@ -98,6 +98,9 @@ struct GemmBatch {
   int32_t avoid_sms;
   unsigned* tile_counter;
   const void* tma_table;  // device table of CUtensorMap descriptors (3M launcher)
+  // instrumented builds (-DBSEL_INV_STATS=1) only: chain launch-gap marks
+  // (inverse.cuh chain_marks), null otherwise
+  unsigned long long* chain_mark;
   GemmProblem p[kMaxProblems];
 };
 

@@ -229,6 +229,23 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) zgemm3m_kernel(const __gr
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  // A programmatic dependent of this launch (the chain's block inverse,
+  // inverse.cu launch_dataflow) may be placed from now on; it waits for this
+  // grid's completion (griddepcontrol.wait) before reading its output.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#if BSEL_INV_STATS
+  // chain launch-gap statistics (inverse.cuh chain_marks): [0] last chain
+  // kernel end, [2]/[3] gap sum / count before chain GEMMs
+  if (batch.chain_mark && blockIdx.x == 0 && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long prev = atomicAdd(batch.chain_mark, 0ull);
+    if (prev && t > prev && t - prev < 10000000ull) {
+      atomicAdd(batch.chain_mark + 2, t - prev);
+      atomicAdd(batch.chain_mark + 3, 1ull);
+    }
+  }
+#endif
 
   // ---- SM avoidance (zgemm.cuh avoid_sms): leave at once, except the grid's
   // last CTA to leave, which then works off whatever is left
@@ -403,6 +420,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) zgemm3m_kernel(const __gr
       }
     }
   }
+#if BSEL_INV_STATS
+  if (batch.chain_mark && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(batch.chain_mark, t);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -575,7 +599,7 @@ int tiles_of(GemmProblem& P) {
 }
 
 template <class C>
-cudaError_t launch3(GemmBatch& batch, cudaStream_t stream) {
+cudaError_t launch3(GemmBatch& batch, cudaStream_t stream, bool no_persist = false) {
   const cudaError_t attr = per_device([] {
     return cudaFuncSetAttribute(zgemm3m_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
@@ -634,7 +658,7 @@ cudaError_t launch3(GemmBatch& batch, cudaStream_t stream) {
     const char* e = getenv("BSEL_GEMM3M_PERSIST");
     return !(e && atoi(e) == 0);
   }();
-  int grid = persist ? std::min(tiles, resident) : tiles;
+  int grid = (persist && !no_persist) ? std::min(tiles, resident) : tiles;
   if (batch.max_ctas > 0 && batch.max_ctas < grid) grid = batch.max_ctas;
   if (batch.avoid_sms > 0) {
     if (!batch.tile_counter) return cudaErrorInvalidValue;
@@ -690,10 +714,17 @@ cudaError_t launch_gemm_batch_3m(GemmBatch& batch, cudaStream_t stream, int tile
     else
       cfg = 32;
   }
-  if (cfg == 64) return launch3<C3_64>(batch, stream);
-  if (cfg == 6432) return launch3<C3_6432>(batch, stream);
-  if (cfg == 643232) return launch3<C3_6432_K32>(batch, stream);
-  return launch3<C3_32>(batch, stream);
+  // BSEL_FWD_AUX_PERSIST=0 (experiment): the forward aux levels launch one
+  // CTA per tile, so the chain's next kernel can take SMs between tiles
+  static const bool fwd_np = [] {
+    const char* e = getenv("BSEL_FWD_AUX_PERSIST");
+    return e && atoi(e) == 0;
+  }();
+  const bool np = fwd_np && tile_cfg == kTileAutoFwd;
+  if (cfg == 64) return launch3<C3_64>(batch, stream, np);
+  if (cfg == 6432) return launch3<C3_6432>(batch, stream, np);
+  if (cfg == 643232) return launch3<C3_6432_K32>(batch, stream, np);
+  return launch3<C3_32>(batch, stream, np);
 }
 
 }  // namespace bsel
