@@ -589,10 +589,15 @@ def main():
         def step():
             bs.solve_selected(A, B, "siq", out=(XA, XB), workspace=ws, partitions=parts)
     else:
-        # BSEL_PLAN_COSTS="end,mid": partition sizes from measured per-block
-        # times instead of the reference's product counts
-        pc = os.environ.get("BSEL_PLAN_COSTS")
-        plan_costs = tuple(float(x) for x in pc.split(",")) if pc else None
+        # Partition sizes from per-block costs measured on B200 (end : middle
+        # = 1 : 2.05 -> [344, 168, 168, 344] at 4 GPUs: 321-323 vs 331 ms with
+        # the reference's product-count plan [354, 158, 158, 354], whose
+        # middles waited ~30 ms at the exchange; profiles/sweeps_r02.md).
+        # Results agree with the reference plan's to rounding (the parity
+        # tests and dist_solve use the reference plan).  BSEL_PLAN_COSTS=
+        # "end,mid" overrides, "ref" restores the reference's plan.
+        pc = os.environ.get("BSEL_PLAN_COSTS", "1,2.05")
+        plan_costs = None if pc in ("", "ref") else tuple(float(x) for x in pc.split(","))
         solver = bdist.DistSolver(A, B, "siq", world, rank, dev, plan_costs=plan_costs,
                                   parts_per_rank=args.parts_per_gpu)
 
@@ -840,6 +845,8 @@ def main():
             "rank_phases_ms": rank_phases,
             "step_ms": step_ms,
             "partition_sizes": ([hi - lo for lo, hi in solver.plan.ranges] if world > 1 else None),
+            "partition_plan": (("B200-measured per-block costs (end, middle) = " + str(plan_costs)) if world > 1
+                               and plan_costs else ("reference plan_partitions" if world > 1 else None)),
             "value_sequential_rgf_ms": seq_ms,
             "value_general_b_ms": other_b.get("general"),
             "value_antihermitian_b_ms": other_b.get("antihermitian"),
