@@ -93,12 +93,15 @@ def to_host(d: DeviceBta, *, pinned=False) -> BtaMatrix:
     return out
 
 
-def generate_dd_bta_device(n, b, a, seed, dominance=1.5, device=None, *, out=None) -> DeviceBta:
+def generate_dd_bta_device(n, b, a, seed, dominance=1.5, device=None, *, out=None, _lane: int = 0) -> DeviceBta:
     """generate_dd_bta (matrix.py:224-284) computed on the GPU: the same
     splitmix64 stream bit for bit; the dominance shift's |row| sums are
     accumulated sequentially (host: numpy pairwise), so shifted diagonal
     entries may differ from the host generator in the last bit.  ``out``:
-    an existing DeviceBta of the shape to overwrite (on the current stream)."""
+    an existing DeviceBta of the shape to overwrite (on the current stream).
+    ``_lane`` (internal): native context lane -- callers generating from
+    several host threads at once (EnergySweep pipes) need lanes of their own,
+    because a context's stream binding is per context, not per thread."""
     import ctypes
 
     if n < 1 or b < 1 or a < 0:
@@ -107,7 +110,7 @@ def generate_dd_bta_device(n, b, a, seed, dominance=1.5, device=None, *, out=Non
         if out.shape_params != (n, b, a):
             raise ShapeMismatchError("out has a different shape")
         device = out.device
-    ctx = _native.Context.get(None if device is None else torch.device(device).index)
+    ctx = _native.Context.get(None if device is None else torch.device(device).index, lane=_lane)
     if out is None:
         out = DeviceBta.empty(n, b, a, torch.device("cuda", ctx.device), zero=False)
     d = out.desc()
@@ -116,11 +119,12 @@ def generate_dd_bta_device(n, b, a, seed, dominance=1.5, device=None, *, out=Non
     return out
 
 
-def hermitianize_device(m: DeviceBta) -> DeviceBta:
-    """In-place (m + m^H)/2 on the pattern (matrix.py:337-354); returns m."""
+def hermitianize_device(m: DeviceBta, *, _lane: int = 0) -> DeviceBta:
+    """In-place (m + m^H)/2 on the pattern (matrix.py:337-354); returns m.
+    ``_lane``: see generate_dd_bta_device."""
     import ctypes
 
-    ctx = _native.Context.get(m.device.index)
+    ctx = _native.Context.get(m.device.index, lane=_lane)
     d = m.desc()
     ctx.bind_stream()
     ctx.call("bsel_hermitianize", ctypes.byref(d))

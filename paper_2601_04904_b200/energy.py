@@ -107,9 +107,14 @@ class EnergySweep:
         with torch.cuda.device(self.device), torch.cuda.stream(g):
             if pipe["free"][slot] is not None:
                 g.wait_event(pipe["free"][slot])
-            generate_dd_bta_device(self.n, self.b, self.a, sa, self.dominance, out=A)
+            # a generator context of this pipe: with concurrent pipes (host
+            # threads), the default context is pipe 0's solve context, whose
+            # stream binding another thread must not change mid-solve
+            lane = 0 if self.concurrent == 1 else 2000 + self.pipes.index(pipe)
+            generate_dd_bta_device(self.n, self.b, self.a, sa, self.dominance, out=A, _lane=lane)
             if B is not None:
-                hermitianize_device(generate_dd_bta_device(self.n, self.b, self.a, sb, self.dominance, out=B))
+                hermitianize_device(generate_dd_bta_device(self.n, self.b, self.a, sb, self.dominance, out=B,
+                                                           _lane=lane), _lane=lane)
             ready = torch.cuda.Event()
             ready.record(g)
         return ready
