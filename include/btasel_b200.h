@@ -98,8 +98,9 @@ int bsel_context_destroy(bsel_context_t* ctx);
 /* Run subsequent calls on `cuda_stream` (cudaStream_t; NULL = legacy default). */
 int bsel_context_set_stream(bsel_context_t* ctx, void* cuda_stream);
 /* CTAs of the persistent block inverse on this context (0 = default: 64 or
- * BSEL_INV_GRID).  Contexts sweeping concurrently on one GPU (in-GPU
- * partitions) use fewer so the chains leave SMs to each other's GEMMs.    */
+ * BSEL_INV_GRID), for the sweeps and bsel_block_inverse.  Contexts sweeping
+ * concurrently on one GPU (in-GPU partitions) use fewer so the chains leave
+ * SMs to each other's GEMMs.                                                */
 int bsel_context_set_inverse_grid(bsel_context_t* ctx, int ctas);
 /* Symmetry of the right-hand side B.  Every forward entry point checks B
  * EXACTLY on its pattern (B = B^H, B = -B^H) while staging it; when B = s B^H

@@ -325,7 +325,8 @@ int bsel_block_inverse(bsel_context_t* ctx, const double* a, int64_t lda, double
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), s), "flag");
     cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), s), "flag");
     double2* work = cx.inv_work(block_inverse_workspace((int)n));
-    cudaError_t e = launch_block_inverse(dp(a), lda, dp(out), ldo, (int)n, work, flag, nullptr, 0, s);
+    cudaError_t e = launch_block_inverse(dp(a), lda, dp(out), ldo, (int)n, work, flag, nullptr, 0, s,
+                                         cx.inverse_grid());
     int h = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);

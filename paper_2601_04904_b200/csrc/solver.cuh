@@ -89,6 +89,7 @@ class Context {
   // CTAs of the persistent block inverse (0 = library default).  Fewer when
   // several contexts run sweeps concurrently on one GPU.
   void set_inverse_grid(int ctas) { inv_grid_ = ctas; }
+  int inverse_grid() const { return inv_grid_; }
   cudaStream_t stream() const { return user_stream_; }
   cudaStream_t aux() const { return aux_; }
   // High-priority stream for the latency-critical Schur chain (pivot

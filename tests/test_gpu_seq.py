@@ -15,6 +15,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 
 import oracle  # noqa: E402
 import paper_2601_04904_b200 as bs  # noqa: E402
+from paper_2601_04904_b200 import _native  # noqa: E402
 
 TOL = 1e-10
 rng = np.random.default_rng(20240901)
@@ -111,6 +112,35 @@ def test_block_inverse_singular_reports_row():
     assert info.value.index == 2
     np.testing.assert_allclose(bs.block_inverse(np.array([[2.0, 1.0], [1.0, 2.0]])),
                                [[2 / 3, -1 / 3], [-1 / 3, 2 / 3]], rtol=1e-14)
+
+
+@pytest.mark.parametrize("n,r", [(96, 50), (512, 300)])
+def test_block_inverse_singular_dataflow(n, r):
+    """Multi-panel blocks go through the dataflow kernel, whose exact fallback
+    runs inside the kernel: an exactly singular block is still reported with
+    its pivot row, and the next inverse on the same workspace is exact."""
+    x = crand(n, n) + np.diag(3.0 * n * np.ones(n))
+    x[r, :] = 0.0
+    x[:, r] = 0.0
+    with pytest.raises(bs.SingularBlockError) as info:
+        bs.block_inverse(x)
+    assert info.value.index == r
+    y = crand(n, n) + np.diag(3.0 * n * np.ones(n))
+    np.testing.assert_allclose(bs.block_inverse(y), np.linalg.inv(y), rtol=1e-11, atol=1e-14)
+
+
+@pytest.mark.parametrize("grid", [2, 3, 7, 40, 148])
+def test_block_inverse_grid_sizes(grid):
+    """Dataflow inverse with 1 .. 147 worker CTAs (tile ranges of 256 .. 2
+    tiles, ragged last ranges, empty ranges) and a ragged block size."""
+    ctx = _native.Context.get()
+    ctx.set_inverse_grid(grid)
+    try:
+        for n in (512, 200):
+            x = crand(n, n) + np.diag(3.0 * n * np.ones(n))
+            np.testing.assert_allclose(bs.block_inverse(x), np.linalg.inv(x), rtol=1e-11, atol=1e-14)
+    finally:
+        ctx.set_inverse_grid(0)
 
 
 # --------------------------------------------------------------------------
