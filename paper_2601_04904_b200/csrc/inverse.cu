@@ -442,6 +442,12 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
 // ordered before it (a preceding __threadfence, or fence.acq_rel + relaxed
 // store, measured the same).
 __device__ __forceinline__ void publish_flag(unsigned long long* p, unsigned long long v) { st_release(p, v); }
+// Several flags after the CTA's stores: ONE fence, then relaxed stores (the
+// release pattern; a release store per flag costs a MEMBAR each).
+__device__ __forceinline__ void release_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // Poll back-off: 32 ns (0 / 256 ns and relaxed polling with one final
 // acquire measured the same, tools/build_sweep.sh).
 __device__ __noinline__ void wait_ge_slow(const unsigned long long* p, unsigned long long target) {
@@ -794,13 +800,9 @@ __device__ void gj_tiles_df(PinvSmem& S, TileCtx& T, int t0, int t1, int skip, u
   b.has_x = false;
   auto publish_hot = [&](int kk, int kn) {  // after the last hot tile: flags of every hot tile
     if (flags && kk < len && kn >= len && threadIdx.x == 0) {
-      bool first = true;
+      release_fence();  // orders every hot tile's stores (ordered before it by the stage's barrier)
       for (int t = t0; t < t1; ++t)
-        if (t != skip && hot(t)) {
-          if (first) publish_flag(ver + t, done);  // orders every hot tile's stores
-          else st_release(ver + t, done);
-          first = false;
-        }
+        if (t != skip && hot(t)) st_relaxed(ver + t, done);
     }
   };
   constexpr int kNone = 1 << 30;
