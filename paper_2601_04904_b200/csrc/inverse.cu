@@ -1177,8 +1177,10 @@ __global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_consta
       }
     }
     __syncthreads();
-    load_tile(S.d, g.dinv + (int64_t)p * kT * kT, kT, kT, kT);
-    __syncthreads();
+    // Dinv_p arrives asynchronously with the first tile's operands (its
+    // cp.async group completes before that tile computes)
+    load_tile_async(S.d, g.dinv + (int64_t)p * kT * kT, kT, kT, kT);
+    inv_cp_commit();
     if (blockIdx.x == 1) lap(kStWait1);
     T.p = p;
     T.j0 = p * kT;
@@ -1189,6 +1191,7 @@ __global__ void __launch_bounds__(256, 2) dataflow_gj_kernel(const __grid_consta
     T.r_tk = -1;
     T.keep = false;
     gj_tiles_df(S, T, t0, t1, sp, T.final_ ? nullptr : g.ver, base + p + 1);
+    inv_cp_wait<0>();  // (a range without tiles never waited for its Dinv copy)
     __syncthreads();
     if (threadIdx.x == 0) st_release(g.prog + blockIdx.x, base + p + 1);
     if (blockIdx.x == 1) lap(kStTiles1);
