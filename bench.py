@@ -338,8 +338,9 @@ def pipelined_e2e(args, n, b, a, parts, hA, hB, hXA, hXB, single):
     return {"value": ms, "unit": "ms", "h2d_bytes_per_step": single["h2d_bytes_per_step"],
             "d2h_bytes_per_step": single["d2h_bytes_per_step"],
             "api": f"HostEnergySweep.run: {k} energy points from/to pinned host buffers, H2D of energy k+1 "
-                   f"and D2H of energy k-1 overlapped with energy k's solve (out_slots={slots}); "
-                   "timed region includes the first H2D and the last D2H",
+                   f"and D2H of energy k-1 overlapped with energy k's solve (out_slots={slots}; the last "
+                   "energy's outputs stream out behind its backward); timed region includes the first H2D "
+                   "and the last D2H",
             "single_call_ms": single["value"], "single_call_api": single["api"],
             "device_free_gib_before": round(free_gib, 1)}
 

@@ -246,8 +246,13 @@ class HostEnergySweep:
     out_slots=2, plus the ~36 GiB solve workspace).  ``out_slots=1`` keeps one
     device output set and streams it out behind each backward sweep instead
     (``solve_selected``'s host-output path); ``None`` = 2 when the buffers
-    fit.  Config 4: 1151 ms per energy over 16 energies with 2 slots
-    (steady state 1056-1074 ms), 1200 ms with 1.  The two-slot form needs the
+    fit.  With two slots the LAST energy streams its outputs out behind its
+    backward into its slot (no whole-matrix drain after the final solve) and
+    the first energy's inputs are loaded whole before it (streaming them
+    behind its forward delayed the second energy's load; BSEL_SWEEP_STREAM_
+    FIRST / _LAST switch both).  Config 4, 16 energies, round 2: 880 ms per
+    energy (steady state ~818 ms per energy; device-resident 784 ms); round
+    1: 1151 ms with 2 slots, 1200 ms with 1.  The two-slot form needs the
     solve's status / symmetry reads to bypass the copy engine (a small D2H
     waits behind the in-flight output D2H; they are published through mapped
     host memory, ``Context::publish_flags``).
@@ -324,8 +329,13 @@ class HostEnergySweep:
         # 1 measured 8.5 s for a streamed first energy with device outputs:
         # solve_selected copied the caller's device outputs to pageable host
         # memory for host inputs -- fixed in rgf.py.)
+        # Streaming the first energy's inputs behind its forward finishes it
+        # sooner but delays the second (its load then starts only after those
+        # inputs): config 4, 16 energies, 908 vs 898 ms per energy with the
+        # plain first load (tools/e2e_probe.py) -- off by default.
         stream_first = (self.parts > 1 and self.n >= 2 * self.parts
-                        and os.environ.get("BSEL_SWEEP_STREAM_FIRST", "1") != "0")
+                        and os.environ.get("BSEL_SWEEP_STREAM_FIRST", "0") != "0")
+        self._stream_last = os.environ.get("BSEL_SWEEP_STREAM_LAST", "1") != "0"
         self.done_events = []
         ready = None if stream_first else self._load(inputs[0], 0, None)
         k = 0
@@ -352,7 +362,15 @@ class HostEnergySweep:
                 if k + 1 < len(inputs):
                     io["on_inputs_done"] = lambda ev: held.append(self._load(inputs[k + 1], s ^ 1, ev))
                 kw = {"_device_in": (A, B), "_io_events": io}
-            if self.out is None:
+            # The last energy streams its outputs out behind its backward sweeps
+            # (the form out_slots=1 uses for every energy): a whole-matrix D2H
+            # after its solve would be an unoverlapped 34 GB drain at config 4.
+            last_streamed = self.out is not None and k == len(inputs) - 1 and k > 0 and self._stream_last
+            if self.out is None or last_streamed:
+                if last_streamed:  # device storage behind the streamed outputs: this energy's output slot
+                    if out_free[k % 2] is not None:
+                        main.wait_event(out_free[k % 2])
+                    kw["_device_out"] = self.out[k % 2]
                 solve_selected(src[0], src[1], self.mode, out=host_out, partitions=self.parts, timings=timings,
                                **kw)
                 done = torch.cuda.Event(enable_timing=True)

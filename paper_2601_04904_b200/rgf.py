@@ -298,7 +298,7 @@ def release_caches() -> None:
 
 def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal_only=False,
                    out=None, workspace=None, partitions=None, _b_symmetry=None, _device_in=None,
-                   _io_events=None, _pipe=0) -> SelectedSolution:
+                   _io_events=None, _pipe=0, _device_out=None) -> SelectedSolution:
     """Selected inverse of ``a`` and, in fused mode, the selected quadratic
     solution for ``b`` (rgf.py:497-531).  Never mutates its inputs.
 
@@ -321,7 +321,7 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
     parts = default_partitions(n) if partitions is None else int(partitions)
     if parts > 1 and n >= 2 * parts:
         return _solve_partitioned(a, b if fused else None, mode, parts, counter, timings, diagonal_only, out,
-                                  _device_in, _io_events, _pipe)
+                                  _device_in, _io_events, _pipe, _device_out)
     ctx, device = _ctx_for(a, _pipe)
     host = not isinstance(a, DeviceBta)
     A = DeviceBta.empty(n, bs, asz, device, zero=False).copy_from_host(a) if host else a
@@ -382,12 +382,13 @@ def solve_selected(a, b=None, mode=None, *, counter=None, timings=None, diagonal
 
 
 def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, device_in=None, io_events=None,
-                       pipe=0):
+                       pipe=0, device_out=None):
     """solve_selected through InGpuPartitions (dist.py) with cached buffers.
 
     ``device_in`` (internal, HostEnergySweep): device storage for streamed
     host inputs instead of a fresh allocation; ``io_events`` receives
-    "inputs_done", the event after the last streamed input chunk."""
+    "inputs_done", the event after the last streamed input chunk;
+    ``device_out``: device storage behind streamed host outputs."""
     from .dist import InGpuPartitions
 
     n, bs, asz = a.shape_params
@@ -417,6 +418,8 @@ def _solve_partitioned(a, b, mode, parts, counter, timings, diagonal_only, out, 
         runner = _PARTITIONED[key] = InGpuPartitions((n, bs, asz), mode, parts, device, lane_base=pipe * parts,
                                                      pipe=pipe)
     dev_out = out if (out is not None and isinstance(out[0], DeviceBta)) else None
+    if dev_out is None and stream_out and device_out is not None:
+        dev_out = device_out
     if stream_in or stream_out:
         XA, XB = runner.run(A, B, out=dev_out, host_in=(a, b) if stream_in else None,
                             host_out=host_out if stream_out else None)
