@@ -362,11 +362,32 @@ def dist_e2e(args, solver, A, B, n, world, rank, dev, dist):
     torch.cuda.synchronize()
     solver.solve(host_in=hin, host_out=hout)
     torch.cuda.synchronize()
+    # One streamed call per energy (default), or BSEL_DIST_E2E=pipelined:
+    # DistSolver.solve_energies (energy k+1's window copied in and energy
+    # k-1's outputs copied out while energy k solves) when its extra device
+    # input / output sets fit on every rank.  At 2 GPUs the pipelined form
+    # measured 882 vs 822 ms: the ranks share the host's PCIe / memory
+    # bandwidth (68.6 GB per energy in total), which bounds both forms.
+    form = "single"
+    if os.environ.get("BSEL_DIST_E2E", "single") == "pipelined" and solver.k == 1:
+        try:
+            solver.solve_energies([hin] * 2, [hout] * 2)  # warm: allocates the second slots
+            torch.cuda.synchronize()
+            form = "pipelined"
+        except torch.cuda.OutOfMemoryError:
+            solver._slot1 = None
+            torch.cuda.empty_cache()
+    ok = torch.tensor([1.0 if form == "pipelined" else 0.0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    form = "pipelined" if ok.item() > 0 else "single"
     dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(args.steps):
-        solver.solve(host_in=hin, host_out=hout)
+    if form == "pipelined":
+        solver.solve_energies([hin] * args.steps, [hout] * args.steps)
+    else:
+        for _ in range(args.steps):
+            solver.solve(host_in=hin, host_out=hout)
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / args.steps
@@ -380,8 +401,13 @@ def dist_e2e(args, solver, A, B, n, world, rank, dev, dist):
     dist.all_reduce(stats, op=dist.ReduceOp.SUM)
     return {"value": float(mx.item()), "unit": "ms", "h2d_bytes_per_step": int(stats[1].item()),
             "d2h_bytes_per_step": int(stats[2].item()),
-            "note": "per rank: its partition + separators + tip streamed in behind the forward, its owned "
-                    "solution blocks streamed out behind the backward; max over ranks"}
+            "form": form,
+            "note": ("per rank: its partition + separators + tip copied host->device for energy k+1 and its "
+                     "owned solution blocks of energy k-1 copied back while energy k solves "
+                     "(DistSolver.solve_energies, steps = energies, first load and last copy-out timed)"
+                     if form == "pipelined" else
+                     "per rank: its partition + separators + tip streamed in behind the forward, its owned "
+                     "solution blocks streamed out behind the backward; max over ranks")}
 
 
 def cfg5_side_measurement(args, dev):

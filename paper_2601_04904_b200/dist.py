@@ -719,20 +719,38 @@ class HostWindow:
     def shape_params(self):
         return self.n, self.b, self.a
 
-    def fill_from(self, m: DeviceBta) -> "HostWindow":
+    def fill_from(self, m: DeviceBta, *, non_blocking=False, tip=True) -> "HostWindow":
         """Copy the window's blocks out of a full-size device matrix."""
         lo, hi, c = self.lo, self.hi, self.c_hi
-        self.diag.copy_(m.diag[lo:hi])
-        self.arrow_row.copy_(m.arrow_row[lo:hi])
-        self.arrow_col.copy_(m.arrow_col[lo:hi])
+        nb = dict(non_blocking=non_blocking)
+        self.diag.copy_(m.diag[lo:hi], **nb)
+        self.arrow_row.copy_(m.arrow_row[lo:hi], **nb)
+        self.arrow_col.copy_(m.arrow_col[lo:hi], **nb)
         if c > lo:
-            self.lower.copy_(m.lower[lo:c])
-            self.upper.copy_(m.upper[lo:c])
-        self.tip.copy_(m.tip)
+            self.lower.copy_(m.lower[lo:c], **nb)
+            self.upper.copy_(m.upper[lo:c], **nb)
+        if tip:
+            self.tip.copy_(m.tip, **nb)
         for g, (lw, up) in self.separators.items():
-            lw.copy_(m.lower[g])
-            up.copy_(m.upper[g])
+            lw.copy_(m.lower[g], **nb)
+            up.copy_(m.upper[g], **nb)
         return self
+
+    def copy_to(self, m: DeviceBta) -> DeviceBta:
+        """Copy the window's blocks into a full-size device matrix (current
+        stream, asynchronous: the window is pinned)."""
+        lo, hi, c = self.lo, self.hi, self.c_hi
+        m.diag[lo:hi].copy_(self.diag, non_blocking=True)
+        m.arrow_row[lo:hi].copy_(self.arrow_row, non_blocking=True)
+        m.arrow_col[lo:hi].copy_(self.arrow_col, non_blocking=True)
+        if c > lo:
+            m.lower[lo:c].copy_(self.lower, non_blocking=True)
+            m.upper[lo:c].copy_(self.upper, non_blocking=True)
+        m.tip.copy_(self.tip, non_blocking=True)
+        for g, (lw, up) in self.separators.items():
+            m.lower[g].copy_(lw, non_blocking=True)
+            m.upper[g].copy_(up, non_blocking=True)
+        return m
 
     def separator(self, g):
         if self.lo <= g < self.c_hi:
@@ -1232,6 +1250,78 @@ class DistSolver:
         tm.stop("step")
         self._tm = tm
         return self.out
+
+    def solve_energies(self, inputs, outputs):
+        """Pipelined end-to-end form of ``solve`` for a sequence of energy
+        points: ``inputs[k]`` = (a, b) and ``outputs[k]`` = (x_a, x_b) are
+        HostWindow pairs of this rank (the blocks it reads / owns).  Energy
+        k+1's window is copied into a second device input slot while energy k
+        solves, energy k's owned outputs are copied to the host from a second
+        device output slot while energy k+1 solves (the multi-GPU analogue of
+        HostEnergySweep); energy 0 loads whole.  Needs two more full-size
+        input and output sets on the device: raises torch.OutOfMemoryError
+        when they do not fit (callers fall back to ``solve(host_in,
+        host_out)`` per energy).  One partition per rank only."""
+        if self._runner is not None:
+            raise ValueError("solve_energies: one partition per rank only")
+        if len(inputs) != len(outputs):
+            raise ValueError("inputs and outputs differ in length")
+        if not inputs:
+            return 0
+        A, B = self.A, self.B
+        dev = A.device
+        if getattr(self, "_slot1", None) is None:
+            mk = lambda: DeviceBta.empty(A.n, A.b, A.a, dev, zero=False)  # noqa: E731
+            self._slot1 = ((mk(), mk() if B is not None else None), (mk(), mk() if B is not None else None))
+            self._h2d, self._d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ins = [(A, B), self._slot1[0]]
+        outs = [self.out, self._slot1[1]]
+        main = torch.cuda.current_stream(dev)
+        h2d, d2h = self._h2d, self._d2h
+        in_free, out_free = [None, None], [None, None]
+
+        def load(win, slot):
+            with torch.cuda.stream(h2d):
+                if in_free[slot] is not None:
+                    h2d.wait_event(in_free[slot])
+                for w, D in zip(win, ins[slot]):
+                    if w is not None and D is not None:
+                        w.copy_to(D)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+            return ev
+
+        h2d.wait_stream(main)
+        d2h.wait_stream(main)
+        ready = load(inputs[0], 0)
+        try:
+            for k in range(len(inputs)):
+                s = k & 1
+                nxt = load(inputs[k + 1], s ^ 1) if k + 1 < len(inputs) else None
+                main.wait_event(ready)
+                if out_free[s] is not None:
+                    main.wait_event(out_free[s])
+                self.A, self.B = ins[s]
+                self.out = outs[s]
+                self.solve()
+                done = torch.cuda.Event()
+                done.record(main)
+                in_free[s] = done
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(done)
+                    for w, X in zip(outputs[k], outs[s]):
+                        if w is not None and X is not None:
+                            w.fill_from(X, non_blocking=True, tip=self.rank == 0)
+                    ev = torch.cuda.Event()
+                    ev.record(d2h)
+                out_free[s] = ev
+                ready = nxt
+        finally:
+            self.A, self.B = ins[0]
+            self.out = outs[0]
+        main.wait_stream(d2h)
+        main.wait_stream(h2d)
+        return len(inputs)
 
     def _copy_separators(self, host_in):
         """Couplings at the other partitions' boundaries (the reduced system

@@ -71,6 +71,19 @@ def _rank(rank, world, port, n, b, a, q):
                         assert torch.equal(g_, r_)
                     elif r_.numel():
                         assert torch.linalg.norm(g_ - r_) <= 1e-12 * torch.linalg.norm(r_)
+        # pipelined end-to-end form (DistSolver.solve_energies): 3 energies,
+        # each one's owned outputs in its own host windows
+        outs = [(bs.HostWindow(n, b, a, lo, hi), bs.HostWindow(n, b, a, lo, hi)) for _ in range(3)]
+        s.solve_energies([win] * 3, outs)
+        torch.cuda.synchronize()
+        for H2 in outs:
+            for side, (R, H) in enumerate(zip(ref, H2)):
+                got = (H.diag, H.arrow_row, H.lower, H.upper) + ((H.tip,) if rank == 0 else ())
+                for g_, r_ in zip(got, R):
+                    if side == 0:
+                        assert torch.equal(g_, r_)
+                    elif r_.numel():
+                        assert torch.linalg.norm(g_ - r_) <= 1e-12 * torch.linalg.norm(r_)
         dist.barrier()
         q.put((rank, err, kinds, None))
         dist.destroy_process_group()
